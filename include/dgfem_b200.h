@@ -1,0 +1,298 @@
+/*
+ * dgfem_b200.h -- C-ABI of the B200-native interior-penalty DG assembly.
+ *
+ * This is the drop-in boundary for the reference library's hot path
+ * `dgfem::assemble_all` (/root/reference/proj/src/assembly.cpp:725-737) followed by
+ * `DgSystem::stiffness()` (assembly.cpp:508-510): mesh + reference tables + coefficients +
+ * penalty parameters in, block-sparse stiffness K = (D + C) + R and load vector F out.
+ *
+ * Every signature uses plain pointers, sizes and POD structs (no C++ or torch types), so the
+ * reference's C++ code (or any FFI) can bind it directly; INTEGRATION.md shows the binding.
+ *
+ * Status codes: 0 = success, otherwise 1 + the numeric value of the reference's
+ * `dgfem::ErrorCode` enumerator (errors.hpp:9-27), so the C++ wrapper can rethrow
+ * `dgfem::Error(code, message, detail)` 1:1.  CUDA runtime failures use DGB_STATUS_CUDA.
+ * The message and the `detail` index of the last failure on the calling thread are available
+ * from dgb_last_error_message()/dgb_last_error_detail().
+ *
+ * Arrays that describe a mesh, tables or outputs are either all HOST pointers (functions whose
+ * name contains `host`, and the mesh/reference builders) or all DEVICE pointers (dgb_assemble,
+ * dgb_spmv, dgb_bsr_pattern); each function says which.
+ */
+#ifndef DGFEM_B200_H
+#define DGFEM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---------------------------------------------------------------- status codes */
+/* 1 + dgfem::ErrorCode (errors.hpp:9-27), in declaration order. */
+enum dgb_status {
+  DGB_OK = 0,
+  DGB_STATUS_INVALID_TOPOLOGY = 1,
+  DGB_STATUS_INVALID_BOUNDARY_SPEC = 2,
+  DGB_STATUS_NON_MANIFOLD = 3,
+  DGB_STATUS_DEGENERATE_ELEMENT = 4,
+  DGB_STATUS_UNSUPPORTED_DEGREE = 5,
+  DGB_STATUS_INVALID_INDEX = 6,
+  DGB_STATUS_DIMENSION_MISMATCH = 7,
+  DGB_STATUS_SINGULAR_MATRIX = 8,
+  DGB_STATUS_SOLVE_ACCURACY = 9,
+  DGB_STATUS_INFLOW_ON_NEUMANN = 10,
+  DGB_STATUS_NON_POSITIVE_DIFFUSION = 11,
+  DGB_STATUS_INVALID_REACTION = 12,
+  DGB_STATUS_NO_EXACT_SOLUTION = 13,
+  DGB_STATUS_UNKNOWN_PROBLEM = 14,
+  DGB_STATUS_UNKNOWN_METHOD = 15,
+  DGB_STATUS_IO_FAILURE = 16,
+  DGB_STATUS_INVALID_ARGUMENT = 17,
+  DGB_STATUS_CUDA = 100 /* CUDA runtime / launch failure (no reference equivalent) */
+};
+
+/* Name of a status ("InflowOnNeumann", ...), matching dgfem::to_string(ErrorCode)
+ * (errors.cpp:5-27). */
+const char* dgb_status_name(int status);
+/* Message / detail of the last failure on this thread (detail = -1 when none),
+ * mirroring dgfem::Error::what()/detail() (errors.hpp:35-48). */
+const char* dgb_last_error_message(void);
+long long dgb_last_error_detail(void);
+/* Library version string. */
+const char* dgb_version(void);
+
+/* ---------------------------------------------------------------- mesh */
+/* Edge kinds, as dgfem::EdgeKind (mesh.hpp:12), stored as one byte per edge. */
+enum dgb_edge_kind { DGB_EDGE_INTERIOR = 0, DGB_EDGE_DIRICHLET = 1, DGB_EDGE_NEUMANN = 2 };
+
+/* Flat view of dgfem::Mesh (mesh.hpp:37-49). Same conventions: CCW elements; edges are sorted
+ * node pairs (a < b) in lexicographic order; edge_elements = {left, right} with left the lower
+ * element index and right = -1 on the boundary; local edge l of an element joins its local
+ * vertices (l+1)%3 -> (l+2)%3.  Used with host pointers (mesh builders) and with device
+ * pointers (dgb_assemble / dgb_bsr_pattern). */
+typedef struct dgb_mesh_arrays {
+  int32_t n_nodes;
+  int32_t n_elements;
+  int32_t n_edges;
+  int32_t n_interior_edges;     /* count of DGB_EDGE_INTERIOR edges (sizes the BSR pattern) */
+  const double* nodes;          /* [2*n_nodes] x,y interleaved       (Mesh::nodes)          */
+  const int32_t* elements;      /* [3*n_elements]                    (Mesh::elements)       */
+  const int32_t* edges;         /* [2*n_edges] sorted pairs          (Mesh::edges)          */
+  const uint8_t* edge_kind;     /* [n_edges] dgb_edge_kind           (Mesh::edge_kind)      */
+  const int32_t* edge_elements; /* [2*n_edges] left,right            (Mesh::edge_elements)  */
+  const int32_t* element_edges; /* [3*n_elements]                    (Mesh::element_edges)  */
+} dgb_mesh_arrays;
+
+/* Opaque host-side mesh (owns its arrays). */
+typedef struct dgb_mesh dgb_mesh;
+
+/* Replaces dgfem::build_mesh (mesh.hpp:62-65, mesh.cpp:51-151): derives the sorted edge table,
+ * adjacency and boundary classification, reorienting clockwise elements.  Same checks and
+ * error codes: InvalidTopology, DegenerateElement, NonManifold, InvalidBoundarySpec.
+ * All pointers are HOST pointers; boundary lists are node pairs (any order). */
+int dgb_mesh_build(const double* nodes_xy, int32_t n_nodes, const int32_t* elements,
+                   int32_t n_elements, const int32_t* dirichlet_pairs, int32_t n_dirichlet,
+                   const int32_t* neumann_pairs, int32_t n_neumann, dgb_mesh** out);
+
+/* The benchmark meshes (BASELINE.json configs): the unit square cut into n x n cells, each
+ * split along its (0,0)-(1,1) diagonal into two CCW triangles; nodes numbered row-major.
+ * jitter > 0 moves every interior node by independent U[-jitter*h, jitter*h] offsets per
+ * coordinate (h = 1/n; config 3 uses 0.2); permute != 0 applies a Fisher-Yates shuffle to the
+ * element list before the edge table is built (config 4).  neumann_sides is a bit mask of
+ * sides tagged Neumann (1: x=0, 2: x=1, 4: y=0, 8: y=1); the rest is Dirichlet.  The random
+ * stream is splitmix64(seed) (documented in DESIGN.md).  HOST.  Also returns the raw
+ * (pre-build) arrays through dgb_mesh_raw so the reference build_mesh can be fed the same
+ * input. */
+int dgb_mesh_unit_square(int32_t n, double jitter, uint64_t jitter_seed, int32_t permute,
+                         uint64_t permute_seed, int32_t neumann_sides, dgb_mesh** out);
+
+/* Pointers into the mesh's own storage (valid until dgb_mesh_free). */
+int dgb_mesh_view(const dgb_mesh* mesh, dgb_mesh_arrays* out);
+/* The input that produced the mesh: nodes, elements before reorientation, and the boundary
+ * pair lists.  Any pointer may be NULL; counts are always written.  HOST. */
+int dgb_mesh_raw(const dgb_mesh* mesh, const double** nodes, int32_t* n_nodes,
+                 const int32_t** elements, int32_t* n_elements, const int32_t** dirichlet,
+                 int32_t* n_dirichlet, const int32_t** neumann, int32_t* n_neumann);
+void dgb_mesh_free(dgb_mesh* mesh);
+
+/* ---------------------------------------------------------------- reference element */
+/* Flat view of dgfem::ReferenceElement (reference.hpp:22-77) with the layouts of its public
+ * accessors: phi(q,j) = phi[q*nl+j]; dphi(q,j,d) = dphi[(q*nl+j)*2+d];
+ * edge_phi(l,o,q,j) = edge_phi[((l*2+o)*nq_edge+q)*nl+j];
+ * edge_dphi(l,o,q,j,d) = edge_dphi[(((l*2+o)*nq_edge+q)*nl+j)*2+d]. */
+typedef struct dgb_reference_tables {
+  int32_t degree;
+  int32_t n_local;
+  int32_t nq_vol;
+  int32_t nq_edge;
+  const double* vol_x;      /* [nq_vol]  TriangleRule::x (quadrature.hpp:11-16) */
+  const double* vol_y;      /* [nq_vol]  */
+  const double* vol_w;      /* [nq_vol]  weights, sum 1/2 */
+  const double* edge_t;     /* [nq_edge] Gauss1D::t on [0,1] (quadrature.hpp:26-30) */
+  const double* edge_w;     /* [nq_edge] weights, sum 1 */
+  const double* phi;        /* [nq_vol*nl]            */
+  const double* dphi;       /* [nq_vol*nl*2]          */
+  const double* edge_phi;   /* [3*2*nq_edge*nl]       */
+  const double* edge_dphi;  /* [3*2*nq_edge*nl*2]     */
+} dgb_reference_tables;
+
+typedef struct dgb_reference dgb_reference;
+
+/* Replaces dgfem::ReferenceElement(degree, quad_order) (reference.cpp:87-147): orthonormal
+ * Dubiner basis, degree 1..4 (UnsupportedDegree otherwise); quad_order = 0 picks the default
+ * rules (volume exact to 2k+2, k+1 edge points), quad_order > 0 a volume rule of that
+ * exactness and (quad_order+1)/2 edge points.  HOST. */
+int dgb_reference_create(int32_t degree, int32_t quad_order, dgb_reference** out);
+int dgb_reference_view(const dgb_reference* ref, dgb_reference_tables* out);
+void dgb_reference_free(dgb_reference* ref);
+
+/* ---------------------------------------------------------------- coefficients */
+/* Device-evaluable replacement of dgfem::ProblemSpec's std::function callbacks
+ * (problems.hpp:19-68), which cannot cross to the device.  Each field is an enum-tagged
+ * descriptor; oracle/dg_coeffs.h holds the host twins the oracle feeds to the reference. */
+enum dgb_field_kind {
+  DGB_FIELD_CONSTANT = 0,    /* value                                                        */
+  DGB_FIELD_PER_ELEMENT = 1, /* per_element[e] (piecewise constant; config 5)                */
+  DGB_FIELD_FUNCTION = 2     /* analytic family `fn` with parameters p[], evaluated as `mode` */
+};
+/* Analytic families u(x,y) (each with closed-form gradient and Laplacian). */
+enum dgb_function {
+  DGB_FN_SIN_SIN = 1,    /* u = p0 sin(pi x) sin(pi y)                                       */
+  DGB_FN_TANH_LAYER = 2, /* u = 0.5 (1 - tanh((p0 x + p1 y + p2) / p3))                      */
+  DGB_FN_GAUSSIAN = 3,   /* u = exp(-p0 ((x - p1)^2 + (y - p2)^2))                           */
+  DGB_FN_AFFINE = 4,     /* u = p0 + p1 x + p2 y                                             */
+  DGB_FN_STEP_Y = 5      /* u = (y < p0) ? p1 : p2            (value only)                   */
+};
+/* What a DGB_FIELD_FUNCTION field returns. */
+enum dgb_function_mode {
+  DGB_MODE_VALUE = 0,   /* u                                                                 */
+  DGB_MODE_SOURCE = 1,  /* q0 u - q1 lap(u) + q2 du/dx + q3 du/dy  (manufactured source with
+                           constant alpha = q0, eps = q1, b = (q2, q3))                      */
+  DGB_MODE_FLUX_X = 2   /* q1 du/dx  (conormal flux through x = const sides)                 */
+};
+typedef struct dgb_scalar_field {
+  int32_t kind;               /* dgb_field_kind  */
+  int32_t fn;                 /* dgb_function    */
+  int32_t mode;               /* dgb_function_mode */
+  int32_t pad_;
+  double value;               /* DGB_FIELD_CONSTANT */
+  double p[4];                /* function parameters */
+  double q[4];                /* mode parameters     */
+  const double* per_element;  /* DGB_FIELD_PER_ELEMENT: [n_elements] (device pointer for
+                                 dgb_assemble, host pointer for the host entry points) */
+} dgb_scalar_field;
+
+enum dgb_vector_kind {
+  DGB_VEC_CONSTANT = 0, /* b = (p0, p1)                                                     */
+  DGB_VEC_AFFINE = 1,   /* b = (p0 + p2 x + p3 y, p1 + p4 x + p5 y)         (config 3)        */
+  DGB_VEC_TRIG = 2      /* b = (cos(p0 y), sin(p1 x))                        (config 5)        */
+};
+typedef struct dgb_vector_field {
+  int32_t kind;
+  int32_t pad_;
+  double p[6];
+} dgb_vector_field;
+
+/* The coefficient set of ProblemSpec (problems.hpp:52-68) that assemble_all reads.
+ * diffusion and linear_reaction must be CONSTANT or PER_ELEMENT (every problem in the
+ * reference registry and every BASELINE config is).  For a PER_ELEMENT diffusion the edge
+ * value is 0.5 (eps_L + eps_R) on interior edges and eps_K on boundary edges (SURVEY.md §8
+ * "Config-5 policy"). */
+typedef struct dgb_problem {
+  dgb_scalar_field diffusion;       /* eps   > 0 */
+  dgb_vector_field advection;       /* b         */
+  dgb_scalar_field linear_reaction; /* alpha >= 0 */
+  dgb_scalar_field source;          /* f         */
+  dgb_scalar_field dirichlet;       /* gD        */
+  dgb_scalar_field neumann;         /* gN        */
+} dgb_problem;
+
+/* ---------------------------------------------------------------- parameters */
+/* dgfem::DgMethod (assembly.hpp:15) and dgfem::DgParameters (assembly.hpp:29-35). */
+enum dgb_method { DGB_SIPG = 0, DGB_NIPG = 1, DGB_IIPG = 2 };
+/* What to do when b.n < -tol at a point of a Neumann edge (assembly.cpp:386-397). */
+enum dgb_neumann_inflow {
+  DGB_INFLOW_ERROR = 0, /* reference behaviour: InflowOnNeumann, detail = lowest edge index   */
+  DGB_INFLOW_DROP = 1   /* Neumann boundary treated as outflow-only: no convection terms on it */
+};
+typedef struct dgb_params {
+  int32_t method;         /* dgb_method            */
+  int32_t degree;
+  double kappa;           /* -1 SIPG, +1 NIPG, 0 IIPG */
+  double sigma_interior;
+  double sigma_boundary;
+  int32_t neumann_inflow; /* dgb_neumann_inflow    */
+  int32_t pad_;
+} dgb_params;
+
+/* Replaces dgfem::set_parameters (assembly.cpp:483-506): per-method defaults,
+ * sigma_boundary = 2 sigma_interior; InvalidArgument for degree < 1. */
+int dgb_set_parameters(int32_t method, int32_t degree, dgb_params* out);
+
+/* ---------------------------------------------------------------- BSR output */
+/* Block-sparse stiffness: block row e holds the diagonal block and one block per interior
+ * edge neighbour, block columns sorted ascending, nl x nl row-major FP64 blocks.  Expands 1:1
+ * to the reference's stiffness() CSR (sorted columns, explicit zeros included). */
+typedef struct dgb_bsr {
+  int32_t n_block_rows;   /* = n_elements */
+  int32_t block_dim;      /* = n_local    */
+  int64_t nnzb;           /* = n_elements + 2 * n_interior_edges */
+  int32_t* row_ptr;       /* [n_block_rows + 1] */
+  int32_t* col;           /* [nnzb]             */
+  double* val;            /* [nnzb * block_dim * block_dim] */
+} dgb_bsr;
+
+/* Number of BSR blocks for a mesh. */
+int64_t dgb_bsr_nnzb(int32_t n_elements, int32_t n_interior_edges);
+
+/* ---------------------------------------------------------------- device plan */
+/* A plan owns the device-resident reference-contraction tensors derived from one set of
+ * reference tables, plus scratch (scan partials, error word).  Not re-entrant across host
+ * threads; results are bitwise reproducible run to run (no floating-point atomics). */
+typedef struct dgb_plan dgb_plan;
+
+/* tables: HOST pointers (e.g. dgb_reference_view, or the reference's own ReferenceElement
+ * accessors).  device: CUDA device ordinal.  Degrees 1..4. */
+int dgb_plan_create(const dgb_reference_tables* tables, int32_t device, dgb_plan** out);
+void dgb_plan_destroy(dgb_plan* plan);
+
+/* Full assembly on `stream` (a cudaStream_t; NULL = legacy default stream): writes the BSR
+ * pattern and values of K = (D + C) + R into `out` (DEVICE buffers sized by dgb_bsr_nnzb) and
+ * F into rhs[n_elements * n_local] (DEVICE).  mesh and the per-element pointers of problem are
+ * DEVICE pointers.  Asynchronous: returns after enqueueing; call dgb_plan_status to wait
+ * and collect InflowOnNeumann (only possible with DGB_INFLOW_ERROR and Neumann edges). */
+int dgb_assemble(dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_problem* problem,
+                 const dgb_params* params, dgb_bsr* out, double* rhs, void* stream);
+
+/* Waits for the plan's last dgb_assemble on `stream` and returns its status
+ * (DGB_STATUS_INFLOW_ON_NEUMANN with detail = lowest offending edge, as the reference's
+ * deterministic chunk merge reports it). */
+int dgb_plan_status(dgb_plan* plan, void* stream);
+
+/* Measurement hook: the next dgb_assemble calls record `start` / `stop` (cudaEvent_t, NULL
+ * to disable) on their stream immediately before / after the block-row kernel, so a caller
+ * can time that kernel with CUDA events on the launching stream (bench.py's roofline). */
+int dgb_plan_set_kernel_events(dgb_plan* plan, void* start, void* stop);
+
+/* Kernel launches one dgb_assemble call issues (for bench.py's gpu_launches count). */
+int32_t dgb_assemble_launch_count(void);
+
+/* y = K x with the BSR from dgb_assemble (DEVICE pointers), on `stream`.  Replaces
+ * dgfem::matvec(stiffness(), x) (sparse.cpp:116-129). */
+int dgb_spmv(const dgb_bsr* a, const double* x, double* y, void* stream);
+
+/* One-shot drop-in for `assemble_all(mesh, ref, problem, params)` + `stiffness()` with HOST
+ * buffers in and out: uploads the mesh, tables and per-element coefficients, assembles on
+ * `device`, downloads K (BSR) and F.  Output buffers are caller-allocated host memory sized
+ * by dgb_bsr_nnzb.  Synchronous; returns the reference's error code on failure. */
+int dgb_assemble_all_host(const dgb_mesh_arrays* mesh, const dgb_reference_tables* tables,
+                          const dgb_problem* problem, const dgb_params* params, int32_t device,
+                          dgb_bsr* out, double* rhs);
+
+#ifdef __cplusplus
+} /* extern "C" */
+#endif
+
+#endif /* DGFEM_B200_H */

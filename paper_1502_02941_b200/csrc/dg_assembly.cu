@@ -1,0 +1,1100 @@
+// dg_assembly.cu -- B200 (sm_100a) assembly of the interior-penalty DG system.
+//
+// Replaces the reference hot path dgfem::assemble_all + DgSystem::stiffness
+// (/root/reference/proj/src/assembly.cpp:725-737, :508-510).  Design:
+//
+//  * Gather formulation: every element writes only its own BSR block
+//    row -- diagonal block plus one block per interior-edge neighbour, block columns sorted --
+//    and its own RHS slice.  Each interior face is evaluated from both sides; no atomics, no
+//    triplet sort, bitwise reproducible.
+//  * Reference-tensor contraction: on affine triangles with element-constant eps / alpha
+//    every block is a short linear combination of element-independent nl x nl tensors built
+//    once per plan from the reference tables (volume Gram / mass / transport tensors,
+//    per-(local edge, neighbour local edge) face tensors).  Coefficients that depend on the
+//    element (geometry, edge normals, penalties, per-point upwind weights, per-point source
+//    and boundary data) are computed per element in phase A and combined in phase B.
+//  * Decisions that select terms (upwind side per point, exact-zero flux skip, inflow
+//    tolerance gate, outward normal) use unfused IEEE operations (__dmul_rn/__dadd_rn) on
+//    the reference's expressions so they fall the same way as on the CPU.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include <cub/device/device_scan.cuh>
+
+#include "common.hpp"
+
+namespace dgb {
+
+// ------------------------------------------------------------------------------------------
+// layouts
+// ------------------------------------------------------------------------------------------
+constexpr int kTensorQ = 64;  // max volume points supported
+constexpr int kMaxQE = 8;     // max edge points supported
+
+// Offsets (in doubles) of the reference-contraction tensors in the plan's device buffer.
+// Every tensor is nl x nl row-major [i][j]; the per-point tables are [.][i].
+struct Layout {
+  int S;     // 3 tensors: S00, S01 + S10, S11      S^ab_ij = sum_q w_q d_a phi_qj d_b phi_qi
+  int M;     // 1: sum_q w_q phi_qi phi_qj
+  int T;     // 2: T^a_ij = sum_q w_q phi_qi d_a phi_qj
+  int TA;    // 4: TA^{a,c}_ij = sum_q w_q xhat_qc phi_qi d_a phi_qj   (affine velocity)
+  int TQ;    // 2 nqv: TQ^{q,a}_ij = phi_qi d_a phi_qj                  (pointwise velocity)
+  int Q;     // 6: Q^{l,a}_ij = sum_p w_p phi^l_pi d_a phi^l_pj        (face consistency)
+  int U;     // 3 nqe: U^{l,p}_ij = phi^l_pi phi^l_pj                  (face penalty/upwind)
+  int V;     // 9 nqe: V^{l,m,p}_ij = phi^l_pi phi^m_(n-1-p)j          (cross penalty/upwind)
+  int Y;     // 18: Y^{l,m,a}_ij = sum_p w_p phi^l_pi d_a phi^m_(n-1-p)j
+  int Z;     // 18: Z^{l,m,a}_ij = sum_p w_p d_a phi^l_pi phi^m_(n-1-p)j
+  int PHI;   // nqv x nl volume basis
+  int EPHI;  // 3 nqe x nl edge traces (canonical orientation)
+  int EDPHI; // 3 nqe 2 x nl edge gradients
+  int VX, VY, VW, ET, EW;  // quadrature points / weights
+  int total;
+};
+
+// Offsets (in doubles) inside one element's coefficient record (shared memory).
+struct Rec {
+  int cD, cR, cC, cCA, cCQ, cF, cW, cU, cY, cZ, cV, cG, cH, gam, size;
+};
+
+constexpr int kMeta = 16;  // ints per element: see phase A0
+
+struct KParams {
+  // mesh (device)
+  const double* nodes;
+  const int32_t* elements;
+  const uint8_t* edge_kind;
+  const int32_t* edge_elements;
+  const int32_t* element_edges;
+  int32_t n_elements;
+  // problem (by value; per-element pointers are device pointers)
+  dgb_problem prob;
+  double kappa, sigma_i, sigma_b;
+  int32_t drop_neumann;
+  // tables
+  const double* tens;
+  Layout L;
+  Rec R;
+  int nl, nqv, nqe;
+  int tile;
+  // outputs
+  const int32_t* row_ptr;
+  int32_t* col;
+  double* val;
+  double* rhs;
+  int32_t* err_edge;
+};
+
+// ------------------------------------------------------------------------------------------
+// device helpers
+// ------------------------------------------------------------------------------------------
+#define FMUL __dmul_rn
+#define FADD __dadd_rn
+#define FSUB __dsub_rn
+#define FDIV __ddiv_rn
+
+// sqrt(x^2 + y^2) with a double-double Newton correction (within ~0.5 ulp; glibc's hypot
+// itself is not correctly rounded).
+__device__ __forceinline__ double hypot_dd(double x, double y) {
+  x = fabs(x);
+  y = fabs(y);
+  const double x2 = FMUL(x, x), y2 = FMUL(y, y);
+  const double ex = fma(x, x, -x2), ey = fma(y, y, -y2);
+  const double s = FADD(x2, y2);
+  const double bb = FSUB(s, x2);
+  const double es = FADD(FSUB(x2, FSUB(s, bb)), FSUB(y2, bb));
+  const double lo = es + ex + ey;
+  const double r = __dsqrt_rn(s);
+  const double d = fma(r, r, -s) - lo;
+  return r - d / (2.0 * r);
+}
+
+__device__ __forceinline__ void family(int fn, const double* p, double x, double y, double& u,
+                                       double& ux, double& uy, double& lap) {
+  constexpr double pi = 3.14159265358979323846;
+  switch (fn) {
+    case DGB_FN_SIN_SIN: {
+      double sx, cx, sy, cy;
+      sincos(pi * x, &sx, &cx);
+      sincos(pi * y, &sy, &cy);
+      u = p[0] * (sx * sy);
+      ux = p[0] * (pi * cx * sy);
+      uy = p[0] * (pi * sx * cy);
+      lap = -2.0 * pi * pi * u;
+      return;
+    }
+    case DGB_FN_TANH_LAYER: {
+      const double s = (p[0] * x + p[1] * y + p[2]) / p[3];
+      const double t = tanh(s);
+      const double c = cosh(s);
+      const double sech2 = 1.0 / (c * c);
+      const double gx = p[0] / p[3], gy = p[1] / p[3];
+      u = 0.5 * (1.0 - t);
+      ux = -0.5 * sech2 * gx;
+      uy = -0.5 * sech2 * gy;
+      lap = t * sech2 * (gx * gx + gy * gy);
+      return;
+    }
+    case DGB_FN_GAUSSIAN: {
+      const double dx = x - p[1], dy = y - p[2];
+      const double r2 = dx * dx + dy * dy;
+      const double v = exp(-p[0] * r2);
+      u = v;
+      ux = -2.0 * p[0] * dx * v;
+      uy = -2.0 * p[0] * dy * v;
+      lap = (4.0 * p[0] * p[0] * r2 - 4.0 * p[0]) * v;
+      return;
+    }
+    case DGB_FN_AFFINE:
+      u = p[0] + p[1] * x + p[2] * y;
+      ux = p[1];
+      uy = p[2];
+      lap = 0.0;
+      return;
+    case DGB_FN_STEP_Y:
+      u = (y < p[0]) ? p[1] : p[2];
+      ux = uy = lap = 0.0;
+      return;
+    default:
+      u = ux = uy = lap = nan("");
+  }
+}
+
+// CONSTANT / FUNCTION scalar field at a point (device twin of oracle/dg_coeffs.h).
+__device__ __forceinline__ double scalar_point(const dgb_scalar_field& f, double x, double y) {
+  if (f.kind == DGB_FIELD_CONSTANT) return f.value;
+  double u, ux, uy, lap;
+  family(f.fn, f.p, x, y, u, ux, uy, lap);
+  switch (f.mode) {
+    case DGB_MODE_VALUE: return u;
+    case DGB_MODE_SOURCE: return f.q[0] * u - f.q[1] * lap + f.q[2] * ux + f.q[3] * uy;
+    case DGB_MODE_FLUX_X: return f.q[1] * ux;
+    default: return nan("");
+  }
+}
+
+__device__ __forceinline__ double scalar_element(const dgb_scalar_field& f, int e) {
+  return f.kind == DGB_FIELD_PER_ELEMENT ? __ldg(f.per_element + e) : f.value;
+}
+
+// Velocity at a point; the affine form keeps the reference's unfused evaluation order.
+__device__ __forceinline__ void velocity(const dgb_vector_field& b, double x, double y,
+                                         double& bx, double& by) {
+  switch (b.kind) {
+    case DGB_VEC_CONSTANT:
+      bx = b.p[0];
+      by = b.p[1];
+      return;
+    case DGB_VEC_AFFINE:
+      bx = FADD(FADD(b.p[0], FMUL(b.p[2], x)), FMUL(b.p[3], y));
+      by = FADD(FADD(b.p[1], FMUL(b.p[4], x)), FMUL(b.p[5], y));
+      return;
+    case DGB_VEC_TRIG:
+      bx = cos(FMUL(b.p[0], y));
+      by = sin(FMUL(b.p[1], x));
+      return;
+    default:
+      bx = by = nan("");
+  }
+}
+
+struct Geo {
+  double B00, B01, B10, B11, G00, G01, G10, G11, det, ox, oy;
+};
+
+// element_geometry (mesh.cpp:212-230), unfused.
+__device__ __forceinline__ Geo element_geo(const double* __restrict__ nodes,
+                                           const int32_t* v) {
+  Geo g;
+  const double2 p0 = __ldg(reinterpret_cast<const double2*>(nodes) + v[0]);
+  const double2 p1 = __ldg(reinterpret_cast<const double2*>(nodes) + v[1]);
+  const double2 p2 = __ldg(reinterpret_cast<const double2*>(nodes) + v[2]);
+  g.B00 = FSUB(p1.x, p0.x);
+  g.B01 = FSUB(p2.x, p0.x);
+  g.B10 = FSUB(p1.y, p0.y);
+  g.B11 = FSUB(p2.y, p0.y);
+  g.det = FSUB(FMUL(g.B00, g.B11), FMUL(g.B01, g.B10));
+  g.G00 = FDIV(g.B11, g.det);
+  g.G01 = FDIV(-g.B10, g.det);
+  g.G10 = FDIV(-g.B01, g.det);
+  g.G11 = FDIV(g.B00, g.det);
+  g.ox = p0.x;
+  g.oy = p0.y;
+  return g;
+}
+
+// Meta ints per element (shared memory):
+//  0: n_blocks   1: diagonal slot   2..4: slot of local edge l (-1: boundary)
+//  5..7: neighbour local edge lf    8..10: edge kind    11..13: vertices    14: element
+enum { M_NB = 0, M_DIAG = 1, M_SLOT = 2, M_LF = 5, M_KIND = 8, M_VERT = 11 };
+constexpr int kGeo = 13;  // doubles per element: B(4) G(4) det ox oy eps alpha
+
+// ------------------------------------------------------------------------------------------
+// pattern: row_ptr = scan(1 + #interior edges); also resets the error word
+// ------------------------------------------------------------------------------------------
+__global__ void count_blocks_kernel(const uint8_t* __restrict__ edge_kind,
+                                    const int32_t* __restrict__ element_edges, int32_t n,
+                                    int32_t* __restrict__ row_ptr, int32_t* err_edge) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e == 0) {
+    row_ptr[0] = 0;
+    *err_edge = INT_MAX;
+  }
+  if (e >= n) return;
+  int c = 1;
+#pragma unroll
+  for (int l = 0; l < 3; ++l) {
+    c += __ldg(edge_kind + __ldg(element_edges + 3 * e + l)) == DGB_EDGE_INTERIOR;
+  }
+  row_ptr[e + 1] = c;
+}
+
+// ------------------------------------------------------------------------------------------
+// the block-row kernel
+// ------------------------------------------------------------------------------------------
+template <int NL>
+__global__ void __launch_bounds__(256) assemble_kernel(const __grid_constant__ KParams P) {
+  extern __shared__ double smem[];
+  constexpr int NL2 = NL * NL;
+  const int TE = P.tile;
+  const int e0 = blockIdx.x * TE;
+  const int ne = min(TE, P.n_elements - e0);
+  const int nqv = P.nqv, nqe = P.nqe;
+  const Rec& R = P.R;
+  const Layout& L = P.L;
+  const double* __restrict__ tens = P.tens;
+
+  double* rec = smem;                         // TE * R.size
+  double* geo = rec + TE * R.size;            // TE * kGeo
+  int* meta = reinterpret_cast<int*>(geo + TE * kGeo);  // TE * kMeta
+  int* blk = meta + TE * kMeta;               // 4 * TE: (element << 3) | (kind + 1)
+  int* s_nblk = blk + 4 * TE;
+
+  // ---- A0: per element: geometry, neighbours, sorted block columns -----------------------
+  for (int el = threadIdx.x; el < ne; el += blockDim.x) {
+    const int e = e0 + el;
+    int* m = meta + el * kMeta;
+    int v[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) v[k] = __ldg(P.elements + 3 * e + k);
+    const Geo g = element_geo(P.nodes, v);
+    double* gg = geo + el * kGeo;
+    gg[0] = g.B00; gg[1] = g.B01; gg[2] = g.B10; gg[3] = g.B11;
+    gg[4] = g.G00; gg[5] = g.G01; gg[6] = g.G10; gg[7] = g.G11;
+    gg[8] = g.det; gg[9] = g.ox; gg[10] = g.oy;
+    const double eps = scalar_element(P.prob.diffusion, e);
+    const double alpha = scalar_element(P.prob.linear_reaction, e);
+    gg[11] = eps;
+    gg[12] = alpha;
+    int cols[4], kinds[4];
+    int nb = 0;
+    cols[nb] = e;
+    kinds[nb++] = -1;
+#pragma unroll
+    for (int l = 0; l < 3; ++l) {
+      m[M_VERT + l] = v[l];
+      const int edge = __ldg(P.element_edges + 3 * e + l);
+      const int kind = __ldg(P.edge_kind + edge);
+      m[M_KIND + l] = kind;
+      m[M_SLOT + l] = -1;
+      if (kind == DGB_EDGE_INTERIOR) {
+        const int2 lr = __ldg(reinterpret_cast<const int2*>(P.edge_elements) + edge);
+        cols[nb] = lr.x == e ? lr.y : lr.x;
+        kinds[nb++] = l;
+      }
+    }
+    // sort block columns ascending (CSR order of the reference's stiffness())
+    for (int a = 1; a < nb; ++a) {
+      for (int b = a; b > 0 && cols[b - 1] > cols[b]; --b) {
+        int t = cols[b]; cols[b] = cols[b - 1]; cols[b - 1] = t;
+        t = kinds[b]; kinds[b] = kinds[b - 1]; kinds[b - 1] = t;
+      }
+    }
+    m[M_NB] = nb;
+    const int base = __ldg(P.row_ptr + e);
+    for (int s = 0; s < nb; ++s) {
+      P.col[base + s] = cols[s];
+      if (kinds[s] < 0) m[M_DIAG] = s; else m[M_SLOT + kinds[s]] = s;
+    }
+    // volume coefficients that are constant per element
+    double* r = rec + el * R.size;
+    const double de = g.det * eps;
+    r[R.cD + 0] = de * (g.G00 * g.G00 + g.G10 * g.G10);
+    r[R.cD + 1] = de * (g.G00 * g.G01 + g.G10 * g.G11);
+    r[R.cD + 2] = de * (g.G01 * g.G01 + g.G11 * g.G11);
+    r[R.cR] = g.det * alpha;
+    const dgb_vector_field& b = P.prob.advection;
+    if (b.kind == DGB_VEC_CONSTANT) {
+      r[R.cC + 0] = g.det * (g.G00 * b.p[0] + g.G10 * b.p[1]);
+      r[R.cC + 1] = g.det * (g.G01 * b.p[0] + g.G11 * b.p[1]);
+    } else if (b.kind == DGB_VEC_AFFINE) {
+      // b(o + B xhat) = (c + A o) + (A B) xhat
+      const double bo0 = b.p[0] + b.p[2] * g.ox + b.p[3] * g.oy;
+      const double bo1 = b.p[1] + b.p[4] * g.ox + b.p[5] * g.oy;
+      const double AB00 = b.p[2] * g.B00 + b.p[3] * g.B10, AB01 = b.p[2] * g.B01 + b.p[3] * g.B11;
+      const double AB10 = b.p[4] * g.B00 + b.p[5] * g.B10, AB11 = b.p[4] * g.B01 + b.p[5] * g.B11;
+      r[R.cC + 0] = g.det * (g.G00 * bo0 + g.G10 * bo1);
+      r[R.cC + 1] = g.det * (g.G01 * bo0 + g.G11 * bo1);
+      r[R.cCA + 0] = g.det * (g.G00 * AB00 + g.G10 * AB10);  // a = 0, c = 0
+      r[R.cCA + 1] = g.det * (g.G00 * AB01 + g.G10 * AB11);  // a = 0, c = 1
+      r[R.cCA + 2] = g.det * (g.G01 * AB00 + g.G11 * AB10);  // a = 1, c = 0
+      r[R.cCA + 3] = g.det * (g.G01 * AB01 + g.G11 * AB11);  // a = 1, c = 1
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int n = 0;
+    for (int el = 0; el < ne; ++el) {
+      const int* m = meta + el * kMeta;
+      for (int s = 0; s < m[M_NB]; ++s) {
+        int kind = -1;
+        if (s != m[M_DIAG]) {
+          for (int l = 0; l < 3; ++l) if (m[M_SLOT + l] == s) kind = l;
+        }
+        blk[n++] = (el << 3) | (kind + 1);
+      }
+    }
+    *s_nblk = n;
+  }
+
+  // ---- A1: per (element, local edge): face coefficients ----------------------------------
+  for (int t = threadIdx.x; t < 3 * ne; t += blockDim.x) {
+    const int el = t / 3, l = t - 3 * el;
+    const int e = e0 + el;
+    int* m = meta + el * kMeta;
+    const double* gg = geo + el * kGeo;
+    double* r = rec + el * R.size;
+    const int kind = m[M_KIND + l];
+    const int va = m[M_VERT + (l + 1) % 3], vb = m[M_VERT + (l + 2) % 3];
+    const int o = va < vb ? 0 : 1;  // make_side orientation (assembly.cpp:125-126)
+    const int na = min(va, vb), nb_ = max(va, vb);
+    const double2 A = __ldg(reinterpret_cast<const double2*>(P.nodes) + na);
+    const double2 B = __ldg(reinterpret_cast<const double2*>(P.nodes) + nb_);
+    // edge_geometry (mesh.cpp:232-257); outward normal of e from its orientation
+    const double dx = FSUB(B.x, A.x), dy = FSUB(B.y, A.y);
+    const double h = hypot_dd(dx, dy);
+    const double tx = FDIV(dx, h), ty = FDIV(dy, h);
+    const double nx = o == 0 ? ty : -ty, ny = o == 0 ? -tx : tx;
+    const double gam0 = gg[4] * nx + gg[6] * ny;  // (G^T n)_0
+    const double gam1 = gg[5] * nx + gg[7] * ny;  // (G^T n)_1
+    r[R.gam + 2 * l] = gam0;
+    r[R.gam + 2 * l + 1] = gam1;
+    double* cW = r + R.cW + 2 * l;
+    double* cU = r + R.cU + l * nqe;
+    double* cY = r + R.cY + 2 * l;
+    double* cZ = r + R.cZ + 2 * l;
+    double* cV = r + R.cV + l * nqe;
+    double* cG = r + R.cG + l * nqe;
+    double* cH = r + R.cH + l * nqe;
+    const double* et = tens + L.ET;
+    const double* ew = tens + L.EW;
+    const dgb_vector_field& bf = P.prob.advection;
+
+    if (kind == DGB_EDGE_INTERIOR) {
+      const int2 lr = __ldg(reinterpret_cast<const int2*>(P.edge_elements) +
+                            __ldg(P.element_edges + 3 * e + l));
+      const int f = lr.x == e ? lr.y : lr.x;
+      int vf[3];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) vf[k] = __ldg(P.elements + 3 * f + k);
+      int lf = 0;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) if (vf[k] != va && vf[k] != vb) lf = k;
+      m[M_LF + l] = lf;
+      const Geo gf = element_geo(P.nodes, vf);
+      double eps_e = gg[11];
+      if (P.prob.diffusion.kind == DGB_FIELD_PER_ELEMENT) {
+        const double ef = __ldg(P.prob.diffusion.per_element + f);
+        eps_e = e < f ? 0.5 * (gg[11] + ef) : 0.5 * (ef + gg[11]);
+      }
+      const double base = 0.5 * h * eps_e;  // avg * h * eps
+      cW[0] = base * gam0;
+      cW[1] = base * gam1;
+      cY[0] = -base * (gf.G00 * nx + gf.G10 * ny);
+      cY[1] = -base * (gf.G01 * nx + gf.G11 * ny);
+      cZ[0] = -P.kappa * base * gam0;
+      cZ[1] = -P.kappa * base * gam1;
+      const double sh = FDIV(P.sigma_i, h);
+      for (int q = 0; q < nqe; ++q) {
+        const int p = o == 0 ? q : nqe - 1 - q;
+        const double w = FMUL(ew[q], h);
+        const double pen = FMUL(sh, FMUL(w, eps_e));
+        double up = 0.0;
+        if (bf.kind == DGB_VEC_CONSTANT) {
+          const double fl = FADD(FMUL(bf.p[0], nx), FMUL(bf.p[1], ny));
+          if (fl < 0.0) up = FMUL(w, fl);
+        } else {
+          const double px = FADD(A.x, FMUL(et[q], dx)), py = FADD(A.y, FMUL(et[q], dy));
+          double bx, by;
+          velocity(bf, px, py, bx, by);
+          const double fl = FADD(FMUL(bx, nx), FMUL(by, ny));
+          if (fl < 0.0) up = FMUL(w, fl);
+        }
+        cU[p] = pen - up;   // diag: penalty + (-w b.n_e) on inflow points
+        cV[p] = up - pen;   // off:  -penalty + (w b.n_e) on inflow points
+        cG[p] = 0.0;
+        cH[p] = 0.0;
+      }
+    } else {
+      m[M_LF + l] = 0;
+      cY[0] = cY[1] = cZ[0] = cZ[1] = 0.0;
+      for (int q = 0; q < nqe; ++q) cV[q] = 0.0;
+      const double eps_e = gg[11];
+      // boundary convection gate (assembly.cpp:383-401)
+      double flq[kMaxQE], pxq[kMaxQE], pyq[kMaxQE];
+      bool any_inflow = false;
+      for (int q = 0; q < nqe; ++q) {
+        pxq[q] = FADD(A.x, FMUL(et[q], dx));
+        pyq[q] = FADD(A.y, FMUL(et[q], dy));
+        double bx, by;
+        velocity(bf, pxq[q], pyq[q], bx, by);
+        flq[q] = FADD(FMUL(bx, nx), FMUL(by, ny));
+        const double tol = 1e-12 * fmax(1.0, hypot_dd(bx, by));
+        if (flq[q] < -tol) any_inflow = true;
+      }
+      if (kind == DGB_EDGE_NEUMANN) {
+        cW[0] = cW[1] = 0.0;
+        if (any_inflow && !P.drop_neumann) {
+          atomicMin(P.err_edge, __ldg(P.element_edges + 3 * e + l));
+        }
+        for (int q = 0; q < nqe; ++q) {
+          const int p = o == 0 ? q : nqe - 1 - q;
+          const double w = FMUL(ew[q], h);
+          cU[p] = 0.0;
+          cG[p] = FMUL(w, scalar_point(P.prob.neumann, pxq[q], pyq[q]));
+          cH[p] = 0.0;
+        }
+      } else {  // Dirichlet
+        const double base = h * eps_e;  // avg = 1
+        cW[0] = base * gam0;
+        cW[1] = base * gam1;
+        const double sh = FDIV(P.sigma_b, h);
+        for (int q = 0; q < nqe; ++q) {
+          const int p = o == 0 ? q : nqe - 1 - q;
+          const double w = FMUL(ew[q], h);
+          const double pen = FMUL(sh, FMUL(w, eps_e));
+          const double gd = scalar_point(P.prob.dirichlet, pxq[q], pyq[q]);
+          const double wgd = w * gd;
+          double win = 0.0;
+          if (any_inflow && flq[q] < 0.0) win = -FMUL(w, flq[q]);
+          cU[p] = pen + win;
+          cG[p] = wgd * (sh * eps_e) + win * gd;
+          cH[p] = wgd * (P.kappa * eps_e);
+        }
+      }
+    }
+  }
+
+  // ---- A2: per (element, volume point): source and pointwise transport coefficients -----
+  const bool pointwise_b = P.prob.advection.kind == DGB_VEC_TRIG;
+  for (int t = threadIdx.x; t < nqv * ne; t += blockDim.x) {
+    const int el = t / nqv, q = t - el * nqv;
+    const int e = e0 + el;
+    const double* gg = geo + el * kGeo;
+    double* r = rec + el * R.size;
+    const double xh = tens[L.VX + q], yh = tens[L.VY + q], wq = tens[L.VW + q];
+    const double px = FADD(FADD(gg[9], FMUL(gg[0], xh)), FMUL(gg[1], yh));
+    const double py = FADD(FADD(gg[10], FMUL(gg[2], xh)), FMUL(gg[3], yh));
+    const dgb_scalar_field& fs = P.prob.source;
+    const double f = fs.kind == DGB_FIELD_PER_ELEMENT ? __ldg(fs.per_element + e)
+                                                      : scalar_point(fs, px, py);
+    r[R.cF + q] = gg[8] * wq * f;
+    if (pointwise_b) {
+      double bx, by;
+      velocity(P.prob.advection, px, py, bx, by);
+      const double dw = gg[8] * wq;
+      r[R.cCQ + 2 * q] = dw * (gg[4] * bx + gg[6] * by);
+      r[R.cCQ + 2 * q + 1] = dw * (gg[5] * bx + gg[7] * by);
+    }
+  }
+  __syncthreads();
+
+  // ---- B: block-row values, streamed in output order ---------------------------------------
+  const int nblk = *s_nblk;
+  const long long vbase = static_cast<long long>(__ldg(P.row_ptr + e0)) * NL2;
+  const int bkind = P.prob.advection.kind;
+  const double kappa = P.kappa;
+  for (int g = threadIdx.x; g < nblk * NL2; g += blockDim.x) {
+    const int bi = g / NL2, k = g - bi * NL2;
+    const int i = k / NL, j = k - i * NL;
+    const int code = blk[bi];
+    const int el = code >> 3, kind = (code & 7) - 1;
+    const double* r = rec + el * R.size;
+    double v;
+    if (kind < 0) {
+      v = r[R.cD] * __ldg(tens + L.S + k);
+      v = fma(r[R.cD + 1], __ldg(tens + L.S + NL2 + k), v);
+      v = fma(r[R.cD + 2], __ldg(tens + L.S + 2 * NL2 + k), v);
+      v = fma(r[R.cR], __ldg(tens + L.M + k), v);
+      if (bkind == DGB_VEC_TRIG) {
+        for (int q = 0; q < 2 * nqv; ++q) v = fma(r[R.cCQ + q], __ldg(tens + L.TQ + q * NL2 + k), v);
+      } else {
+        v = fma(r[R.cC], __ldg(tens + L.T + k), v);
+        v = fma(r[R.cC + 1], __ldg(tens + L.T + NL2 + k), v);
+        if (bkind == DGB_VEC_AFFINE) {
+#pragma unroll
+          for (int a = 0; a < 4; ++a) v = fma(r[R.cCA + a], __ldg(tens + L.TA + a * NL2 + k), v);
+        }
+      }
+      const int kt = j * NL + i;
+#pragma unroll
+      for (int l = 0; l < 3; ++l) {
+#pragma unroll
+        for (int a = 0; a < 2; ++a) {
+          const double* Qla = tens + L.Q + (2 * l + a) * NL2;
+          v = fma(r[R.cW + 2 * l + a], fma(kappa, __ldg(Qla + kt), -__ldg(Qla + k)), v);
+        }
+        for (int p = 0; p < nqe; ++p) {
+          v = fma(r[R.cU + l * nqe + p], __ldg(tens + L.U + (l * nqe + p) * NL2 + k), v);
+        }
+      }
+    } else {
+      const int l = kind;
+      const int lf = meta[el * kMeta + M_LF + l];
+      const int lm = l * 3 + lf;
+      v = 0.0;
+      for (int p = 0; p < nqe; ++p) {
+        v = fma(r[R.cV + l * nqe + p], __ldg(tens + L.V + (lm * nqe + p) * NL2 + k), v);
+      }
+#pragma unroll
+      for (int a = 0; a < 2; ++a) {
+        v = fma(r[R.cY + 2 * l + a], __ldg(tens + L.Y + (lm * 2 + a) * NL2 + k), v);
+        v = fma(r[R.cZ + 2 * l + a], __ldg(tens + L.Z + (lm * 2 + a) * NL2 + k), v);
+      }
+    }
+    P.val[vbase + g] = v;
+  }
+
+  // ---- B': RHS slice --------------------------------------------------------------------
+  for (int g = threadIdx.x; g < ne * NL; g += blockDim.x) {
+    const int el = g / NL, i = g - el * NL;
+    const double* r = rec + el * R.size;
+    const int* m = meta + el * kMeta;
+    double v = 0.0;
+    for (int q = 0; q < nqv; ++q) v = fma(r[R.cF + q], __ldg(tens + L.PHI + q * NL + i), v);
+#pragma unroll
+    for (int l = 0; l < 3; ++l) {
+      if (m[M_KIND + l] == DGB_EDGE_INTERIOR) continue;
+      const double g0 = r[R.gam + 2 * l], g1 = r[R.gam + 2 * l + 1];
+      for (int p = 0; p < nqe; ++p) {
+        const int row = l * nqe + p;
+        const double dn = fma(g0, __ldg(tens + L.EDPHI + (2 * row) * NL + i),
+                              g1 * __ldg(tens + L.EDPHI + (2 * row + 1) * NL + i));
+        v = fma(r[R.cG + row], __ldg(tens + L.EPHI + row * NL + i), v);
+        v = fma(r[R.cH + row], dn, v);
+      }
+    }
+    P.rhs[static_cast<long long>(e0 + el) * NL + i] = v;
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// BSR SpMV: y = K x (one thread per scalar row)
+// ------------------------------------------------------------------------------------------
+template <int NL>
+__global__ void __launch_bounds__(256) spmv_kernel(int32_t n_rows,
+                                                   const int32_t* __restrict__ row_ptr,
+                                                   const int32_t* __restrict__ col,
+                                                   const double* __restrict__ val,
+                                                   const double* __restrict__ x,
+                                                   double* __restrict__ y) {
+  const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= static_cast<long long>(n_rows) * NL) return;
+  const int e = static_cast<int>(t / NL), i = static_cast<int>(t - static_cast<long long>(e) * NL);
+  const int b0 = __ldg(row_ptr + e), b1 = __ldg(row_ptr + e + 1);
+  double s = 0.0;
+  for (int b = b0; b < b1; ++b) {
+    const double* blkrow = val + (static_cast<long long>(b) * NL + i) * NL;
+    const double* xs = x + static_cast<long long>(__ldg(col + b)) * NL;
+#pragma unroll
+    for (int j = 0; j < NL; ++j) s = fma(__ldg(blkrow + j), __ldg(xs + j), s);
+  }
+  y[t] = s;
+}
+
+// ------------------------------------------------------------------------------------------
+// host: tensors from reference tables
+// ------------------------------------------------------------------------------------------
+Layout make_layout(int nl, int nqv, int nqe) {
+  const int n2 = nl * nl;
+  Layout L;
+  int o = 0;
+  L.S = o; o += 3 * n2;
+  L.M = o; o += n2;
+  L.T = o; o += 2 * n2;
+  L.TA = o; o += 4 * n2;
+  L.TQ = o; o += 2 * nqv * n2;
+  L.Q = o; o += 6 * n2;
+  L.U = o; o += 3 * nqe * n2;
+  L.V = o; o += 9 * nqe * n2;
+  L.Y = o; o += 18 * n2;
+  L.Z = o; o += 18 * n2;
+  L.PHI = o; o += nqv * nl;
+  L.EPHI = o; o += 3 * nqe * nl;
+  L.EDPHI = o; o += 3 * nqe * 2 * nl;
+  L.VX = o; o += nqv;
+  L.VY = o; o += nqv;
+  L.VW = o; o += nqv;
+  L.ET = o; o += nqe;
+  L.EW = o; o += nqe;
+  L.total = o;
+  return L;
+}
+
+Rec make_rec(int nqv, int nqe) {
+  Rec R;
+  int o = 0;
+  R.cD = o; o += 3;
+  R.cR = o; o += 1;
+  R.cC = o; o += 2;
+  R.cCA = o; o += 4;
+  R.cCQ = o; o += 2 * nqv;
+  R.cF = o; o += nqv;
+  R.cW = o; o += 6;
+  R.cU = o; o += 3 * nqe;
+  R.cY = o; o += 6;
+  R.cZ = o; o += 6;
+  R.cV = o; o += 3 * nqe;
+  R.cG = o; o += 3 * nqe;
+  R.cH = o; o += 3 * nqe;
+  R.gam = o; o += 6;
+  R.size = o | 1;  // odd stride: spreads per-element records over banks
+  return R;
+}
+
+std::vector<double> build_tensors(const dgb_reference_tables& t, const Layout& L) {
+  const int nl = t.n_local, nq = t.nq_vol, ne = t.nq_edge, n2 = nl * nl;
+  std::vector<double> out(L.total, 0.0);
+  auto phi = [&](int q, int i) { return t.phi[q * nl + i]; };
+  auto dphi = [&](int q, int i, int a) { return t.dphi[(q * nl + i) * 2 + a]; };
+  auto ephi = [&](int l, int p, int i) { return t.edge_phi[((l * 2) * ne + p) * nl + i]; };
+  auto edphi = [&](int l, int p, int i, int a) {
+    return t.edge_dphi[(((l * 2) * ne + p) * nl + i) * 2 + a];
+  };
+  for (int i = 0; i < nl; ++i) {
+    for (int j = 0; j < nl; ++j) {
+      const int k = i * nl + j;
+      long double s00 = 0, s01 = 0, s11 = 0, m = 0, t0 = 0, t1 = 0, ta[4] = {0, 0, 0, 0};
+      for (int q = 0; q < nq; ++q) {
+        const long double w = t.vol_w[q];
+        s00 += w * dphi(q, j, 0) * dphi(q, i, 0);
+        s01 += w * (static_cast<long double>(dphi(q, j, 0)) * dphi(q, i, 1) +
+                    static_cast<long double>(dphi(q, j, 1)) * dphi(q, i, 0));
+        s11 += w * dphi(q, j, 1) * dphi(q, i, 1);
+        m += w * phi(q, j) * phi(q, i);
+        t0 += w * phi(q, i) * dphi(q, j, 0);
+        t1 += w * phi(q, i) * dphi(q, j, 1);
+        const long double xq[2] = {t.vol_x[q], t.vol_y[q]};
+        for (int a = 0; a < 2; ++a) {
+          for (int c = 0; c < 2; ++c) ta[a * 2 + c] += w * xq[c] * phi(q, i) * dphi(q, j, a);
+        }
+        for (int a = 0; a < 2; ++a) {
+          out[L.TQ + (2 * q + a) * n2 + k] = phi(q, i) * dphi(q, j, a);
+        }
+      }
+      out[L.S + k] = static_cast<double>(s00);
+      out[L.S + n2 + k] = static_cast<double>(s01);
+      out[L.S + 2 * n2 + k] = static_cast<double>(s11);
+      out[L.M + k] = static_cast<double>(m);
+      out[L.T + k] = static_cast<double>(t0);
+      out[L.T + n2 + k] = static_cast<double>(t1);
+      for (int a = 0; a < 4; ++a) out[L.TA + a * n2 + k] = static_cast<double>(ta[a]);
+      for (int l = 0; l < 3; ++l) {
+        for (int a = 0; a < 2; ++a) {
+          long double qs = 0;
+          for (int p = 0; p < ne; ++p) qs += static_cast<long double>(t.edge_w[p]) * ephi(l, p, i) * edphi(l, p, j, a);
+          out[L.Q + (2 * l + a) * n2 + k] = static_cast<double>(qs);
+        }
+        for (int p = 0; p < ne; ++p) out[L.U + (l * ne + p) * n2 + k] = ephi(l, p, i) * ephi(l, p, j);
+        for (int mm = 0; mm < 3; ++mm) {
+          const int lm = l * 3 + mm;
+          for (int p = 0; p < ne; ++p) {
+            out[L.V + (lm * ne + p) * n2 + k] = ephi(l, p, i) * ephi(mm, ne - 1 - p, j);
+          }
+          for (int a = 0; a < 2; ++a) {
+            long double ys = 0, zs = 0;
+            for (int p = 0; p < ne; ++p) {
+              const long double w = t.edge_w[p];
+              ys += w * ephi(l, p, i) * edphi(mm, ne - 1 - p, j, a);
+              zs += w * edphi(l, p, i, a) * ephi(mm, ne - 1 - p, j);
+            }
+            out[L.Y + (lm * 2 + a) * n2 + k] = static_cast<double>(ys);
+            out[L.Z + (lm * 2 + a) * n2 + k] = static_cast<double>(zs);
+          }
+        }
+      }
+    }
+  }
+  for (int q = 0; q < nq; ++q) {
+    for (int i = 0; i < nl; ++i) out[L.PHI + q * nl + i] = phi(q, i);
+    out[L.VX + q] = t.vol_x[q];
+    out[L.VY + q] = t.vol_y[q];
+    out[L.VW + q] = t.vol_w[q];
+  }
+  for (int l = 0; l < 3; ++l) {
+    for (int p = 0; p < ne; ++p) {
+      for (int i = 0; i < nl; ++i) {
+        out[L.EPHI + (l * ne + p) * nl + i] = ephi(l, p, i);
+        for (int a = 0; a < 2; ++a) out[L.EDPHI + ((l * ne + p) * 2 + a) * nl + i] = edphi(l, p, i, a);
+      }
+    }
+  }
+  for (int p = 0; p < ne; ++p) {
+    out[L.ET + p] = t.edge_t[p];
+    out[L.EW + p] = t.edge_w[p];
+  }
+  return out;
+}
+
+void cuda_check(cudaError_t err, const char* what) {
+  if (err != cudaSuccess) {
+    throw Error(DGB_STATUS_CUDA, std::string(what) + ": " + cudaGetErrorString(err));
+  }
+}
+
+int tile_for(int nl) { return nl <= 6 ? 64 : 32; }
+
+}  // namespace dgb
+
+// ------------------------------------------------------------------------------------------
+// plan + C-ABI
+// ------------------------------------------------------------------------------------------
+struct dgb_plan {
+  int device = 0;
+  int degree = 0, nl = 0, nqv = 0, nqe = 0;
+  dgb::Layout L;
+  dgb::Rec R;
+  double* d_tens = nullptr;
+  int32_t* d_err = nullptr;
+  int32_t* h_err = nullptr;  // pinned
+  void* d_scan = nullptr;
+  size_t scan_bytes = 0;
+  int32_t scan_n = 0;
+  int last_status = DGB_OK;
+  cudaEvent_t ev_start = nullptr, ev_stop = nullptr;  // measurement hook (not owned)
+};
+
+namespace {
+
+using dgb::cuda_check;
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    cuda_check(cudaSetDevice(dev), "cudaSetDevice");
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+template <int NL>
+void launch_assemble(const dgb::KParams& P, int n_tiles, size_t smem, cudaStream_t s) {
+  static bool configured = false;
+  if (!configured) {
+    cuda_check(cudaFuncSetAttribute(dgb::assemble_kernel<NL>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024),
+               "cudaFuncSetAttribute");
+    configured = true;
+  }
+  dgb::assemble_kernel<NL><<<n_tiles, 256, smem, s>>>(P);
+}
+
+template <int NL>
+void launch_spmv(const dgb_bsr* a, const double* x, double* y, cudaStream_t s) {
+  const long long rows = static_cast<long long>(a->n_block_rows) * NL;
+  const int grid = static_cast<int>((rows + 255) / 256);
+  if (grid > 0) dgb::spmv_kernel<NL><<<grid, 256, 0, s>>>(a->n_block_rows, a->row_ptr, a->col, a->val, x, y);
+}
+
+void validate_tables(const dgb_reference_tables* t) {
+  if (!t || t->degree < 1 || t->degree > 4) {
+    throw dgb::Error(DGB_STATUS_UNSUPPORTED_DEGREE, "polynomial degree must be between 1 and 4",
+                     t ? t->degree : -1);
+  }
+  if (t->n_local != (t->degree + 1) * (t->degree + 2) / 2) {
+    throw dgb::Error(DGB_STATUS_DIMENSION_MISMATCH, "n_local does not match the degree");
+  }
+  if (t->nq_vol < 1 || t->nq_vol > dgb::kTensorQ || t->nq_edge < 1 || t->nq_edge > dgb::kMaxQE) {
+    throw dgb::Error(DGB_STATUS_INVALID_ARGUMENT, "unsupported quadrature size");
+  }
+}
+
+void validate_field(const dgb_scalar_field& f, bool element_constant, const char* name) {
+  if (f.kind == DGB_FIELD_PER_ELEMENT && !f.per_element) {
+    throw dgb::Error(DGB_STATUS_INVALID_ARGUMENT, std::string(name) + ": per_element is null");
+  }
+  if (element_constant && f.kind == DGB_FIELD_FUNCTION) {
+    throw dgb::Error(DGB_STATUS_INVALID_ARGUMENT,
+                     std::string(name) + " must be CONSTANT or PER_ELEMENT on the GPU path");
+  }
+  if (f.kind > DGB_FIELD_FUNCTION || f.kind < 0) {
+    throw dgb::Error(DGB_STATUS_INVALID_ARGUMENT, std::string(name) + ": unknown field kind");
+  }
+}
+
+// Device allocations freed on scope exit (dgb_assemble_all_host).
+struct Buffers {
+  std::vector<void*> ptrs;
+  ~Buffers() {
+    for (void* p : ptrs) cudaFree(p);
+  }
+  template <typename T>
+  T* alloc(size_t n) {
+    void* p = nullptr;
+    cuda_check(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)), "cudaMalloc");
+    ptrs.push_back(p);
+    return static_cast<T*>(p);
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
+int dgb_plan_create(const dgb_reference_tables* tables, int32_t device, dgb_plan** out) {
+  *out = nullptr;
+  return dgb::guarded([&] {
+    validate_tables(tables);
+    DeviceGuard guard(device);
+    auto* p = new dgb_plan();
+    try {
+      p->device = device;
+      p->degree = tables->degree;
+      p->nl = tables->n_local;
+      p->nqv = tables->nq_vol;
+      p->nqe = tables->nq_edge;
+      p->L = dgb::make_layout(p->nl, p->nqv, p->nqe);
+      p->R = dgb::make_rec(p->nqv, p->nqe);
+      const std::vector<double> h = dgb::build_tensors(*tables, p->L);
+      cuda_check(cudaMalloc(&p->d_tens, h.size() * sizeof(double)), "cudaMalloc(tensors)");
+      cuda_check(cudaMemcpy(p->d_tens, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice),
+                 "cudaMemcpy(tensors)");
+      cuda_check(cudaMalloc(&p->d_err, sizeof(int32_t)), "cudaMalloc(err)");
+      cuda_check(cudaMallocHost(&p->h_err, sizeof(int32_t)), "cudaMallocHost(err)");
+      *p->h_err = INT_MAX;
+    } catch (...) {
+      dgb_plan_destroy(p);
+      throw;
+    }
+    *out = p;
+  });
+}
+
+void dgb_plan_destroy(dgb_plan* p) {
+  if (!p) return;
+  int prev = -1;
+  cudaGetDevice(&prev);
+  cudaSetDevice(p->device);
+  cudaFree(p->d_tens);
+  cudaFree(p->d_err);
+  cudaFree(p->d_scan);
+  if (p->h_err) cudaFreeHost(p->h_err);
+  if (prev >= 0) cudaSetDevice(prev);
+  delete p;
+}
+
+int dgb_assemble(dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_problem* problem,
+                 const dgb_params* params, dgb_bsr* out, double* rhs, void* stream) {
+  return dgb::guarded([&] {
+    if (!plan || !mesh || !problem || !params || !out || !rhs) {
+      throw dgb::Error(DGB_STATUS_INVALID_ARGUMENT, "null argument");
+    }
+    validate_field(problem->diffusion, true, "diffusion");
+    validate_field(problem->linear_reaction, true, "linear_reaction");
+    validate_field(problem->source, false, "source");
+    validate_field(problem->dirichlet, false, "dirichlet");
+    validate_field(problem->neumann, false, "neumann");
+    if (problem->dirichlet.kind == DGB_FIELD_PER_ELEMENT ||
+        problem->neumann.kind == DGB_FIELD_PER_ELEMENT) {
+      throw dgb::Error(DGB_STATUS_INVALID_ARGUMENT, "boundary data cannot be PER_ELEMENT");
+    }
+    if (problem->advection.kind < DGB_VEC_CONSTANT || problem->advection.kind > DGB_VEC_TRIG) {
+      throw dgb::Error(DGB_STATUS_INVALID_ARGUMENT, "unknown velocity kind");
+    }
+    if (out->block_dim != plan->nl || out->n_block_rows != mesh->n_elements ||
+        out->nnzb != dgb_bsr_nnzb(mesh->n_elements, mesh->n_interior_edges)) {
+      throw dgb::Error(DGB_STATUS_DIMENSION_MISMATCH, "BSR output does not match mesh / plan");
+    }
+    DeviceGuard guard(plan->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int E = mesh->n_elements;
+    plan->last_status = DGB_OK;
+    if (E == 0) {
+      return;
+    }
+    // pattern: counts -> inclusive scan into row_ptr[1..E]
+    dgb::count_blocks_kernel<<<(E + 255) / 256, 256, 0, s>>>(mesh->edge_kind, mesh->element_edges,
+                                                             E, out->row_ptr, plan->d_err);
+    cuda_check(cudaGetLastError(), "count_blocks_kernel");
+    if (plan->scan_n != E) {
+      size_t bytes = 0;
+      cub::DeviceScan::InclusiveSum(nullptr, bytes, out->row_ptr + 1, out->row_ptr + 1, E, s);
+      if (bytes > plan->scan_bytes) {
+        cudaFree(plan->d_scan);
+        plan->d_scan = nullptr;
+        cuda_check(cudaMalloc(&plan->d_scan, bytes), "cudaMalloc(scan)");
+        plan->scan_bytes = bytes;
+      }
+      plan->scan_n = E;
+    }
+    size_t bytes = plan->scan_bytes;
+    cuda_check(cub::DeviceScan::InclusiveSum(plan->d_scan, bytes, out->row_ptr + 1,
+                                             out->row_ptr + 1, E, s),
+               "DeviceScan");
+
+    dgb::KParams P;
+    std::memset(&P, 0, sizeof P);
+    P.nodes = mesh->nodes;
+    P.elements = mesh->elements;
+    P.edge_kind = mesh->edge_kind;
+    P.edge_elements = mesh->edge_elements;
+    P.element_edges = mesh->element_edges;
+    P.n_elements = E;
+    P.prob = *problem;
+    P.kappa = params->kappa;
+    P.sigma_i = params->sigma_interior;
+    P.sigma_b = params->sigma_boundary;
+    P.drop_neumann = params->neumann_inflow == DGB_INFLOW_DROP;
+    P.tens = plan->d_tens;
+    P.L = plan->L;
+    P.R = plan->R;
+    P.nl = plan->nl;
+    P.nqv = plan->nqv;
+    P.nqe = plan->nqe;
+    P.tile = dgb::tile_for(plan->nl);
+    P.row_ptr = out->row_ptr;
+    P.col = out->col;
+    P.val = out->val;
+    P.rhs = rhs;
+    P.err_edge = plan->d_err;
+    const int n_tiles = (E + P.tile - 1) / P.tile;
+    const size_t smem = static_cast<size_t>(P.tile) * (plan->R.size + dgb::kGeo) * sizeof(double) +
+                        static_cast<size_t>(P.tile) * (dgb::kMeta + 4) * sizeof(int) + 16;
+    if (plan->ev_start) cuda_check(cudaEventRecord(plan->ev_start, s), "cudaEventRecord");
+    switch (plan->nl) {
+      case 3: launch_assemble<3>(P, n_tiles, smem, s); break;
+      case 6: launch_assemble<6>(P, n_tiles, smem, s); break;
+      case 10: launch_assemble<10>(P, n_tiles, smem, s); break;
+      case 15: launch_assemble<15>(P, n_tiles, smem, s); break;
+      default: throw dgb::Error(DGB_STATUS_UNSUPPORTED_DEGREE, "unsupported n_local", plan->nl);
+    }
+    cuda_check(cudaGetLastError(), "assemble_kernel");
+    if (plan->ev_stop) cuda_check(cudaEventRecord(plan->ev_stop, s), "cudaEventRecord");
+    cuda_check(cudaMemcpyAsync(plan->h_err, plan->d_err, sizeof(int32_t), cudaMemcpyDeviceToHost, s),
+               "cudaMemcpyAsync(err)");
+  });
+}
+
+int dgb_plan_set_kernel_events(dgb_plan* plan, void* start, void* stop) {
+  if (!plan) return DGB_STATUS_INVALID_ARGUMENT;
+  plan->ev_start = static_cast<cudaEvent_t>(start);
+  plan->ev_stop = static_cast<cudaEvent_t>(stop);
+  return DGB_OK;
+}
+
+// count_blocks_kernel + cub scan (init + scan kernels) + assemble_kernel
+int32_t dgb_assemble_launch_count(void) { return 4; }
+
+int dgb_plan_status(dgb_plan* plan, void* stream) {
+  return dgb::guarded([&] {
+    if (!plan) throw dgb::Error(DGB_STATUS_INVALID_ARGUMENT, "null plan");
+    DeviceGuard guard(plan->device);
+    cuda_check(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)), "cudaStreamSynchronize");
+    if (*plan->h_err != INT_MAX) {
+      throw dgb::Error(DGB_STATUS_INFLOW_ON_NEUMANN,
+                       "inflow across a Neumann edge: no boundary data to upwind from",
+                       *plan->h_err);
+    }
+  });
+}
+
+int dgb_spmv(const dgb_bsr* a, const double* x, double* y, void* stream) {
+  return dgb::guarded([&] {
+    if (!a || !x || !y) throw dgb::Error(DGB_STATUS_INVALID_ARGUMENT, "null argument");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    switch (a->block_dim) {
+      case 3: launch_spmv<3>(a, x, y, s); break;
+      case 6: launch_spmv<6>(a, x, y, s); break;
+      case 10: launch_spmv<10>(a, x, y, s); break;
+      case 15: launch_spmv<15>(a, x, y, s); break;
+      default: throw dgb::Error(DGB_STATUS_UNSUPPORTED_DEGREE, "unsupported block size", a->block_dim);
+    }
+    cuda_check(cudaGetLastError(), "spmv_kernel");
+  });
+}
+
+int dgb_assemble_all_host(const dgb_mesh_arrays* mesh, const dgb_reference_tables* tables,
+                          const dgb_problem* problem, const dgb_params* params, int32_t device,
+                          dgb_bsr* out, double* rhs) {
+  dgb_plan* plan = nullptr;
+  const int st = dgb::guarded([&] {
+    if (!mesh || !tables || !problem || !params || !out || !rhs) {
+      throw dgb::Error(DGB_STATUS_INVALID_ARGUMENT, "null argument");
+    }
+    DeviceGuard guard(device);
+    Buffers buf;
+    const int E = mesh->n_elements, ne = mesh->n_edges, nn = mesh->n_nodes;
+    const int nl = tables->n_local;
+    const int64_t nnzb = dgb_bsr_nnzb(E, mesh->n_interior_edges);
+    if (out->nnzb != nnzb || out->block_dim != nl || out->n_block_rows != E) {
+      throw dgb::Error(DGB_STATUS_DIMENSION_MISMATCH, "BSR output does not match mesh / tables");
+    }
+    cudaStream_t s;
+    cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate");
+    struct StreamGuard {
+      cudaStream_t s;
+      ~StreamGuard() { cudaStreamDestroy(s); }
+    } sg{s};
+    dgb_mesh_arrays dm = *mesh;
+    auto up = [&](const void* src, size_t bytes) {
+      void* d = buf.alloc<char>(bytes);
+      cuda_check(cudaMemcpyAsync(d, src, bytes, cudaMemcpyHostToDevice, s), "cudaMemcpyAsync(H2D)");
+      return d;
+    };
+    dm.nodes = static_cast<const double*>(up(mesh->nodes, sizeof(double) * 2 * nn));
+    dm.elements = static_cast<const int32_t*>(up(mesh->elements, sizeof(int32_t) * 3 * E));
+    dm.edges = static_cast<const int32_t*>(up(mesh->edges, sizeof(int32_t) * 2 * ne));
+    dm.edge_kind = static_cast<const uint8_t*>(up(mesh->edge_kind, ne));
+    dm.edge_elements = static_cast<const int32_t*>(up(mesh->edge_elements, sizeof(int32_t) * 2 * ne));
+    dm.element_edges = static_cast<const int32_t*>(up(mesh->element_edges, sizeof(int32_t) * 3 * E));
+    dgb_problem dp = *problem;
+    dgb_scalar_field* fields[] = {&dp.diffusion, &dp.linear_reaction, &dp.source, &dp.dirichlet,
+                                  &dp.neumann};
+    for (dgb_scalar_field* f : fields) {
+      if (f->kind == DGB_FIELD_PER_ELEMENT && f->per_element) {
+        f->per_element = static_cast<const double*>(up(f->per_element, sizeof(double) * E));
+      }
+    }
+    const int pc = dgb_plan_create(tables, device, &plan);
+    if (pc != DGB_OK) throw dgb::Error(pc, dgb_last_error_message(), dgb_last_error_detail());
+    dgb_bsr d;
+    d.n_block_rows = E;
+    d.block_dim = nl;
+    d.nnzb = nnzb;
+    d.row_ptr = buf.alloc<int32_t>(E + 1);
+    d.col = buf.alloc<int32_t>(nnzb);
+    d.val = buf.alloc<double>(static_cast<size_t>(nnzb) * nl * nl);
+    double* d_rhs = buf.alloc<double>(static_cast<size_t>(E) * nl);
+    int rc = dgb_assemble(plan, &dm, &dp, params, &d, d_rhs, s);
+    if (rc != DGB_OK) throw dgb::Error(rc, dgb_last_error_message(), dgb_last_error_detail());
+    rc = dgb_plan_status(plan, s);
+    if (rc != DGB_OK) throw dgb::Error(rc, dgb_last_error_message(), dgb_last_error_detail());
+    cuda_check(cudaMemcpyAsync(out->row_ptr, d.row_ptr, sizeof(int32_t) * (E + 1), cudaMemcpyDeviceToHost, s), "D2H");
+    cuda_check(cudaMemcpyAsync(out->col, d.col, sizeof(int32_t) * nnzb, cudaMemcpyDeviceToHost, s), "D2H");
+    cuda_check(cudaMemcpyAsync(out->val, d.val, sizeof(double) * nnzb * nl * nl, cudaMemcpyDeviceToHost, s), "D2H");
+    cuda_check(cudaMemcpyAsync(rhs, d_rhs, sizeof(double) * E * nl, cudaMemcpyDeviceToHost, s), "D2H");
+    cuda_check(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+  });
+  dgb_plan_destroy(plan);
+  return st;
+}
+
+}  // extern "C"

@@ -1,0 +1,73 @@
+"""GPU parity: the sm_100a assembly vs the C restatement oracle (pinned bitwise to the
+reference), through the C-ABI.  Comparator: SURVEY.md §8(c)."""
+import numpy as np
+import pytest
+
+from helpers import compare_system, gather_rows
+from oracle.oracle import OracleLib
+from paper_1502_02941_b200 import capi, dgfem, problems
+
+pytestmark = pytest.mark.gpu
+
+REGISTRY = ["smooth-sine", "smooth-sine-mixed", "poly-exact", "paper-boundary-layer-linear",
+            "pure-advection-patch"]
+
+
+@pytest.fixture(scope="module")
+def oracle():
+    return OracleLib()
+
+
+def run_gpu(mesh, ref, spec, params):
+    import torch
+    s = dgfem.assemble_all(mesh, ref, spec, params)
+    torch.cuda.synchronize()
+    return (s.row_ptr.cpu().numpy(), s.col.cpu().numpy(), s.val.cpu().numpy(),
+            s.rhs.cpu().numpy())
+
+
+@pytest.mark.parametrize("name", REGISTRY)
+@pytest.mark.parametrize("degree", [1, 2, 3, 4])
+def test_registry_problems(oracle, name, degree):
+    spec = problems.registry_get(name)
+    mesh = dgfem.unit_square_mesh(6, 0.15, 11, True, 12, spec.neumann_sides)
+    ref = dgfem.ReferenceElement(degree)
+    for method in (capi.SIPG, capi.NIPG, capi.IIPG):
+        params = dgfem.set_parameters(method, degree)
+        g = run_gpu(mesh, ref, spec, params)
+        o = oracle.assemble(mesh.arrays(), ref.tables(), spec.c, params)
+        compare_system(g, o)
+
+
+@pytest.mark.parametrize("index", [1, 2, 3, 4, 5])
+def test_configs_small(oracle, index):
+    cfg = problems.CONFIGS[index]
+    n = 12
+    mesh = dgfem.unit_square_mesh(n, cfg.jitter, problems.SEED_JITTER, cfg.permute,
+                                  problems.SEED_PERMUTE, cfg.neumann_sides)
+    ref = dgfem.ReferenceElement(cfg.degree, cfg.quad_order)
+    spec = problems.config_problem(index, mesh.n_elements)
+    for method in cfg.methods:
+        params = dgfem.config_parameters(cfg, method)
+        g = run_gpu(mesh, ref, spec, params)
+        o = oracle.assemble(mesh.arrays(), ref.tables(), spec.c, params)
+        compare_system(g, o)
+
+
+@pytest.mark.parametrize("index", [1, 2, 3, 4, 5])
+def test_configs_full_size_sampled_rows(oracle, index):
+    """Full BASELINE.json sizes; the oracle recomputes a seeded sample of block rows."""
+    cfg = problems.CONFIGS[index]
+    mesh = dgfem.config_mesh(cfg)
+    ref = dgfem.ReferenceElement(cfg.degree, cfg.quad_order)
+    spec = problems.config_problem(index, mesh.n_elements)
+    rng = np.random.default_rng(1000 + index)
+    rows = np.unique(np.concatenate([
+        rng.choice(mesh.n_elements, size=min(mesh.n_elements, 4000), replace=False),
+        np.arange(min(64, mesh.n_elements)), np.arange(mesh.n_elements - 64, mesh.n_elements)]))
+    for method in cfg.methods:
+        params = dgfem.config_parameters(cfg, method)
+        g = run_gpu(mesh, ref, spec, params)
+        assert g[0][-1] == mesh.n_elements + 2 * mesh.n_interior_edges
+        o = oracle.assemble(mesh.arrays(), ref.tables(), spec.c, params, rows=rows)
+        compare_system(gather_rows(*g, rows), o)
