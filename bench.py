@@ -1,0 +1,424 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 DG system assembly (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C]
+
+Workload (default): BASELINE.json configs[1] = config 2 -- the 256x256 unit-square mesh
+(131,072 triangles), P2, assembled with each of SIPG, NIPG and IIPG (sigma = 18).  One step =
+the three assemblies (K = D + C + R in BSR form plus F).  `value` = elements assembled per
+second with mesh, tables and coefficients resident in HBM; `e2e` = the same metric through
+the host-buffer C-ABI call (dgb_assemble_all_host: H2D of the mesh, assembly, D2H of K and F).
+
+Under torchrun (N > 1) each rank assembles its own shard (weak scaling; no collective on the
+data path), the step time is the max over ranks.  `--impl reference` times the reference's
+own CPU assembly (oracle/_ref, OpenMP on all host cores) on a bounded sample of the workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+HBM_FALLBACK_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
+PROFILE_SUMMARY = os.path.join(ROOT, "profiles", "ncu_summary.json")
+METRIC = "DG system assembly elements/sec (fp64, 1 B200) and achieved HBM GB/s vs roofline"
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--minblocks", type=int, default=0, help="tuning knob (P2 kernel CTAs/SM)")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- helpers
+def peak_hbm():
+    try:
+        with open(PEAKS_FILE) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return HBM_FALLBACK_GBS, "fallback"
+
+
+def algorithmic_bytes(mesh, nl: int, per_element_fields: int) -> int:
+    """every input read once, every output written once.
+    reads : 16 n_nodes + 12 E (elements) + 12 E (element_edges) + 8 n_edges (edge_elements)
+            + 1 n_edges (edge_kind) + 8 E per per-element coefficient field
+    writes: 8 nl^2 (E + 2I) (values) + 4 (E + 2I) (block cols) + 4 (E + 1) (row ptr)
+            + 8 nl E (RHS)"""
+    E, I, ne, nn = mesh.n_elements, mesh.n_interior_edges, mesh.n_edges, mesh.n_nodes
+    nb = E + 2 * I
+    reads = 16 * nn + 12 * E + 12 * E + 8 * ne + ne + 8 * E * per_element_fields
+    writes = 8 * nl * nl * nb + 4 * nb + 4 * (E + 1) + 8 * nl * E
+    return reads + writes
+
+
+class ClockSampler:
+    """Samples SM clock and throttle reasons with NVML during the timed region."""
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x2: "applications_clocks_setting", 0x1: "gpu_idle"}
+
+    def __init__(self, device_index: int):
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nvml = None
+
+    def _sample(self):
+        p = self.nvml
+        self.samples.append(p.nvmlDeviceGetClockInfo(self.h, p.NVML_CLOCK_SM))
+        try:
+            mask = p.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        except Exception:
+            mask = p.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+        for bit, name in self.REASONS.items():
+            if mask & bit and name != "gpu_idle":
+                self.reasons.add(name)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self._sample()
+            except Exception:
+                return
+            self._stop.wait(0.01)
+
+    def __enter__(self):
+        if self.nvml:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *exc):
+        if self.nvml:
+            self._stop.set()
+            self.t.join()
+            try:
+                self._sample()
+            except Exception:
+                pass
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml unavailable"]}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def cpu_reference_sample(cfg_index: int, n_sample: int, seconds: float):
+    """Times the reference's own assemble_all + stiffness() (oracle/_ref, OpenMP on every host
+    core) on config `cfg_index`'s coefficients over an n_sample^2 unit-square mesh; falls back
+    to the plain-C restatement when the reference library is absent.  Returns
+    (elements/s, kind, cores, sample description, seconds)."""
+    from oracle import oracle as orc
+    from paper_1502_02941_b200 import dgfem, problems
+    cfg = problems.CONFIGS[cfg_index]
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    mesh = dgfem.unit_square_mesh(n_sample, cfg.jitter, problems.SEED_JITTER, cfg.permute,
+                                  problems.SEED_PERMUTE, cfg.neumann_sides)
+    spec = problems.config_problem(cfg_index, mesh.n_elements)
+    params = [dgfem.config_parameters(cfg, m) for m in cfg.methods]
+    elements = 0
+    t_total = 0.0
+    try:
+        lib = orc.RefLib()
+        raw = mesh.raw()
+        rmesh = lib.build_mesh(raw["nodes"], raw["elements"], raw["dirichlet"], raw["neumann"])
+        rref = lib.reference(cfg.degree, cfg.quad_order)
+        kind = "reference"
+        clip = cfg.neumann_sides if cfg.neumann_inflow == 1 else 0
+        while True:
+            for p in params:
+                s = lib.assemble(rmesh, rref, spec.c, p, threads=cores, clip_sides=clip)
+                t_total += s.seconds[0] + s.seconds[1]
+                elements += mesh.n_elements
+                del s
+            if t_total >= seconds:
+                break
+    except FileNotFoundError:
+        ol = orc.OracleLib()
+        kind = "port"
+        arrays, tables = mesh.arrays(), dgfem.ReferenceElement(cfg.degree, cfg.quad_order).tables()
+        while True:
+            for p in params:
+                t0 = time.perf_counter()
+                ol.assemble(arrays, tables, spec.c, p, threads=cores)
+                t_total += time.perf_counter() - t0
+                elements += mesh.n_elements
+            if t_total >= seconds:
+                break
+    desc = (f"config {cfg_index} coefficients on a {n_sample}x{n_sample} unit-square mesh "
+            f"({mesh.n_elements} elements), methods {len(params)}, assemble_all + stiffness(), "
+            f"{elements // mesh.n_elements} assemblies in {t_total:.1f} s")
+    return elements / t_total, kind, cores, desc, t_total
+
+
+# ----------------------------------------------------------------------------- ours
+def run_ours(args, world, rank, local):
+    import ctypes as C
+
+    import torch
+    from paper_1502_02941_b200 import capi, dgfem, problems
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    lib = capi.load()
+    cfg = problems.CONFIGS[args.config]
+    mesh = dgfem.config_mesh(cfg)
+    ref = dgfem.ReferenceElement(cfg.degree, cfg.quad_order)
+    spec = problems.config_problem(args.config, mesh.n_elements)
+    params = [dgfem.config_parameters(cfg, m) for m in cfg.methods]
+    plan = dgfem.Plan(ref.view, local)
+    if args.minblocks:
+        plan.set_option(capi.OPTION_MIN_BLOCKS, args.minblocks)
+    dmesh = dgfem.DeviceMesh(mesh, local)
+    dprob = dgfem.DeviceProblem(spec, local)
+    outs = [plan.allocate(dmesh) for _ in params]
+    stream = torch.cuda.current_stream(local)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=f"cuda:{local}")  # 256 MiB > L2
+
+    def step(kernel_events=None):
+        for i, (p, o) in enumerate(zip(params, outs)):
+            if kernel_events is not None:
+                ks, ke = kernel_events[i]
+                lib.dgb_plan_set_kernel_events(plan._h, C.c_void_p(ks.cuda_event), C.c_void_p(ke.cuda_event))
+            plan.assemble(dmesh, dprob, p, o, stream=stream, check=False)
+        lib.dgb_plan_set_kernel_events(plan._h, None, None)
+
+    for _ in range(args.warmup):
+        flush.fill_(1.0)
+        step()
+    dgfem._check(lib.dgb_plan_status(plan._h, C.c_void_p(stream.cuda_stream)))
+    torch.cuda.synchronize()
+
+    K = args.steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    kev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            for _ in params] for _ in range(K)]
+    for row in kev:  # torch creates the cudaEvent_t lazily: record once so .cuda_event exists
+        for a, b in row:
+            a.record(stream)
+            b.record(stream)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        for k in range(K):
+            flush.fill_(float(k))          # L2 flush between timed steps (outside the events)
+            ev[k][0].record(stream)
+            step(kev[k])
+            ev[k][1].record(stream)
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    dgfem._check(lib.dgb_plan_status(plan._h, C.c_void_p(stream.cuda_stream)))
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    kern_ms = [a.elapsed_time(b) for row in kev for a, b in row]
+    total_ms = sum(step_ms)
+    if dist:
+        t = torch.tensor([total_ms], device=f"cuda:{local}", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / K
+    units_per_step = len(params) * mesh.n_elements
+    value = world * units_per_step * K / (total_ms / 1e3)
+
+    # roofline of the block-row kernel (dominant launch)
+    per_elem_fields = len(spec.per_element)
+    bytes_per_launch = algorithmic_bytes(mesh, ref.n_local, per_elem_fields)
+    kern_avg_ms = sum(kern_ms) / len(kern_ms)
+    achieved = bytes_per_launch / (kern_avg_ms / 1e3) / 1e9
+    peak, peak_kind = peak_hbm()
+    traffic = None
+    try:
+        with open(PROFILE_SUMMARY) as f:
+            prof = json.load(f)
+        entry = prof.get(f"config{args.config}")
+        if entry:
+            traffic = entry.get("dram_bytes_per_launch")
+    except Exception:
+        pass
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": traffic,
+                "peak_source": peak_kind, "kernel": f"assemble_kernel<{ref.n_local}>",
+                "kernel_ms": round(kern_avg_ms, 4), "bytes_per_launch": bytes_per_launch,
+                "kernel_share_of_step": round(sum(kern_ms) / total_ms, 3) if world == 1 else None}
+
+    # e2e through the host-buffer C-ABI entry point (pinned host memory in and out)
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, mesh, ref, spec, params, local)
+        if dist:
+            t = torch.tensor([e2e["seconds"]], device=f"cuda:{local}", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e["value"] = world * e2e["elements"] / float(t.item())
+        e2e = {"value": round(e2e["value"], 1), "unit": "elements/s",
+               "h2d_bytes_per_step": e2e["h2d"], "d2h_bytes_per_step": e2e["d2h"],
+               "steps": e2e["steps"], "api": "dgb_assemble_all_host"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        n_sample = {1: 32, 2: 96, 3: 32, 4: 128, 5: 24}[args.config]
+        v, kind, cores, desc, secs = cpu_reference_sample(args.config, n_sample, args.cpu_seconds)
+        cpu = {"value": round(v, 1), "unit": "elements/s", "cores": cores, "kind": kind,
+               "sample": desc}
+
+    if dist:
+        dist.destroy_process_group()
+    if rank != 0:
+        return
+    line = {
+        "metric": METRIC, "value": round(value, 1), "unit": "elements/s", "n_gpus": world,
+        "steps": K, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded BASELINE.json config inputs; no dataset involved)",
+        "config": {
+            "workload": f"config {args.config}: {cfg.n}x{cfg.n} unit square, {mesh.n_elements} "
+                        f"triangles, P{cfg.degree}, methods "
+                        + "/".join(["SIPG", "NIPG", "IIPG"][m] for m in cfg.methods)
+                        + f", sigma={cfg.sigma:g}",
+            "elements_per_step": units_per_step, "n_local": ref.n_local,
+            "nq_vol": ref.nq_vol, "nq_edge": ref.nq_edge,
+            "l2": "flushed between timed steps by a 256 MiB write (outside the timed events)",
+            "parallelism": f"{world} rank(s), element-row shards" if world > 1 else "1 GPU",
+        },
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": K * len(params) * lib.dgb_assemble_launch_count(),
+        "clocks": clocks.summary(),
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_e2e(args, mesh, ref, spec, params, device):
+    """dgb_assemble_all_host per method: H2D of the mesh + coefficient arrays from pinned host
+    memory, plan setup, assembly, D2H of K (BSR) and F into pinned host memory."""
+    import ctypes as C
+
+    import torch
+    from paper_1502_02941_b200 import capi, dgfem
+    from paper_1502_02941_b200.capi import Bsr, MeshArrays
+
+    lib = capi.load()
+    pinned = {}
+    for k, a in mesh.arrays().items():
+        t = torch.from_numpy(a.copy()).pin_memory()
+        pinned[k] = t
+    mv = MeshArrays()
+    mv.n_nodes, mv.n_elements, mv.n_edges = mesh.n_nodes, mesh.n_elements, mesh.n_edges
+    mv.n_interior_edges = mesh.n_interior_edges
+    for k, t in pinned.items():
+        setattr(mv, k, t.data_ptr())
+    prob = type(spec.c).from_buffer_copy(spec.c)
+    keep = []
+    for name, arr in spec.per_element.items():
+        t = torch.from_numpy(arr).pin_memory()
+        keep.append(t)
+        getattr(prob, name).per_element = t.data_ptr()
+    E, nl = mesh.n_elements, ref.n_local
+    nnzb = lib.dgb_bsr_nnzb(E, mesh.n_interior_edges)
+    rp = torch.empty(E + 1, dtype=torch.int32).pin_memory()
+    col = torch.empty(nnzb, dtype=torch.int32).pin_memory()
+    val = torch.empty(nnzb * nl * nl, dtype=torch.float64).pin_memory()
+    rhs = torch.empty(E * nl, dtype=torch.float64).pin_memory()
+    b = Bsr()
+    b.n_block_rows, b.block_dim, b.nnzb = E, nl, nnzb
+    b.row_ptr, b.col, b.val = rp.data_ptr(), col.data_ptr(), val.data_ptr()
+    h2d = sum(t.numel() * t.element_size() for t in pinned.values()) + sum(
+        t.numel() * t.element_size() for t in keep)
+    d2h = rp.numel() * 4 + col.numel() * 4 + val.numel() * 8 + rhs.numel() * 8
+
+    def one_step():
+        for p in params:
+            dgfem._check(lib.dgb_assemble_all_host(C.byref(mv), C.byref(ref.view), C.byref(prob),
+                                                   C.byref(p), device, C.byref(b), rhs.data_ptr()))
+
+    one_step()  # warm-up (module load, allocator)
+    steps = max(2, min(args.steps, 5))
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        one_step()
+    secs = time.perf_counter() - t0
+    elements = steps * len(params) * E
+    return {"value": elements / secs, "seconds": secs, "elements": elements, "steps": steps,
+            "h2d": h2d * len(params), "d2h": d2h * len(params)}
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    from paper_1502_02941_b200 import problems
+    cfg = problems.CONFIGS[args.config]
+    n_sample = {1: 32, 2: 64, 3: 24, 4: 96, 5: 16}[args.config]
+    per_step = max(0.5, min(10.0, 120.0 / max(1, args.steps + args.warmup)))
+    for _ in range(args.warmup):
+        cpu_reference_sample(args.config, n_sample, 0.0)
+    vals, secs_total = [], 0.0
+    kind = cores = desc = None
+    for _ in range(args.steps):
+        v, kind, cores, desc, secs = cpu_reference_sample(args.config, n_sample, per_step)
+        vals.append(v)
+        secs_total += secs
+    value = statistics.fmean(vals)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 1), "unit": "elements/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1e3 * secs_total / args.steps, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded BASELINE.json config inputs)",
+        "config": {"workload": f"config {args.config} (bounded CPU sample: {desc})",
+                   "parallelism": f"OpenMP, {cores} host threads"},
+        "cpu_baseline": {"value": round(value, 1), "unit": "elements/s", "cores": cores,
+                         "kind": kind, "sample": desc},
+        "e2e": {"value": round(value, 1), "unit": "elements/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse_args()
+    world, rank, local = dist_setup(args)
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+    else:
+        run_ours(args, world, rank, local)
+
+
+if __name__ == "__main__":
+    main()

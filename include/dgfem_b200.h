@@ -276,6 +276,14 @@ int dgb_plan_status(dgb_plan* plan, void* stream);
  * can time that kernel with CUDA events on the launching stream (bench.py's roofline). */
 int dgb_plan_set_kernel_events(dgb_plan* plan, void* start, void* stop);
 
+/* Plan options.  DGB_OPTION_FORCE_GENERIC_KERNEL = 1: run the generic (any quadrature) block-row
+ * kernel even where a specialised one exists (used by the tests to check both). */
+enum dgb_plan_option {
+  DGB_OPTION_FORCE_GENERIC_KERNEL = 1,
+  DGB_OPTION_MIN_BLOCKS = 2 /* tuning knob: register budget of the P2 kernel (CTAs per SM) */
+};
+int dgb_plan_set_option(dgb_plan* plan, int32_t option, int32_t value);
+
 /* Kernel launches one dgb_assemble call issues (for bench.py's gpu_launches count). */
 int32_t dgb_assemble_launch_count(void);
 

@@ -166,8 +166,29 @@ __device__ __forceinline__ void family(int fn, const double* p, double x, double
   }
 }
 
+// FUNCTION scalar field at a point (out of line: one copy of the transcendental families).
+__device__ __noinline__ double scalar_function(int fn, int mode, double p0, double p1, double p2,
+                                               double p3, double q0, double q1, double q2,
+                                               double q3, double x, double y) {
+  const double p[4] = {p0, p1, p2, p3};
+  double u, ux, uy, lap;
+  family(fn, p, x, y, u, ux, uy, lap);
+  switch (mode) {
+    case DGB_MODE_VALUE: return u;
+    case DGB_MODE_SOURCE: return q0 * u - q1 * lap + q2 * ux + q3 * uy;
+    case DGB_MODE_FLUX_X: return q1 * ux;
+    default: return nan("");
+  }
+}
+
 // CONSTANT / FUNCTION scalar field at a point (device twin of oracle/dg_coeffs.h).
 __device__ __forceinline__ double scalar_point(const dgb_scalar_field& f, double x, double y) {
+  if (f.kind == DGB_FIELD_CONSTANT) return f.value;
+  return scalar_function(f.fn, f.mode, f.p[0], f.p[1], f.p[2], f.p[3], f.q[0], f.q[1], f.q[2],
+                         f.q[3], x, y);
+}
+
+__device__ __forceinline__ double scalar_point_inline(const dgb_scalar_field& f, double x, double y) {
   if (f.kind == DGB_FIELD_CONSTANT) return f.value;
   double u, ux, uy, lap;
   family(f.fn, f.p, x, y, u, ux, uy, lap);
@@ -183,6 +204,12 @@ __device__ __forceinline__ double scalar_element(const dgb_scalar_field& f, int 
   return f.kind == DGB_FIELD_PER_ELEMENT ? __ldg(f.per_element + e) : f.value;
 }
 
+__device__ __noinline__ void velocity_trig(double w0, double w1, double x, double y, double& bx,
+                                          double& by) {
+  bx = cos(FMUL(w0, y));
+  by = sin(FMUL(w1, x));
+}
+
 // Velocity at a point; the affine form keeps the reference's unfused evaluation order.
 __device__ __forceinline__ void velocity(const dgb_vector_field& b, double x, double y,
                                          double& bx, double& by) {
@@ -196,8 +223,7 @@ __device__ __forceinline__ void velocity(const dgb_vector_field& b, double x, do
       by = FADD(FADD(b.p[1], FMUL(b.p[4], x)), FMUL(b.p[5], y));
       return;
     case DGB_VEC_TRIG:
-      bx = cos(FMUL(b.p[0], y));
-      by = sin(FMUL(b.p[1], x));
+      velocity_trig(b.p[0], b.p[1], x, y, bx, by);
       return;
     default:
       bx = by = nan("");
@@ -234,6 +260,12 @@ __device__ __forceinline__ Geo element_geo(const double* __restrict__ nodes,
 //  5..7: neighbour local edge lf    8..10: edge kind    11..13: vertices    14: element
 enum { M_NB = 0, M_DIAG = 1, M_SLOT = 2, M_LF = 5, M_KIND = 8, M_VERT = 11 };
 constexpr int kGeo = 13;  // doubles per element: B(4) G(4) det ox oy eps alpha
+
+}  // namespace dgb
+
+#include "assemble_v2.cuh"
+
+namespace dgb {
 
 // ------------------------------------------------------------------------------------------
 // pattern: row_ptr = scan(1 + #interior edges); also resets the error word
@@ -778,6 +810,11 @@ struct dgb_plan {
   int32_t scan_n = 0;
   int last_status = DGB_OK;
   cudaEvent_t ev_start = nullptr, ev_stop = nullptr;  // measurement hook (not owned)
+  std::vector<double> h_tens;   // V1 layout (host copy)
+  std::vector<double> h_P;      // [3][nl*nl] face mass tensors P^l
+  std::vector<double> h_dphi;   // [nqv][2][nl] volume gradients
+  int force_generic = 0;        // testing: always use the generic kernel
+  int minblocks = 0;            // tuning: min resident CTAs/SM for the P2 kernel (0 = default)
 };
 
 namespace {
@@ -840,6 +877,104 @@ void validate_field(const dgb_scalar_field& f, bool element_constant, const char
   }
 }
 
+// Fills the V2 tensor parameter block from the plan's host tensors (W = kappa Q^T - Q is
+// folded per launch) and launches the element-per-thread kernel.
+template <int NL, int NQV, int NQE, bool TRIG, int MINB = 1>
+void launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_problem* problem,
+               const dgb_params* params, dgb_bsr* out, double* rhs, cudaStream_t s) {
+  using L = dgb::v2::Lay<NL, NQV, NQE, TRIG>;
+  using PT = dgb::v2::Params2<NL, NQV, NQE, TRIG>;
+  static_assert(sizeof(PT) <= 32000, "tensor parameter block exceeds the kernel parameter limit");
+  constexpr int N2 = NL * NL;
+  static thread_local PT P;  // ~20 KB: keep it off the stack
+  std::memset(&P, 0, sizeof P);
+  P.nodes = mesh->nodes;
+  P.elements = mesh->elements;
+  P.edge_kind = mesh->edge_kind;
+  P.edge_elements = mesh->edge_elements;
+  P.element_edges = mesh->element_edges;
+  P.row_ptr = out->row_ptr;
+  P.col = out->col;
+  P.val = out->val;
+  P.rhs = rhs;
+  P.err_edge = plan->d_err;
+  P.n_elements = mesh->n_elements;
+  P.drop_neumann = params->neumann_inflow == DGB_INFLOW_DROP;
+  P.kappa = params->kappa;
+  P.sigma_i = params->sigma_interior;
+  P.sigma_b = params->sigma_boundary;
+  P.prob = *problem;
+  const double* h = plan->h_tens.data();
+  const dgb::Layout& V = plan->L;
+  double* x = P.t.x;
+  auto copy = [&](int dst, int src, int n) { std::memcpy(x + dst, h + src, sizeof(double) * n); };
+  copy(L::S, V.S, 3 * N2);
+  copy(L::M, V.M, N2);
+  for (int la = 0; la < 6; ++la) {
+    for (int i = 0; i < NL; ++i) {
+      for (int j = 0; j < NL; ++j) {
+        x[L::W + la * N2 + i * NL + j] =
+            params->kappa * h[V.Q + la * N2 + j * NL + i] - h[V.Q + la * N2 + i * NL + j];
+      }
+    }
+  }
+  if (!TRIG) copy(L::T, V.T, 2 * N2);
+  if (L::kHasTA) copy(L::TA, V.TA, 4 * N2);
+  if (L::kHasP) std::memcpy(x + L::P, plan->h_P.data(), sizeof(double) * 3 * N2);
+  copy(L::PHI, V.PHI, NQV * NL);
+  if (TRIG) std::memcpy(x + L::DPHI, plan->h_dphi.data(), sizeof(double) * NQV * 2 * NL);
+  copy(L::EPHI, V.EPHI, 3 * NQE * NL);
+  copy(L::EDPHI, V.EDPHI, 3 * NQE * 2 * NL);
+  copy(L::VX, V.VX, NQV);
+  copy(L::VY, V.VY, NQV);
+  copy(L::VW, V.VW, NQV);
+  copy(L::ET, V.ET, NQE);
+  copy(L::EW, V.EW, NQE);
+  constexpr int kThreads = 128;
+  const size_t smem =
+      sizeof(double) * (((3 * NQE * 3 * NL + 1) & ~1) +
+                        (kThreads / 32) * 32 * dgb::v2::Stage<N2>::kStride);
+  static bool configured = false;
+  if (!configured) {
+    cuda_check(cudaFuncSetAttribute(dgb::v2::assemble_kernel<NL, NQV, NQE, TRIG, MINB>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(smem)),
+               "cudaFuncSetAttribute(v2)");
+    configured = true;
+  }
+  const int grid = (mesh->n_elements + kThreads - 1) / kThreads;
+  dgb::v2::assemble_kernel<NL, NQV, NQE, TRIG, MINB><<<grid, kThreads, smem, s>>>(P);
+}
+
+// Specialised element-per-thread kernels by (n_local, nq_vol, nq_edge, pointwise velocity);
+// returns false when no specialisation exists (the generic kernel runs instead).
+bool try_launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_problem* problem,
+                   const dgb_params* params, dgb_bsr* out, double* rhs, cudaStream_t s) {
+  if (plan->force_generic) return false;
+  const bool trig = problem->advection.kind == DGB_VEC_TRIG;
+  const int key = plan->nl * 10000 + plan->nqv * 100 + plan->nqe;
+#define DGB_V2(NL_, NQV_, NQE_, TRIG_)                                                     \
+  if (key == NL_ * 10000 + NQV_ * 100 + NQE_ && trig == TRIG_) {                          \
+    launch_v2<NL_, NQV_, NQE_, TRIG_>(plan, mesh, problem, params, out, rhs, s);           \
+    return true;                                                                           \
+  }
+  DGB_V2(3, 6, 2, false)
+  DGB_V2(3, 6, 2, true)
+  if (key == 60703 && !trig && plan->minblocks == 3) {
+    launch_v2<6, 7, 3, false, 3>(plan, mesh, problem, params, out, rhs, s);
+    return true;
+  }
+  if (key == 60703 && !trig && plan->minblocks == 4) {
+    launch_v2<6, 7, 3, false, 4>(plan, mesh, problem, params, out, rhs, s);
+    return true;
+  }
+  DGB_V2(6, 7, 3, false)
+  DGB_V2(6, 12, 3, false)
+  DGB_V2(10, 16, 4, false)
+#undef DGB_V2
+  return false;
+}
+
 // Device allocations freed on scope exit (dgb_assemble_all_host).
 struct Buffers {
   std::vector<void*> ptrs;
@@ -874,6 +1009,31 @@ int dgb_plan_create(const dgb_reference_tables* tables, int32_t device, dgb_plan
       p->L = dgb::make_layout(p->nl, p->nqv, p->nqe);
       p->R = dgb::make_rec(p->nqv, p->nqe);
       const std::vector<double> h = dgb::build_tensors(*tables, p->L);
+      p->h_tens = h;
+      {
+        const int nl = p->nl, ne = p->nqe, n2 = nl * nl;
+        p->h_P.assign(3 * n2, 0.0);
+        for (int l = 0; l < 3; ++l) {
+          for (int i = 0; i < nl; ++i) {
+            for (int j = 0; j < nl; ++j) {
+              long double acc = 0;
+              for (int q = 0; q < ne; ++q) {
+                const double* ph = tables->edge_phi + ((l * 2) * ne + q) * nl;
+                acc += static_cast<long double>(tables->edge_w[q]) * ph[i] * ph[j];
+              }
+              p->h_P[l * n2 + i * nl + j] = static_cast<double>(acc);
+            }
+          }
+        }
+        p->h_dphi.assign(static_cast<size_t>(p->nqv) * 2 * nl, 0.0);
+        for (int q = 0; q < p->nqv; ++q) {
+          for (int a = 0; a < 2; ++a) {
+            for (int i = 0; i < nl; ++i) {
+              p->h_dphi[(q * 2 + a) * nl + i] = tables->dphi[(q * nl + i) * 2 + a];
+            }
+          }
+        }
+      }
       cuda_check(cudaMalloc(&p->d_tens, h.size() * sizeof(double)), "cudaMalloc(tensors)");
       cuda_check(cudaMemcpy(p->d_tens, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice),
                  "cudaMemcpy(tensors)");
@@ -979,7 +1139,7 @@ int dgb_assemble(dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_problem*
     const size_t smem = static_cast<size_t>(P.tile) * (plan->R.size + dgb::kGeo) * sizeof(double) +
                         static_cast<size_t>(P.tile) * (dgb::kMeta + 4) * sizeof(int) + 16;
     if (plan->ev_start) cuda_check(cudaEventRecord(plan->ev_start, s), "cudaEventRecord");
-    switch (plan->nl) {
+    if (!try_launch_v2(plan, mesh, problem, params, out, rhs, s)) switch (plan->nl) {
       case 3: launch_assemble<3>(P, n_tiles, smem, s); break;
       case 6: launch_assemble<6>(P, n_tiles, smem, s); break;
       case 10: launch_assemble<10>(P, n_tiles, smem, s); break;
@@ -998,6 +1158,15 @@ int dgb_plan_set_kernel_events(dgb_plan* plan, void* start, void* stop) {
   plan->ev_start = static_cast<cudaEvent_t>(start);
   plan->ev_stop = static_cast<cudaEvent_t>(stop);
   return DGB_OK;
+}
+
+int dgb_plan_set_option(dgb_plan* plan, int32_t option, int32_t value) {
+  if (!plan) return DGB_STATUS_INVALID_ARGUMENT;
+  switch (option) {
+    case DGB_OPTION_FORCE_GENERIC_KERNEL: plan->force_generic = value; return DGB_OK;
+    case DGB_OPTION_MIN_BLOCKS: plan->minblocks = value; return DGB_OK;
+    default: return DGB_STATUS_INVALID_ARGUMENT;
+  }
 }
 
 // count_blocks_kernel + cub scan (init + scan kernels) + assemble_kernel

@@ -246,6 +246,13 @@ class Plan:
         self.device = device
         self.n_local = tables.n_local
 
+    def set_option(self, option: int, value: int) -> None:
+        _check(self._lib.dgb_plan_set_option(self._h, option, value))
+
+    def set_generic(self, on: bool = True) -> None:
+        """Force the generic block-row kernel (testing)."""
+        _check(self._lib.dgb_plan_set_option(self._h, capi.OPTION_FORCE_GENERIC_KERNEL, int(on)))
+
     def allocate(self, dmesh: DeviceMesh) -> BsrSystem:
         import torch
         dev = torch.device("cuda", self.device)
@@ -289,10 +296,12 @@ class Plan:
 
 
 def assemble_all(mesh: Mesh, ref: ReferenceElement, problem: ProblemSpec, params: Params,
-                 device: int = 0) -> BsrSystem:
+                 device: int = 0, generic: bool = False) -> BsrSystem:
     """`dgfem::assemble_all(mesh, ref, problem, params)` + `stiffness()` on the GPU: returns
     K (BSR) and F as device tensors.  Raises Error like the reference."""
     plan = Plan(ref.view, device)
+    if generic:
+        plan.set_generic(True)
     dmesh = DeviceMesh(mesh, device)
     dprob = DeviceProblem(problem, device)
     out = plan.allocate(dmesh)

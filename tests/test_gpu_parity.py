@@ -71,3 +71,33 @@ def test_configs_full_size_sampled_rows(oracle, index):
         assert g[0][-1] == mesh.n_elements + 2 * mesh.n_interior_edges
         o = oracle.assemble(mesh.arrays(), ref.tables(), spec.c, params, rows=rows)
         compare_system(gather_rows(*g, rows), o)
+
+
+@pytest.mark.parametrize("index", [1, 2, 3, 4, 5])
+def test_generic_kernel_matches_oracle(oracle, index):
+    """The generic (any quadrature) block-row kernel stays parity-green too."""
+    import torch
+    cfg = problems.CONFIGS[index]
+    mesh = dgfem.unit_square_mesh(10, cfg.jitter, problems.SEED_JITTER, cfg.permute,
+                                  problems.SEED_PERMUTE, cfg.neumann_sides)
+    ref = dgfem.ReferenceElement(cfg.degree, cfg.quad_order)
+    spec = problems.config_problem(index, mesh.n_elements)
+    params = dgfem.config_parameters(cfg, cfg.methods[-1])
+    s = dgfem.assemble_all(mesh, ref, spec, params, generic=True)
+    torch.cuda.synchronize()
+    g = (s.row_ptr.cpu().numpy(), s.col.cpu().numpy(), s.val.cpu().numpy(), s.rhs.cpu().numpy())
+    compare_system(g, oracle.assemble(mesh.arrays(), ref.tables(), spec.c, params))
+
+
+def test_velocity_kinds_on_p1(oracle):
+    """Constant, affine and trigonometric velocities through the specialised P1 kernels."""
+    mesh = dgfem.unit_square_mesh(9, 0.2, 5, True, 6, 0)
+    ref = dgfem.ReferenceElement(1, 3)
+    for b in (problems.vec_constant(0.3, -0.7), problems.vec_affine(0.5, -0.5, 0.0, -1.0, 1.0, 0.0),
+              problems.vec_trig(2 * problems.PI, 2 * problems.PI)):
+        spec = problems.config_problem(1)
+        spec.c.advection = b
+        for method in (capi.SIPG, capi.NIPG, capi.IIPG):
+            params = dgfem.set_parameters(method, 1)
+            compare_system(run_gpu(mesh, ref, spec, params),
+                           oracle.assemble(mesh.arrays(), ref.tables(), spec.c, params))
