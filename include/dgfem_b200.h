@@ -108,6 +108,13 @@ int dgb_mesh_build(const double* nodes_xy, int32_t n_nodes, const int32_t* eleme
 int dgb_mesh_unit_square(int32_t n, double jitter, uint64_t jitter_seed, int32_t permute,
                          uint64_t permute_seed, int32_t neumann_sides, dgb_mesh** out);
 
+/* The same construction on [0, lx] x [0, ly] with nx x ny cells (sides 1: x=0, 2: x=lx, 4: y=0,
+ * 8: y=ly).  dgb_mesh_unit_square(n, ...) == dgb_mesh_rectangle(n, n, 1, 1, ...).  Used for the
+ * weak-scaling global mesh of the multi-GPU benchmark (N x 1 strip of config-sized squares). */
+int dgb_mesh_rectangle(int32_t nx, int32_t ny, double lx, double ly, double jitter,
+                       uint64_t jitter_seed, int32_t permute, uint64_t permute_seed,
+                       int32_t neumann_sides, dgb_mesh** out);
+
 /* Pointers into the mesh's own storage (valid until dgb_mesh_free). */
 int dgb_mesh_view(const dgb_mesh* mesh, dgb_mesh_arrays* out);
 /* The input that produced the mesh: nodes, elements before reorientation, and the boundary
@@ -265,6 +272,18 @@ void dgb_plan_destroy(dgb_plan* plan);
  * and collect InflowOnNeumann (only possible with DGB_INFLOW_ERROR and Neumann edges). */
 int dgb_assemble(dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_problem* problem,
                  const dgb_params* params, dgb_bsr* out, double* rhs, void* stream);
+
+/* Shard form of dgb_assemble: block rows [row_begin, row_end) only.  `out`
+ * holds those rows (row_ptr relative to the shard, starting at 0; block columns global) and
+ * rhs their F slices; out->nnzb from dgb_count_blocks_host.  The mesh arrays are the full mesh
+ * (device).  No collective is needed: shards are independent and their global block offsets
+ * are a prefix sum of the shard block counts. */
+int dgb_assemble_rows(dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_problem* problem,
+                      const dgb_params* params, int32_t row_begin, int32_t row_end, dgb_bsr* out,
+                      double* rhs, void* stream);
+
+/* Number of BSR blocks of block rows [row_begin, row_end) of a HOST mesh (-1 on bad input). */
+int64_t dgb_count_blocks_host(const dgb_mesh_arrays* mesh, int32_t row_begin, int32_t row_end);
 
 /* Waits for the plan's last dgb_assemble on `stream` and returns its status
  * (DGB_STATUS_INFLOW_ON_NEUMANN with detail = lowest offending edge, as the reference's

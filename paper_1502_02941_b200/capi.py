@@ -98,6 +98,8 @@ def _declare(lib: C.CDLL) -> C.CDLL:
                                      C.c_int32, P(vp)]),
         "dgb_mesh_unit_square": (C.c_int, [C.c_int32, C.c_double, C.c_uint64, C.c_int32,
                                            C.c_uint64, C.c_int32, P(vp)]),
+        "dgb_mesh_rectangle": (C.c_int, [C.c_int32, C.c_int32, C.c_double, C.c_double, C.c_double,
+                                         C.c_uint64, C.c_int32, C.c_uint64, C.c_int32, P(vp)]),
         "dgb_mesh_view": (C.c_int, [vp, P(MeshArrays)]),
         "dgb_mesh_raw": (C.c_int, [vp, P(vp), P(C.c_int32), P(vp), P(C.c_int32), P(vp),
                                    P(C.c_int32), P(vp), P(C.c_int32)]),
@@ -115,6 +117,9 @@ def _declare(lib: C.CDLL) -> C.CDLL:
         "dgb_assemble_launch_count": (C.c_int32, []),
         "dgb_plan_set_option": (C.c_int, [vp, C.c_int32, C.c_int32]),
         "dgb_spmv": (C.c_int, [P(Bsr), vp, vp, vp]),
+        "dgb_assemble_rows": (C.c_int, [vp, P(MeshArrays), P(Problem), P(Params), C.c_int32,
+                                        C.c_int32, P(Bsr), vp, vp]),
+        "dgb_count_blocks_host": (C.c_int64, [P(MeshArrays), C.c_int32, C.c_int32]),
         "dgb_assemble_all_host": (C.c_int, [P(MeshArrays), P(ReferenceTables), P(Problem),
                                             P(Params), C.c_int32, P(Bsr), vp]),
     }
@@ -132,6 +137,7 @@ EXPORTED_SYMBOLS = [
     "dgb_set_parameters", "dgb_bsr_nnzb", "dgb_plan_create", "dgb_plan_destroy",
     "dgb_assemble", "dgb_plan_status", "dgb_plan_set_kernel_events",
     "dgb_assemble_launch_count", "dgb_plan_set_option", "dgb_spmv", "dgb_assemble_all_host",
+    "dgb_mesh_rectangle", "dgb_assemble_rows", "dgb_count_blocks_host",
 ]
 OPTION_FORCE_GENERIC_KERNEL = 1
 OPTION_MIN_BLOCKS = 2

@@ -62,6 +62,7 @@ struct Params2 {
   double* rhs;
   int32_t* err_edge;
   int32_t n_elements;
+  int32_t row_begin, row_end;  // block rows [row_begin, row_end) of this launch (a shard)
   int32_t drop_neumann;
   double kappa, sigma_i, sigma_b;
   dgb_problem prob;
@@ -145,9 +146,9 @@ __global__ void __launch_bounds__(128, MINB) assemble_kernel(
   constexpr int SS = Stage<N2>::kStride;
   double* stw = smem + ((kTr + 1) & ~1) + warp * 32 * SS;
   double* st = stw + lane * SS;
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  const bool active = e < P.n_elements;
-  const int ee = active ? e : P.n_elements - 1;  // inactive lanes mirror a valid element
+  const int e = P.row_begin + blockIdx.x * blockDim.x + threadIdx.x;
+  const bool active = e < P.row_end;
+  const int ee = active ? e : P.row_end - 1;  // inactive lanes mirror a valid element
 
   // ---- element geometry and edge states ---------------------------------------------------
   int v[3];
@@ -223,7 +224,7 @@ __global__ void __launch_bounds__(128, MINB) assemble_kernel(
       }
     }
   }
-  const int rp = __ldg(P.row_ptr + ee);
+  const int rp = __ldg(P.row_ptr + (ee - P.row_begin));
   int diag_slot = 0;
 #pragma unroll
   for (int s = 0; s < 4; ++s) {
@@ -544,8 +545,8 @@ __global__ void __launch_bounds__(128, MINB) assemble_kernel(
 #pragma unroll
     for (int i = 0; i < NL; ++i) st[i] = F[i];
     __syncwarp();
-    const int e_first = blockIdx.x * blockDim.x + warp * 32;
-    const int n_here = min(32, P.n_elements - e_first);
+    const int e_first = blockIdx.x * blockDim.x + warp * 32;  // relative to row_begin
+    const int n_here = min(32, P.row_end - P.row_begin - e_first);
     for (int idx = lane; idx < n_here * NL; idx += 32) {
       const int L = idx / NL, i = idx - L * NL;
       P.rhs[static_cast<long long>(e_first) * NL + idx] = stw[L * SS + i];

@@ -73,6 +73,7 @@ struct KParams {
   const int32_t* edge_elements;
   const int32_t* element_edges;
   int32_t n_elements;
+  int32_t row_begin, row_end;  // block rows of this launch
   // problem (by value; per-element pointers are device pointers)
   dgb_problem prob;
   double kappa, sigma_i, sigma_b;
@@ -271,20 +272,21 @@ namespace dgb {
 // pattern: row_ptr = scan(1 + #interior edges); also resets the error word
 // ------------------------------------------------------------------------------------------
 __global__ void count_blocks_kernel(const uint8_t* __restrict__ edge_kind,
-                                    const int32_t* __restrict__ element_edges, int32_t n,
-                                    int32_t* __restrict__ row_ptr, int32_t* err_edge) {
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e == 0) {
+                                    const int32_t* __restrict__ element_edges, int32_t begin,
+                                    int32_t n, int32_t* __restrict__ row_ptr, int32_t* err_edge) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r == 0) {
     row_ptr[0] = 0;
     *err_edge = INT_MAX;
   }
-  if (e >= n) return;
+  if (r >= n) return;
+  const int e = begin + r;
   int c = 1;
 #pragma unroll
   for (int l = 0; l < 3; ++l) {
     c += __ldg(edge_kind + __ldg(element_edges + 3 * e + l)) == DGB_EDGE_INTERIOR;
   }
-  row_ptr[e + 1] = c;
+  row_ptr[r + 1] = c;
 }
 
 // ------------------------------------------------------------------------------------------
@@ -295,8 +297,8 @@ __global__ void __launch_bounds__(256) assemble_kernel(const __grid_constant__ K
   extern __shared__ double smem[];
   constexpr int NL2 = NL * NL;
   const int TE = P.tile;
-  const int e0 = blockIdx.x * TE;
-  const int ne = min(TE, P.n_elements - e0);
+  const int e0 = P.row_begin + blockIdx.x * TE;
+  const int ne = min(TE, P.row_end - e0);
   const int nqv = P.nqv, nqe = P.nqe;
   const Rec& R = P.R;
   const Layout& L = P.L;
@@ -349,7 +351,7 @@ __global__ void __launch_bounds__(256) assemble_kernel(const __grid_constant__ K
       }
     }
     m[M_NB] = nb;
-    const int base = __ldg(P.row_ptr + e);
+    const int base = __ldg(P.row_ptr + (e - P.row_begin));
     for (int s = 0; s < nb; ++s) {
       P.col[base + s] = cols[s];
       if (kinds[s] < 0) m[M_DIAG] = s; else m[M_SLOT + kinds[s]] = s;
@@ -549,7 +551,7 @@ __global__ void __launch_bounds__(256) assemble_kernel(const __grid_constant__ K
 
   // ---- B: block-row values, streamed in output order ---------------------------------------
   const int nblk = *s_nblk;
-  const long long vbase = static_cast<long long>(__ldg(P.row_ptr + e0)) * NL2;
+  const long long vbase = static_cast<long long>(__ldg(P.row_ptr + (e0 - P.row_begin))) * NL2;
   const int bkind = P.prob.advection.kind;
   const double kappa = P.kappa;
   for (int g = threadIdx.x; g < nblk * NL2; g += blockDim.x) {
@@ -622,7 +624,7 @@ __global__ void __launch_bounds__(256) assemble_kernel(const __grid_constant__ K
         v = fma(r[R.cH + row], dn, v);
       }
     }
-    P.rhs[static_cast<long long>(e0 + el) * NL + i] = v;
+    P.rhs[static_cast<long long>(e0 - P.row_begin + el) * NL + i] = v;
   }
 }
 
@@ -881,7 +883,8 @@ void validate_field(const dgb_scalar_field& f, bool element_constant, const char
 // folded per launch) and launches the element-per-thread kernel.
 template <int NL, int NQV, int NQE, bool TRIG, int MINB = 1>
 void launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_problem* problem,
-               const dgb_params* params, dgb_bsr* out, double* rhs, cudaStream_t s) {
+               const dgb_params* params, dgb_bsr* out, double* rhs, cudaStream_t s,
+               int out_row_begin, int out_row_end) {
   using L = dgb::v2::Lay<NL, NQV, NQE, TRIG>;
   using PT = dgb::v2::Params2<NL, NQV, NQE, TRIG>;
   static_assert(sizeof(PT) <= 32000, "tensor parameter block exceeds the kernel parameter limit");
@@ -899,6 +902,8 @@ void launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_prob
   P.rhs = rhs;
   P.err_edge = plan->d_err;
   P.n_elements = mesh->n_elements;
+  P.row_begin = out_row_begin;
+  P.row_end = out_row_end;
   P.drop_neumann = params->neumann_inflow == DGB_INFLOW_DROP;
   P.kappa = params->kappa;
   P.sigma_i = params->sigma_interior;
@@ -942,30 +947,31 @@ void launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_prob
                "cudaFuncSetAttribute(v2)");
     configured = true;
   }
-  const int grid = (mesh->n_elements + kThreads - 1) / kThreads;
+  const int grid = (out_row_end - out_row_begin + kThreads - 1) / kThreads;
   dgb::v2::assemble_kernel<NL, NQV, NQE, TRIG, MINB><<<grid, kThreads, smem, s>>>(P);
 }
 
 // Specialised element-per-thread kernels by (n_local, nq_vol, nq_edge, pointwise velocity);
 // returns false when no specialisation exists (the generic kernel runs instead).
 bool try_launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_problem* problem,
-                   const dgb_params* params, dgb_bsr* out, double* rhs, cudaStream_t s) {
+                   const dgb_params* params, dgb_bsr* out, double* rhs, cudaStream_t s,
+                   int rb, int re) {
   if (plan->force_generic) return false;
   const bool trig = problem->advection.kind == DGB_VEC_TRIG;
   const int key = plan->nl * 10000 + plan->nqv * 100 + plan->nqe;
 #define DGB_V2(NL_, NQV_, NQE_, TRIG_)                                                     \
   if (key == NL_ * 10000 + NQV_ * 100 + NQE_ && trig == TRIG_) {                          \
-    launch_v2<NL_, NQV_, NQE_, TRIG_>(plan, mesh, problem, params, out, rhs, s);           \
+    launch_v2<NL_, NQV_, NQE_, TRIG_>(plan, mesh, problem, params, out, rhs, s, rb, re);           \
     return true;                                                                           \
   }
   DGB_V2(3, 6, 2, false)
   DGB_V2(3, 6, 2, true)
   if (key == 60703 && !trig && plan->minblocks == 3) {
-    launch_v2<6, 7, 3, false, 3>(plan, mesh, problem, params, out, rhs, s);
+    launch_v2<6, 7, 3, false, 3>(plan, mesh, problem, params, out, rhs, s, rb, re);
     return true;
   }
   if (key == 60703 && !trig && plan->minblocks == 4) {
-    launch_v2<6, 7, 3, false, 4>(plan, mesh, problem, params, out, rhs, s);
+    launch_v2<6, 7, 3, false, 4>(plan, mesh, problem, params, out, rhs, s, rb, re);
     return true;
   }
   DGB_V2(6, 7, 3, false)
@@ -1061,8 +1067,9 @@ void dgb_plan_destroy(dgb_plan* p) {
   delete p;
 }
 
-int dgb_assemble(dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_problem* problem,
-                 const dgb_params* params, dgb_bsr* out, double* rhs, void* stream) {
+int dgb_assemble_rows(dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_problem* problem,
+                      const dgb_params* params, int32_t row_begin, int32_t row_end, dgb_bsr* out,
+                      double* rhs, void* stream) {
   return dgb::guarded([&] {
     if (!plan || !mesh || !problem || !params || !out || !rhs) {
       throw dgb::Error(DGB_STATUS_INVALID_ARGUMENT, "null argument");
@@ -1079,20 +1086,23 @@ int dgb_assemble(dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_problem*
     if (problem->advection.kind < DGB_VEC_CONSTANT || problem->advection.kind > DGB_VEC_TRIG) {
       throw dgb::Error(DGB_STATUS_INVALID_ARGUMENT, "unknown velocity kind");
     }
-    if (out->block_dim != plan->nl || out->n_block_rows != mesh->n_elements ||
-        out->nnzb != dgb_bsr_nnzb(mesh->n_elements, mesh->n_interior_edges)) {
-      throw dgb::Error(DGB_STATUS_DIMENSION_MISMATCH, "BSR output does not match mesh / plan");
+    if (row_begin < 0 || row_end > mesh->n_elements || row_begin > row_end) {
+      throw dgb::Error(DGB_STATUS_INVALID_INDEX, "block row range outside the mesh", row_begin);
+    }
+    if (out->block_dim != plan->nl || out->n_block_rows != row_end - row_begin) {
+      throw dgb::Error(DGB_STATUS_DIMENSION_MISMATCH, "BSR output does not match rows / plan");
     }
     DeviceGuard guard(plan->device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    const int E = mesh->n_elements;
+    const int E = row_end - row_begin;
     plan->last_status = DGB_OK;
     if (E == 0) {
+      cuda_check(cudaMemsetAsync(out->row_ptr, 0, sizeof(int32_t), s), "cudaMemsetAsync");
       return;
     }
     // pattern: counts -> inclusive scan into row_ptr[1..E]
-    dgb::count_blocks_kernel<<<(E + 255) / 256, 256, 0, s>>>(mesh->edge_kind, mesh->element_edges,
-                                                             E, out->row_ptr, plan->d_err);
+    dgb::count_blocks_kernel<<<(E + 255) / 256, 256, 0, s>>>(
+        mesh->edge_kind, mesh->element_edges, row_begin, E, out->row_ptr, plan->d_err);
     cuda_check(cudaGetLastError(), "count_blocks_kernel");
     if (plan->scan_n != E) {
       size_t bytes = 0;
@@ -1110,47 +1120,74 @@ int dgb_assemble(dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_problem*
                                              out->row_ptr + 1, E, s),
                "DeviceScan");
 
-    dgb::KParams P;
-    std::memset(&P, 0, sizeof P);
-    P.nodes = mesh->nodes;
-    P.elements = mesh->elements;
-    P.edge_kind = mesh->edge_kind;
-    P.edge_elements = mesh->edge_elements;
-    P.element_edges = mesh->element_edges;
-    P.n_elements = E;
-    P.prob = *problem;
-    P.kappa = params->kappa;
-    P.sigma_i = params->sigma_interior;
-    P.sigma_b = params->sigma_boundary;
-    P.drop_neumann = params->neumann_inflow == DGB_INFLOW_DROP;
-    P.tens = plan->d_tens;
-    P.L = plan->L;
-    P.R = plan->R;
-    P.nl = plan->nl;
-    P.nqv = plan->nqv;
-    P.nqe = plan->nqe;
-    P.tile = dgb::tile_for(plan->nl);
-    P.row_ptr = out->row_ptr;
-    P.col = out->col;
-    P.val = out->val;
-    P.rhs = rhs;
-    P.err_edge = plan->d_err;
-    const int n_tiles = (E + P.tile - 1) / P.tile;
-    const size_t smem = static_cast<size_t>(P.tile) * (plan->R.size + dgb::kGeo) * sizeof(double) +
-                        static_cast<size_t>(P.tile) * (dgb::kMeta + 4) * sizeof(int) + 16;
     if (plan->ev_start) cuda_check(cudaEventRecord(plan->ev_start, s), "cudaEventRecord");
-    if (!try_launch_v2(plan, mesh, problem, params, out, rhs, s)) switch (plan->nl) {
-      case 3: launch_assemble<3>(P, n_tiles, smem, s); break;
-      case 6: launch_assemble<6>(P, n_tiles, smem, s); break;
-      case 10: launch_assemble<10>(P, n_tiles, smem, s); break;
-      case 15: launch_assemble<15>(P, n_tiles, smem, s); break;
-      default: throw dgb::Error(DGB_STATUS_UNSUPPORTED_DEGREE, "unsupported n_local", plan->nl);
+    if (!try_launch_v2(plan, mesh, problem, params, out, rhs, s, row_begin, row_end)) {
+      dgb::KParams P;
+      std::memset(&P, 0, sizeof P);
+      P.nodes = mesh->nodes;
+      P.elements = mesh->elements;
+      P.edge_kind = mesh->edge_kind;
+      P.edge_elements = mesh->edge_elements;
+      P.element_edges = mesh->element_edges;
+      P.n_elements = mesh->n_elements;
+      P.row_begin = row_begin;
+      P.row_end = row_end;
+      P.prob = *problem;
+      P.kappa = params->kappa;
+      P.sigma_i = params->sigma_interior;
+      P.sigma_b = params->sigma_boundary;
+      P.drop_neumann = params->neumann_inflow == DGB_INFLOW_DROP;
+      P.tens = plan->d_tens;
+      P.L = plan->L;
+      P.R = plan->R;
+      P.nl = plan->nl;
+      P.nqv = plan->nqv;
+      P.nqe = plan->nqe;
+      P.tile = dgb::tile_for(plan->nl);
+      P.row_ptr = out->row_ptr;
+      P.col = out->col;
+      P.val = out->val;
+      P.rhs = rhs;
+      P.err_edge = plan->d_err;
+      const int n_tiles = (E + P.tile - 1) / P.tile;
+      const size_t smem =
+          static_cast<size_t>(P.tile) * (plan->R.size + dgb::kGeo) * sizeof(double) +
+          static_cast<size_t>(P.tile) * (dgb::kMeta + 4) * sizeof(int) + 16;
+      switch (plan->nl) {
+        case 3: launch_assemble<3>(P, n_tiles, smem, s); break;
+        case 6: launch_assemble<6>(P, n_tiles, smem, s); break;
+        case 10: launch_assemble<10>(P, n_tiles, smem, s); break;
+        case 15: launch_assemble<15>(P, n_tiles, smem, s); break;
+        default: throw dgb::Error(DGB_STATUS_UNSUPPORTED_DEGREE, "unsupported n_local", plan->nl);
+      }
     }
     cuda_check(cudaGetLastError(), "assemble_kernel");
     if (plan->ev_stop) cuda_check(cudaEventRecord(plan->ev_stop, s), "cudaEventRecord");
     cuda_check(cudaMemcpyAsync(plan->h_err, plan->d_err, sizeof(int32_t), cudaMemcpyDeviceToHost, s),
                "cudaMemcpyAsync(err)");
   });
+}
+
+int dgb_assemble(dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_problem* problem,
+                 const dgb_params* params, dgb_bsr* out, double* rhs, void* stream) {
+  if (mesh && out && out->nnzb != dgb_bsr_nnzb(mesh->n_elements, mesh->n_interior_edges)) {
+    return dgb::record_error(DGB_STATUS_DIMENSION_MISMATCH,
+                             "DimensionMismatch: BSR output does not match mesh", -1);
+  }
+  return dgb_assemble_rows(plan, mesh, problem, params, 0, mesh ? mesh->n_elements : 0, out, rhs,
+                           stream);
+}
+
+int64_t dgb_count_blocks_host(const dgb_mesh_arrays* mesh, int32_t row_begin, int32_t row_end) {
+  if (!mesh || row_begin < 0 || row_end > mesh->n_elements || row_begin > row_end) return -1;
+  int64_t n = 0;
+  for (int32_t e = row_begin; e < row_end; ++e) {
+    n += 1;
+    for (int l = 0; l < 3; ++l) {
+      n += mesh->edge_kind[mesh->element_edges[3 * static_cast<int64_t>(e) + l]] == DGB_EDGE_INTERIOR;
+    }
+  }
+  return n;
 }
 
 int dgb_plan_set_kernel_events(dgb_plan* plan, void* start, void* stop) {

@@ -210,36 +210,40 @@ int dgb_mesh_build(const double* nodes_xy, int32_t n_nodes, const int32_t* eleme
   });
 }
 
-int dgb_mesh_unit_square(int32_t n, double jitter, uint64_t jitter_seed, int32_t permute,
-                         uint64_t permute_seed, int32_t neumann_sides, dgb_mesh** out) {
+int dgb_mesh_rectangle(int32_t nx, int32_t ny, double lx, double ly, double jitter,
+                       uint64_t jitter_seed, int32_t permute, uint64_t permute_seed,
+                       int32_t neumann_sides, dgb_mesh** out) {
   *out = nullptr;
   return dgb::guarded([&] {
-    if (n < 1 || n > 16384) throw dgb::Error(DGB_STATUS_INVALID_ARGUMENT, "n out of range", n);
+    if (nx < 1 || ny < 1 || static_cast<int64_t>(nx) * ny > (int64_t{1} << 29)) {
+      throw dgb::Error(DGB_STATUS_INVALID_ARGUMENT, "grid size out of range", nx);
+    }
+    if (!(lx > 0.0 && ly > 0.0)) throw dgb::Error(DGB_STATUS_INVALID_ARGUMENT, "bad extent");
     if (!(jitter >= 0.0 && jitter < 0.5)) {
       throw dgb::Error(DGB_STATUS_INVALID_ARGUMENT, "jitter must be in [0, 0.5)");
     }
     auto* m = new dgb_mesh();
     try {
-      const int64_t np = static_cast<int64_t>(n) + 1;
-      auto node = [np](int64_t i, int64_t j) { return static_cast<int32_t>(j * np + i); };
-      m->raw_nodes.resize(2 * np * np);
-      const double h = 1.0 / n;
+      const int64_t px = static_cast<int64_t>(nx) + 1, py = static_cast<int64_t>(ny) + 1;
+      auto node = [px](int64_t i, int64_t j) { return static_cast<int32_t>(j * px + i); };
+      m->raw_nodes.resize(2 * px * py);
+      const double hx = lx / nx, hy = ly / ny;
       SplitMix64 rng{jitter_seed};
-      for (int64_t j = 0; j < np; ++j) {
-        for (int64_t i = 0; i < np; ++i) {
-          double x = static_cast<double>(i) / n, y = static_cast<double>(j) / n;
-          if (jitter > 0.0 && i > 0 && i < n && j > 0 && j < n) {
-            x += (2.0 * rng.uniform() - 1.0) * (jitter * h);
-            y += (2.0 * rng.uniform() - 1.0) * (jitter * h);
+      for (int64_t j = 0; j < py; ++j) {
+        for (int64_t i = 0; i < px; ++i) {
+          double x = lx * (static_cast<double>(i) / nx), y = ly * (static_cast<double>(j) / ny);
+          if (jitter > 0.0 && i > 0 && i < nx && j > 0 && j < ny) {
+            x += (2.0 * rng.uniform() - 1.0) * (jitter * hx);
+            y += (2.0 * rng.uniform() - 1.0) * (jitter * hy);
           }
           m->raw_nodes[2 * node(i, j)] = x;
           m->raw_nodes[2 * node(i, j) + 1] = y;
         }
       }
-      m->raw_elements.resize(6 * static_cast<int64_t>(n) * n);
-      for (int64_t j = 0; j < n; ++j) {
-        for (int64_t i = 0; i < n; ++i) {
-          const int64_t c = j * n + i;
+      m->raw_elements.resize(6 * static_cast<int64_t>(nx) * ny);
+      for (int64_t j = 0; j < ny; ++j) {
+        for (int64_t i = 0; i < nx; ++i) {
+          const int64_t c = j * nx + i;
           const int32_t v00 = node(i, j), v10 = node(i + 1, j), v01 = node(i, j + 1),
                         v11 = node(i + 1, j + 1);
           int32_t* lo = &m->raw_elements[6 * c];
@@ -249,23 +253,23 @@ int dgb_mesh_unit_square(int32_t n, double jitter, uint64_t jitter_seed, int32_t
       }
       if (permute) {  // Fisher-Yates over the element list (config 4)
         SplitMix64 prng{permute_seed};
-        const int64_t ne = 2 * static_cast<int64_t>(n) * n;
+        const int64_t ne = 2 * static_cast<int64_t>(nx) * ny;
         for (int64_t i = ne - 1; i > 0; --i) {
           const int64_t k = static_cast<int64_t>(prng.next() % static_cast<uint64_t>(i + 1));
           for (int t = 0; t < 3; ++t) std::swap(m->raw_elements[3 * i + t], m->raw_elements[3 * k + t]);
         }
       }
-      auto side = [&](int bit, int64_t i0, int64_t j0, int64_t di, int64_t dj) {
+      auto side = [&](int bit, int64_t i0, int64_t j0, int64_t di, int64_t dj, int64_t count) {
         auto& list = (neumann_sides & bit) ? m->raw_neumann : m->raw_dirichlet;
-        for (int64_t s = 0; s < n; ++s) {
+        for (int64_t s = 0; s < count; ++s) {
           list.push_back(node(i0 + s * di, j0 + s * dj));
           list.push_back(node(i0 + (s + 1) * di, j0 + (s + 1) * dj));
         }
       };
-      side(4, 0, 0, 1, 0);  // y = 0
-      side(8, 0, n, 1, 0);  // y = 1
-      side(1, 0, 0, 0, 1);  // x = 0
-      side(2, n, 0, 0, 1);  // x = 1
+      side(4, 0, 0, 1, 0, nx);   // y = 0
+      side(8, 0, ny, 1, 0, nx);  // y = ly
+      side(1, 0, 0, 0, 1, ny);   // x = 0
+      side(2, nx, 0, 0, 1, ny);  // x = lx
       build(*m);
     } catch (...) {
       delete m;
@@ -273,6 +277,16 @@ int dgb_mesh_unit_square(int32_t n, double jitter, uint64_t jitter_seed, int32_t
     }
     *out = m;
   });
+}
+
+int dgb_mesh_unit_square(int32_t n, double jitter, uint64_t jitter_seed, int32_t permute,
+                         uint64_t permute_seed, int32_t neumann_sides, dgb_mesh** out) {
+  if (n < 1 || n > 16384) {
+    *out = nullptr;
+    return dgb::record_error(DGB_STATUS_INVALID_ARGUMENT, "InvalidArgument: n out of range", n);
+  }
+  return dgb_mesh_rectangle(n, n, 1.0, 1.0, jitter, jitter_seed, permute, permute_seed,
+                            neumann_sides, out);
 }
 
 int dgb_mesh_view(const dgb_mesh* m, dgb_mesh_arrays* out) {

@@ -115,10 +115,26 @@ def unit_square_mesh(n: int, jitter: float = 0.0, jitter_seed: int = 0, permute:
     return Mesh(h)
 
 
-def config_mesh(cfg) -> Mesh:
+def rectangle_mesh(nx: int, ny: int, lx: float, ly: float, jitter: float = 0.0,
+                   jitter_seed: int = 0, permute: bool = False, permute_seed: int = 0,
+                   neumann_sides: int = 0) -> Mesh:
+    """dgb_mesh_rectangle: the same construction on [0, lx] x [0, ly]."""
+    lib = capi.load()
+    h = C.c_void_p()
+    _check(lib.dgb_mesh_rectangle(nx, ny, lx, ly, jitter, jitter_seed, int(permute),
+                                  permute_seed, neumann_sides, C.byref(h)))
+    return Mesh(h)
+
+
+def config_mesh(cfg, strips: int = 1) -> Mesh:
+    """Config mesh; strips > 1 gives the weak-scaling global mesh ([0, strips] x [0, 1], i.e.
+    `strips` config-sized squares side by side).  strips = 1 is the config's unit square."""
     from .problems import SEED_JITTER, SEED_PERMUTE
-    return unit_square_mesh(cfg.n, cfg.jitter, SEED_JITTER, cfg.permute, SEED_PERMUTE,
-                            cfg.neumann_sides)
+    if strips == 1:
+        return unit_square_mesh(cfg.n, cfg.jitter, SEED_JITTER, cfg.permute, SEED_PERMUTE,
+                                cfg.neumann_sides)
+    return rectangle_mesh(strips * cfg.n, cfg.n, float(strips), 1.0, cfg.jitter, SEED_JITTER,
+                          cfg.permute, SEED_PERMUTE, cfg.neumann_sides)
 
 
 # ------------------------------------------------------------------------------ reference

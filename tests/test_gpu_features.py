@@ -1,0 +1,229 @@
+"""GPU: SpMV, error reporting, determinism, the host-buffer drop-in entry, shards, and
+size-independent properties at full BASELINE sizes."""
+import numpy as np
+import pytest
+
+from helpers import compare_system, gather_rows
+from oracle.oracle import OracleLib, bsr_to_csr
+from paper_1502_02941_b200 import capi, dgfem, problems, shard
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def oracle():
+    return OracleLib()
+
+
+def to_np(s):
+    return (s.row_ptr.cpu().numpy(), s.col.cpu().numpy(), s.val.cpu().numpy(), s.rhs.cpu().numpy())
+
+
+def test_spmv_matches_oracle_config4_size(oracle):
+    """Config 4 (2048^2 x 2, P1, permuted) K x for seeded U[-1,1] x: |dy_i| <= 1e-12 sum_j |K_ij x_j|
+    (SURVEY.md §8(c)); 100 products reuse the same K (bench --config 4 times them)."""
+    import torch
+    cfg = problems.CONFIGS[4]
+    mesh = dgfem.config_mesh(cfg)
+    ref = dgfem.ReferenceElement(cfg.degree, cfg.quad_order)
+    spec = problems.config_problem(4)
+    params = dgfem.config_parameters(cfg, capi.SIPG)
+    plan = dgfem.Plan(ref.view)
+    dm, dp = dgfem.DeviceMesh(mesh), dgfem.DeviceProblem(spec)
+    out = plan.assemble(dm, dp, params, plan.allocate(dm))
+    n = mesh.n_elements * ref.n_local
+    x = torch.from_numpy(2.0 * problems.uniform01(problems.SEED_SPMV_X, n) - 1.0).cuda()
+    y = torch.empty_like(x)
+    for _ in range(3):
+        plan.spmv(out, x, y)
+    torch.cuda.synchronize()
+    rp, col, val, _ = to_np(out)
+    xs = x.cpu().numpy()
+    y_ref = oracle.spmv(rp, col, val, xs)
+    absx = np.abs(xs)
+    scale = oracle.spmv(rp, col, np.abs(val), absx)
+    assert np.all(np.abs(y.cpu().numpy() - y_ref) <= 1e-12 * scale + 1e-300)
+
+
+def test_inflow_on_neumann_reports_lowest_edge(oracle):
+    """test_assembly.cpp:371-381, test_parallel_consistency.cpp:152-182."""
+    mesh = dgfem.unit_square_mesh(6, 0.0, 0, False, 0, 15)   # all Neumann
+    ref = dgfem.ReferenceElement(1)
+    spec = problems.registry_get("smooth-sine")
+    params = dgfem.set_parameters(capi.SIPG, 1)
+    with pytest.raises(dgfem.Error) as e:
+        dgfem.assemble_all(mesh, ref, spec, params)
+    assert e.value.code == "InflowOnNeumann"
+    from oracle.oracle import ReferenceError_
+    with pytest.raises(ReferenceError_) as r:
+        oracle.assemble(mesh.arrays(), ref.tables(), spec.c, params)
+    assert e.value.detail == r.value.detail
+    # the DROP policy assembles and matches the oracle's DROP
+    params.neumann_inflow = capi.INFLOW_DROP
+    g = dgfem.assemble_all(mesh, ref, spec, params)
+    compare_system(to_np(g), oracle.assemble(mesh.arrays(), ref.tables(), spec.c, params))
+
+
+@pytest.mark.parametrize("index", [2, 3])
+def test_bitwise_reproducible(index):
+    """No floating-point atomics: two runs give identical bits (test_parallel_consistency.cpp)."""
+    import torch
+    cfg = problems.CONFIGS[index]
+    mesh = dgfem.unit_square_mesh(64, cfg.jitter, problems.SEED_JITTER, cfg.permute,
+                                  problems.SEED_PERMUTE, cfg.neumann_sides)
+    ref = dgfem.ReferenceElement(cfg.degree, cfg.quad_order)
+    spec = problems.config_problem(index, mesh.n_elements)
+    params = dgfem.config_parameters(cfg, cfg.methods[0])
+    a = dgfem.assemble_all(mesh, ref, spec, params)
+    b = dgfem.assemble_all(mesh, ref, spec, params)
+    torch.cuda.synchronize()
+    for x, y in zip((a.row_ptr, a.col, a.val, a.rhs), (b.row_ptr, b.col, b.val, b.rhs)):
+        assert torch.equal(x, y)
+
+
+def test_host_buffer_entry_matches_device_path(oracle):
+    """dgb_assemble_all_host (the C-ABI call a reference maintainer binds) == device path."""
+    import torch
+    cfg = problems.CONFIGS[5]
+    mesh = dgfem.unit_square_mesh(16, 0.0, 0, False, 0, 0)
+    ref = dgfem.ReferenceElement(cfg.degree, cfg.quad_order)
+    spec = problems.config_problem(5, mesh.n_elements)
+    params = dgfem.config_parameters(cfg, capi.IIPG)
+    h = dgfem.assemble_all_host(mesh, ref.view, spec, params)
+    d = to_np(dgfem.assemble_all(mesh, ref, spec, params))
+    torch.cuda.synchronize()
+    for x, y in zip(h, d):
+        np.testing.assert_array_equal(x, y)
+    compare_system(h, oracle.assemble(mesh.arrays(), ref.tables(), spec.c, params))
+
+
+def test_reference_tables_plan(oracle):
+    """A plan built from the REFERENCE's own tables (golden dump), as in a drop-in deployment."""
+    import os
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden", "tables.npz"))
+    t = {k[len("k3_q7_"):]: z[k] for k in z.files if k.startswith("k3_q7_")}
+    for k in ("degree", "n_local", "nq_vol", "nq_edge"):
+        t[k] = int(t[k])
+    cfg = problems.CONFIGS[3]
+    mesh = dgfem.unit_square_mesh(10, cfg.jitter, problems.SEED_JITTER, False, 0, cfg.neumann_sides)
+    spec = problems.config_problem(3)
+    params = dgfem.config_parameters(cfg, capi.SIPG)
+    view = dgfem.tables_struct(t)
+    plan = dgfem.Plan(view)
+    dm, dp = dgfem.DeviceMesh(mesh), dgfem.DeviceProblem(spec)
+    out = plan.assemble(dm, dp, params, plan.allocate(dm))
+    compare_system(to_np(out), oracle.assemble(mesh.arrays(), t, spec.c, params))
+
+
+def test_shards_equal_full_assembly():
+    """dgb_assemble_rows over a 3-way row split concatenates to dgb_assemble's output."""
+    import torch
+    cfg = problems.CONFIGS[2]
+    mesh = dgfem.config_mesh(cfg, strips=3)
+    ref = dgfem.ReferenceElement(cfg.degree, cfg.quad_order)
+    spec = problems.config_problem(2, mesh.n_elements)
+    params = dgfem.config_parameters(cfg, capi.NIPG)
+    full = to_np(dgfem.assemble_all(mesh, ref, spec, params))
+    parts, first = [], None
+    for r in range(3):
+        b, e = shard.row_range(mesh.n_elements, r, 3)
+        sa = shard.ShardAssembler(mesh, ref, spec, 0, b, e, share=first)
+        first = first or sa
+        parts.append(to_np(sa.assemble(params)))
+    torch.cuda.synchronize()
+    off = np.cumsum([0] + [p[0][-1] for p in parts])
+    rp = np.concatenate([p[0][:-1] + o for p, o in zip(parts, off)] + [[off[-1]]])
+    np.testing.assert_array_equal(rp, full[0])
+    for i in (1, 2, 3):
+        np.testing.assert_array_equal(np.concatenate([p[i] for p in parts]), full[i])
+
+
+def test_full_size_sipg_pure_diffusion_symmetric():
+    """Config-3 mesh at full size (2.1 M triangles, P3) with b = 0, alpha = 0: K = D is
+    symmetric to 1e-12 relative (acceptance.cpp criterion 5)."""
+    import torch
+    cfg = problems.CONFIGS[3]
+    mesh = dgfem.config_mesh(cfg)
+    ref = dgfem.ReferenceElement(cfg.degree, cfg.quad_order)
+    spec = problems.config_problem(3)
+    spec.c.advection = problems.vec_constant(0.0, 0.0)
+    spec.c.linear_reaction = problems.constant(0.0)
+    params = dgfem.config_parameters(cfg, capi.SIPG)
+    s = dgfem.assemble_all(mesh, ref, spec, params)
+    nl = ref.n_local
+    E = mesh.n_elements
+    rp = s.row_ptr.long()
+    row_of_block = torch.repeat_interleave(torch.arange(E, device="cuda"), rp[1:] - rp[:-1])
+    # transpose partner of block (e, f) is block (f, e): find it by a sort of (col, row) keys
+    key = row_of_block * E + s.col.long()
+    tkey = s.col.long() * E + row_of_block
+    order = torch.argsort(key)
+    pos = torch.searchsorted(key[order], tkey)
+    partner = order[pos]
+    assert torch.equal(key[partner], tkey)
+    diff = (s.val - s.val[partner].transpose(1, 2)).abs().max().item()
+    assert diff <= 1e-12 * s.val.abs().max().item()
+
+
+def test_full_size_constant_annihilation_config2():
+    """Config 2 at full size: for elements away from the boundary, K applied to the projection
+    of u = 1 equals the reaction term alone (diffusion, penalty, consistency and upwind all
+    annihilate constants; test_assembly.cpp:342-369)."""
+    import torch
+    cfg = problems.CONFIGS[2]
+    mesh = dgfem.config_mesh(cfg)
+    ref = dgfem.ReferenceElement(cfg.degree, cfg.quad_order)
+    spec = problems.config_problem(2)
+    params = dgfem.config_parameters(cfg, capi.SIPG)
+    plan = dgfem.Plan(ref.view)
+    dm, dp = dgfem.DeviceMesh(mesh), dgfem.DeviceProblem(spec)
+    out = plan.assemble(dm, dp, params, plan.allocate(dm))
+    nl = ref.n_local
+    t = ref.tables()
+    c0 = 1.0 / t["phi"].reshape(-1, nl)[0, 0]          # phi_0 is constant: u = 1 -> coef c0
+    x = torch.zeros(mesh.n_elements * nl, dtype=torch.float64, device="cuda")
+    x[0::nl] = c0
+    y = torch.empty_like(x)
+    plan.spmv(out, x, y)
+    # reaction only: R x = det * alpha * M x, M = I: y_e = det_e * c0 on the first dof
+    interior = torch.from_numpy(np.all(mesh.edge_kind[mesh.element_edges] == 0, axis=1)).cuda()
+    nodes, el = mesh.nodes, mesh.elements
+    p0, p1, p2 = nodes[el[:, 0]], nodes[el[:, 1]], nodes[el[:, 2]]
+    det = (p1[:, 0] - p0[:, 0]) * (p2[:, 1] - p0[:, 1]) - (p2[:, 0] - p0[:, 0]) * (p1[:, 1] - p0[:, 1])
+    expect = torch.zeros_like(y).view(-1, nl)
+    expect[:, 0] = torch.from_numpy(det).cuda() * c0
+    err = (y.view(-1, nl) - expect)[interior].abs().max().item()
+    assert err <= 1e-12 * (c0 * 18.0 * 1e-4 * 4)  # << penalty / diffusion scale of the entries
+
+
+def test_config1_solve_error(oracle):
+    """Config 1's own check: solve K u = F on the CPU (scipy; the reference's Eigen solver is
+    absent) and compare the L2 error with the exact solution against the oracle system's."""
+    import scipy.sparse as sp
+    import scipy.sparse.linalg as spla
+    cfg = problems.CONFIGS[1]
+    mesh = dgfem.config_mesh(cfg)
+    ref = dgfem.ReferenceElement(cfg.degree, cfg.quad_order)
+    spec = problems.config_problem(1)
+    params = dgfem.config_parameters(cfg, capi.SIPG)
+    t = ref.tables()
+
+    def l2_error(rp, col, val, rhs):
+        crp, ccol, cval = bsr_to_csr(rp, col, val)
+        n = crp.shape[0] - 1
+        u = spla.spsolve(sp.csr_matrix((cval, ccol, crp), shape=(n, n)).tocsc(), rhs.reshape(-1))
+        nl = t["n_local"]
+        phi = t["phi"].reshape(-1, nl)
+        nodes, el = mesh.nodes, mesh.elements
+        p0, p1, p2 = nodes[el[:, 0]], nodes[el[:, 1]], nodes[el[:, 2]]
+        B = np.stack([p1 - p0, p2 - p0], axis=2)                 # [E, 2, 2]
+        det = np.abs(np.linalg.det(B))
+        xq = p0[:, None, :] + np.einsum("eij,qj->eqi", B, np.stack([t["vol_x"], t["vol_y"]], 1))
+        uh = u.reshape(-1, nl) @ phi.T                            # [E, q]
+        ue = np.sin(np.pi * xq[..., 0]) * np.sin(np.pi * xq[..., 1])
+        return np.sqrt(np.sum(det[:, None] * t["vol_w"][None, :] * (uh - ue) ** 2))
+
+    e_gpu = l2_error(*to_np(dgfem.assemble_all(mesh, ref, spec, params)))
+    e_orc = l2_error(*oracle.assemble(mesh.arrays(), t, spec.c, params))
+    assert e_gpu < 5e-3
+    assert abs(e_gpu - e_orc) <= 1e-9 * e_orc
