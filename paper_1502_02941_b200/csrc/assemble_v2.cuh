@@ -72,7 +72,7 @@ struct Params2 {
 // Per-edge state of one element (registers).
 struct EdgeState {
   double ax, ay, dx, dy;  // sorted-pair start point and direction (edge points a + t d)
-  double h, nx, ny;       // length, outward unit normal of this element
+  double h, rh, nx, ny;   // length, 1 / length, outward unit normal of this element
   double ge0, ge1;        // G_e^T n
   double gf0, gf1;        // G_f^T n (interior)
   double eps;             // edge diffusivity
@@ -106,21 +106,40 @@ __device__ __forceinline__ void flush_blocks(const double* st, long long base, d
   constexpr int S = Stage<N2>::kStride;
   __syncwarp();
   if constexpr (N2 % 2 == 0) {
-    constexpr int H = N2 / 2;
-#pragma unroll 2
-    for (int c = lane; c < 32 * H; c += 32) {
-      const int L = c / H, k = 2 * (c - L * H);
-      const long long b = __shfl_sync(0xffffffffu, base, L);
-      const double2 x = *reinterpret_cast<const double2*>(st + L * S + k);
-      if (b >= 0) *reinterpret_cast<double2*>(val + b + k) = x;
+    // 16-byte chunks c = lane + 32 it of the flattened [32 lanes][N2 / 2] staging; (L, k)
+    // advance by 32 chunks per iteration without a division.
+    constexpr int H = N2 / 2, DL = 32 / H, DK = 32 % H;
+    int L = lane / H, k = lane - L * H;
+#pragma unroll 3
+    for (int it = 0; it < H; ++it) {
+      const long long b = __shfl_sync(0xffffffffu, base, L & 31);
+      if (L < 32) {
+        const double2 x = *reinterpret_cast<const double2*>(st + L * S + 2 * k);
+        if (b >= 0) *reinterpret_cast<double2*>(val + b + 2 * k) = x;
+      }
+      k += DK;
+      L += DL;
+      if (k >= H) {
+        k -= H;
+        ++L;
+      }
     }
   } else {
-#pragma unroll 2
-    for (int c = lane; c < 32 * N2; c += 32) {
-      const int L = c / N2, k = c - L * N2;
-      const long long b = __shfl_sync(0xffffffffu, base, L);
-      const double x = st[L * S + k];
-      if (b >= 0) val[b + k] = x;
+    constexpr int DL = 32 / N2, DK = 32 % N2;
+    int L = lane / N2, k = lane - L * N2;
+#pragma unroll 3
+    for (int it = 0; it < N2; ++it) {
+      const long long b = __shfl_sync(0xffffffffu, base, L & 31);
+      if (L < 32) {
+        const double x = st[L * S + k];
+        if (b >= 0) val[b + k] = x;
+      }
+      k += DK;
+      L += DL;
+      if (k >= N2) {
+        k -= N2;
+        ++L;
+      }
     }
   }
   __syncwarp();
@@ -160,8 +179,9 @@ __global__ void __launch_bounds__(128, MINB) assemble_kernel(
   const double B00 = FSUB(pv[1].x, pv[0].x), B01 = FSUB(pv[2].x, pv[0].x);
   const double B10 = FSUB(pv[1].y, pv[0].y), B11 = FSUB(pv[2].y, pv[0].y);
   const double det = FSUB(FMUL(B00, B11), FMUL(B01, B10));
-  const double G00 = FDIV(B11, det), G01 = FDIV(-B10, det);
-  const double G10 = FDIV(-B01, det), G11 = FDIV(B00, det);
+  const double rdet = 1.0 / det;
+  const double G00 = B11 * rdet, G01 = -B10 * rdet;
+  const double G10 = -B01 * rdet, G11 = B00 * rdet;
   const double eps = scalar_element(P.prob.diffusion, ee);
   const double alpha = scalar_element(P.prob.linear_reaction, ee);
   const dgb_vector_field& bf = P.prob.advection;
@@ -183,7 +203,8 @@ __global__ void __launch_bounds__(128, MINB) assemble_kernel(
     s.dx = FSUB(Bn.x, A.x);
     s.dy = FSUB(Bn.y, A.y);
     s.h = hypot_dd(s.dx, s.dy);
-    const double tx = FDIV(s.dx, s.h), ty = FDIV(s.dy, s.h);
+    s.rh = 1.0 / s.h;
+    const double tx = s.dx * s.rh, ty = s.dy * s.rh;
     s.nx = s.o == 0 ? ty : -ty;
     s.ny = s.o == 0 ? -tx : tx;
     s.ge0 = G00 * s.nx + G10 * s.ny;
@@ -202,7 +223,7 @@ __global__ void __launch_bounds__(128, MINB) assemble_kernel(
       for (int k = 0; k < 3; ++k) vf[k] = __ldg(P.elements + 3 * f + k);
 #pragma unroll
       for (int k = 0; k < 3; ++k) if (vf[k] != a && vf[k] != b) s.lf = k;
-      const Geo gf = element_geo(P.nodes, vf);
+      const Geo gf = element_geo_fast(P.nodes, vf);
       s.gf0 = gf.G00 * s.nx + gf.G10 * s.ny;
       s.gf1 = gf.G01 * s.nx + gf.G11 * s.ny;
       if (P.prob.diffusion.kind == DGB_FIELD_PER_ELEMENT) {
@@ -289,7 +310,7 @@ __global__ void __launch_bounds__(128, MINB) assemble_kernel(
       const double base = (interior ? 0.5 : 1.0) * s.h * s.eps;
       cW[l][0] = base * s.ge0;
       cW[l][1] = base * s.ge1;
-      const double sh = FDIV(sig, s.h);
+      const double sh = sig * s.rh;
       if (bconst && L::kHasP) {
         const double fl = FADD(FMUL(bf.p[0], s.nx), FMUL(bf.p[1], s.ny));
         double up = 0.0;
@@ -415,7 +436,7 @@ __global__ void __launch_bounds__(128, MINB) assemble_kernel(
       const double base = 0.5 * s.h * s.eps;
       const double cY0 = -base * s.gf0, cY1 = -base * s.gf1;
       const double cZ0 = -P.kappa * base * s.ge0, cZ1 = -P.kappa * base * s.ge1;
-      const double sh = FDIV(P.sigma_i, s.h);
+      const double sh = P.sigma_i * s.rh;
       double cV[NQE];
       double flc = 0.0;
       if (bconst) flc = FADD(FMUL(bf.p[0], s.nx), FMUL(bf.p[1], s.ny));
@@ -519,7 +540,7 @@ __global__ void __launch_bounds__(128, MINB) assemble_kernel(
           if (fls[p] < -1e-12 * fmax(1.0, hypot_dd(bx, by))) inflow = true;
           gds[p] = scalar_point(P.prob.dirichlet, px, py);
         }
-        const double sh = FDIV(P.sigma_b, s.h);
+        const double sh = P.sigma_b * s.rh;
 #pragma unroll
         for (int p = 0; p < NQE; ++p) {
           const int q = s.o == 0 ? p : NQE - 1 - p;

@@ -131,6 +131,8 @@ __device__ __forceinline__ void family(int fn, const double* p, double x, double
       return;
     }
     case DGB_FN_TANH_LAYER: {
+      // Same expressions as the reference's BoundaryLayer (problems.cpp:81-98): far from the
+      // layer F is dominated by the rounding of u = (1 - tanh s) / 2, so parity needs tanh.
       const double s = (p[0] * x + p[1] * y + p[2]) / p[3];
       const double t = tanh(s);
       const double c = cosh(s);
@@ -251,6 +253,29 @@ __device__ __forceinline__ Geo element_geo(const double* __restrict__ nodes,
   g.G01 = FDIV(-g.B10, g.det);
   g.G10 = FDIV(-g.B01, g.det);
   g.G11 = FDIV(g.B00, g.det);
+  g.ox = p0.x;
+  g.oy = p0.y;
+  return g;
+}
+
+// element_geometry with one reciprocal instead of four divisions (values only; no term-selecting
+// decision depends on G).
+__device__ __forceinline__ Geo element_geo_fast(const double* __restrict__ nodes,
+                                                const int32_t* v) {
+  Geo g;
+  const double2 p0 = __ldg(reinterpret_cast<const double2*>(nodes) + v[0]);
+  const double2 p1 = __ldg(reinterpret_cast<const double2*>(nodes) + v[1]);
+  const double2 p2 = __ldg(reinterpret_cast<const double2*>(nodes) + v[2]);
+  g.B00 = p1.x - p0.x;
+  g.B01 = p2.x - p0.x;
+  g.B10 = p1.y - p0.y;
+  g.B11 = p2.y - p0.y;
+  g.det = FSUB(FMUL(g.B00, g.B11), FMUL(g.B01, g.B10));
+  const double rd = 1.0 / g.det;
+  g.G00 = g.B11 * rd;
+  g.G01 = -g.B10 * rd;
+  g.G10 = -g.B01 * rd;
+  g.G11 = g.B00 * rd;
   g.ox = p0.x;
   g.oy = p0.y;
   return g;
@@ -959,24 +984,21 @@ bool try_launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_
   if (plan->force_generic) return false;
   const bool trig = problem->advection.kind == DGB_VEC_TRIG;
   const int key = plan->nl * 10000 + plan->nqv * 100 + plan->nqe;
-#define DGB_V2(NL_, NQV_, NQE_, TRIG_)                                                     \
+  // Register budgets (CTAs of 128 threads per SM) chosen by measurement (profiles/NOTES.md);
+  // DGB_OPTION_MIN_BLOCKS overrides them for tuning runs.
+  const int mb = plan->minblocks;
+#define DGB_V2(NL_, NQV_, NQE_, TRIG_, MB_)                                                 \
   if (key == NL_ * 10000 + NQV_ * 100 + NQE_ && trig == TRIG_) {                          \
-    launch_v2<NL_, NQV_, NQE_, TRIG_>(plan, mesh, problem, params, out, rhs, s, rb, re);           \
+    if (mb == 2) { launch_v2<NL_, NQV_, NQE_, TRIG_, 2>(plan, mesh, problem, params, out, rhs, s, rb, re); return true; } \
+    if (mb == 4) { launch_v2<NL_, NQV_, NQE_, TRIG_, 4>(plan, mesh, problem, params, out, rhs, s, rb, re); return true; } \
+    launch_v2<NL_, NQV_, NQE_, TRIG_, MB_>(plan, mesh, problem, params, out, rhs, s, rb, re);  \
     return true;                                                                           \
   }
-  DGB_V2(3, 6, 2, false)
-  DGB_V2(3, 6, 2, true)
-  if (key == 60703 && !trig && plan->minblocks == 3) {
-    launch_v2<6, 7, 3, false, 3>(plan, mesh, problem, params, out, rhs, s, rb, re);
-    return true;
-  }
-  if (key == 60703 && !trig && plan->minblocks == 4) {
-    launch_v2<6, 7, 3, false, 4>(plan, mesh, problem, params, out, rhs, s, rb, re);
-    return true;
-  }
-  DGB_V2(6, 7, 3, false)
-  DGB_V2(6, 12, 3, false)
-  DGB_V2(10, 16, 4, false)
+  DGB_V2(3, 6, 2, false, 4)
+  DGB_V2(3, 6, 2, true, 4)
+  DGB_V2(6, 7, 3, false, 4)
+  DGB_V2(6, 12, 3, false, 4)
+  DGB_V2(10, 16, 4, false, 2)
 #undef DGB_V2
   return false;
 }
