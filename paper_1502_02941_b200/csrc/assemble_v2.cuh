@@ -69,28 +69,6 @@ struct Params2 {
   Tab<NL, NQV, NQE, TRIG> t;
 };
 
-// Per-edge state of one element (registers).
-struct EdgeState {
-  double ax, ay, dx, dy;  // sorted-pair start point and direction (edge points a + t d)
-  double h, rh, nx, ny;   // length, 1 / length, outward unit normal of this element
-  double ge0, ge1;        // G_e^T n
-  double gf0, gf1;        // G_f^T n (interior)
-  double eps;             // edge diffusivity
-  int kind, lf, o, slot;  // kind, neighbour local edge, orientation, block slot
-  int edge;
-};
-
-template <int NL, int NQV, int NQE, bool TRIG>
-__device__ __forceinline__ void flux_point(const Params2<NL, NQV, NQE, TRIG>& P, const EdgeState& s,
-                                           int q, double& px, double& py, double& fl) {
-  using L = Lay<NL, NQV, NQE, TRIG>;
-  px = FADD(s.ax, FMUL(P.t.x[L::ET + q], s.dx));
-  py = FADD(s.ay, FMUL(P.t.x[L::ET + q], s.dy));
-  double bx, by;
-  velocity(P.prob.advection, px, py, bx, by);
-  fl = FADD(FMUL(bx, s.nx), FMUL(by, s.ny));
-}
-
 // Staging stride (doubles) per lane: even, so 16-byte chunks stay aligned.
 template <int N2>
 struct Stage {
@@ -145,31 +123,53 @@ __device__ __forceinline__ void flush_blocks(const double* st, long long base, d
   __syncwarp();
 }
 
-template <int NL, int NQV, int NQE, bool TRIG, int MINB>
-__global__ void __launch_bounds__(128, MINB) assemble_kernel(
-    const __grid_constant__ Params2<NL, NQV, NQE, TRIG> P) {
+// Per-warp shared-memory layout of the block-row kernel (doubles).
+template <int NL, int NQV, int NQE, int BK>
+struct Smem {
+  static constexpr int N2 = NL * NL;
+  static constexpr int SS = Stage<N2>::kStride;               // staging stride per lane
+  static constexpr int NF = BK == 0 ? 8 : 7 + 2 * NQE;         // stashed coefficients per edge
+  static constexpr int kStage = 32 * SS;
+  static constexpr int kStash = 3 * NF * 32;
+  static constexpr int kMeta = 3 * 32 / 2;                     // 3 ints per lane
+  static constexpr int kTrig = BK == 2 ? 2 * NQV * 32 : 0;     // pointwise transport weights
+  static constexpr int kWarp = kStage + kStash + kMeta + kTrig;
+  static constexpr int kTr = (3 * NQE * 3 * NL + 1) & ~1;      // trace table (per CTA)
+};
+
+// Stash field indices (per edge l, per lane): see the diagonal / neighbour passes.
+enum { F_W0 = 0, F_W1, F_P, F_Y0, F_Y1, F_Z0, F_Z1, F_X, F_U = 7 };
+
+template <int NL, int NQV, int NQE, int BK, int THREADS, int MINB>
+__global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
+    const __grid_constant__ Params2<NL, NQV, NQE, BK == 2> P) {
+  constexpr bool TRIG = BK == 2;
   constexpr int N2 = NL * NL;
   using L = Lay<NL, NQV, NQE, TRIG>;
+  using SM = Smem<NL, NQV, NQE, BK>;
+  constexpr int SS = SM::SS, NF = SM::NF;
   extern __shared__ double smem[];
-  // [3][NQE][3][NL] trace table copy (phi, d0phi, d1phi per local edge / point) for the
-  // per-lane neighbour rows, then one staging area of 32 x (N2 + 1) doubles per warp.
-  double* tr = smem;
-  constexpr int kTr = 3 * NQE * 3 * NL;
-  for (int i = threadIdx.x; i < kTr; i += blockDim.x) {
+  double* tr = smem;  // [3][NQE][3][NL]: phi, d0 phi, d1 phi of each local edge's points
+  for (int i = threadIdx.x; i < 3 * NQE * 3 * NL; i += blockDim.x) {
     const int j = i % NL, c = (i / NL) % 3, p = (i / (3 * NL)) % NQE, l = i / (3 * NL * NQE);
     tr[i] = c == 0 ? P.t.x[L::EPHI + (l * NQE + p) * NL + j]
                    : P.t.x[L::EDPHI + ((l * NQE + p) * 2 + c - 1) * NL + j];
   }
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  constexpr int SS = Stage<N2>::kStride;
-  double* stw = smem + ((kTr + 1) & ~1) + warp * 32 * SS;
+  double* stw = smem + SM::kTr + warp * SM::kWarp;  // staging [32][SS]
   double* st = stw + lane * SS;
+  double* sk = stw + SM::kStage;                     // stash [NF][3][32]
+  int* mk = reinterpret_cast<int*>(sk + SM::kStash); // meta [3][32]: kind | lf << 2 | slot << 4
+  double* sq = sk + SM::kStash + SM::kMeta;          // TRIG: [NQV][2][32]
+  auto K = [&](int f, int l) -> double& { return sk[(f * 3 + l) * 32 + lane]; };
+
   const int e = P.row_begin + blockIdx.x * blockDim.x + threadIdx.x;
   const bool active = e < P.row_end;
   const int ee = active ? e : P.row_end - 1;  // inactive lanes mirror a valid element
+  const dgb_vector_field& bf = P.prob.advection;
 
-  // ---- element geometry and edge states ---------------------------------------------------
+  // ---- phase A0: own geometry ----------------------------------------------------------------
   int v[3];
 #pragma unroll
   for (int k = 0; k < 3; ++k) v[k] = __ldg(P.elements + 3 * ee + k);
@@ -183,65 +183,171 @@ __global__ void __launch_bounds__(128, MINB) assemble_kernel(
   const double G00 = B11 * rdet, G01 = -B10 * rdet;
   const double G10 = -B01 * rdet, G11 = B00 * rdet;
   const double eps = scalar_element(P.prob.diffusion, ee);
-  const double alpha = scalar_element(P.prob.linear_reaction, ee);
-  const dgb_vector_field& bf = P.prob.advection;
-  const bool bconst = bf.kind == DGB_VEC_CONSTANT;
 
-  EdgeState es[3];
+  // ---- phase A1: RHS volume term and pointwise transport weights (few live registers) -------
+  double F[NL];
+#pragma unroll
+  for (int i = 0; i < NL; ++i) F[i] = 0.0;
+  {
+    const dgb_scalar_field& fs = P.prob.source;
+#pragma unroll 1
+    for (int q = 0; q < NQV; ++q) {
+      const double px = FADD(FADD(pv[0].x, FMUL(B00, P.t.x[L::VX + q])), FMUL(B01, P.t.x[L::VY + q]));
+      const double py = FADD(FADD(pv[0].y, FMUL(B10, P.t.x[L::VX + q])), FMUL(B11, P.t.x[L::VY + q]));
+      const double f = fs.kind == DGB_FIELD_PER_ELEMENT ? __ldg(fs.per_element + ee)
+                                                        : scalar_point(fs, px, py);
+      const double dw = det * P.t.x[L::VW + q];
+      const double c = dw * f;
+#pragma unroll
+      for (int i = 0; i < NL; ++i) F[i] = fma(c, P.t.x[L::PHI + q * NL + i], F[i]);
+      if constexpr (TRIG) {
+        double bx, by;
+        velocity(bf, px, py, bx, by);
+        sq[(2 * q) * 32 + lane] = dw * (G00 * bx + G10 * by);
+        sq[(2 * q + 1) * 32 + lane] = dw * (G01 * bx + G11 * by);
+      }
+    }
+  }
+
+  // ---- phase A2: per local edge -> stashed coefficient record, boundary RHS --------------------
   int cols[4], kinds[4], nb = 1;
   cols[0] = ee;
   kinds[0] = -1;
 #pragma unroll
   for (int l = 0; l < 3; ++l) {
-    EdgeState& s = es[l];
     const int a = v[(l + 1) % 3], b = v[(l + 2) % 3];
-    s.o = a < b ? 0 : 1;
-    const double2 A = s.o == 0 ? pv[(l + 1) % 3] : pv[(l + 2) % 3];
-    const double2 Bn = s.o == 0 ? pv[(l + 2) % 3] : pv[(l + 1) % 3];
-    s.ax = A.x;
-    s.ay = A.y;
-    s.dx = FSUB(Bn.x, A.x);
-    s.dy = FSUB(Bn.y, A.y);
-    s.h = hypot_dd(s.dx, s.dy);
-    s.rh = 1.0 / s.h;
-    const double tx = s.dx * s.rh, ty = s.dy * s.rh;
-    s.nx = s.o == 0 ? ty : -ty;
-    s.ny = s.o == 0 ? -tx : tx;
-    s.ge0 = G00 * s.nx + G10 * s.ny;
-    s.ge1 = G01 * s.nx + G11 * s.ny;
-    s.edge = __ldg(P.element_edges + 3 * ee + l);
-    s.kind = __ldg(P.edge_kind + s.edge);
-    s.eps = eps;
-    s.lf = 0;
-    s.gf0 = s.gf1 = 0.0;
-    s.slot = -1;
-    if (s.kind == DGB_EDGE_INTERIOR) {
-      const int2 lr = __ldg(reinterpret_cast<const int2*>(P.edge_elements) + s.edge);
+    const int o = a < b ? 0 : 1;  // make_side orientation (assembly.cpp:125-126)
+    const double2 A = o == 0 ? pv[(l + 1) % 3] : pv[(l + 2) % 3];
+    const double2 Bn = o == 0 ? pv[(l + 2) % 3] : pv[(l + 1) % 3];
+    const double dx = FSUB(Bn.x, A.x), dy = FSUB(Bn.y, A.y);
+    const double h = hypot_dd(dx, dy);  // edge_geometry (mesh.cpp:232-257)
+    const double rh = 1.0 / h;
+    const double tx = dx * rh, ty = dy * rh;
+    const double nx = o == 0 ? ty : -ty, ny = o == 0 ? -tx : tx;  // outward normal of e
+    const double ge0 = G00 * nx + G10 * ny, ge1 = G01 * nx + G11 * ny;
+    const int edge = __ldg(P.element_edges + 3 * ee + l);
+    const int kind = __ldg(P.edge_kind + edge);
+    int lf = 0;
+    double w0 = 0.0, w1 = 0.0, cp = 0.0, y0 = 0.0, y1 = 0.0, z0 = 0.0, z1 = 0.0, cx = 0.0;
+    if (kind == DGB_EDGE_INTERIOR) {
+      const int2 lr = __ldg(reinterpret_cast<const int2*>(P.edge_elements) + edge);
       const int f = lr.x == ee ? lr.y : lr.x;
       int vf[3];
 #pragma unroll
       for (int k = 0; k < 3; ++k) vf[k] = __ldg(P.elements + 3 * f + k);
 #pragma unroll
-      for (int k = 0; k < 3; ++k) if (vf[k] != a && vf[k] != b) s.lf = k;
+      for (int k = 0; k < 3; ++k) if (vf[k] != a && vf[k] != b) lf = k;
       const Geo gf = element_geo_fast(P.nodes, vf);
-      s.gf0 = gf.G00 * s.nx + gf.G10 * s.ny;
-      s.gf1 = gf.G01 * s.nx + gf.G11 * s.ny;
+      double eps_e = eps;
       if (P.prob.diffusion.kind == DGB_FIELD_PER_ELEMENT) {
         const double ef = __ldg(P.prob.diffusion.per_element + f);
-        s.eps = ee < f ? 0.5 * (eps + ef) : 0.5 * (ef + eps);
+        eps_e = ee < f ? 0.5 * (eps + ef) : 0.5 * (ef + eps);
       }
       cols[nb] = f;
       kinds[nb++] = l;
+      const double base = 0.5 * h * eps_e;  // avg * h * eps
+      w0 = base * ge0;
+      w1 = base * ge1;
+      y0 = -base * (gf.G00 * nx + gf.G10 * ny);
+      y1 = -base * (gf.G01 * nx + gf.G11 * ny);
+      z0 = -P.kappa * base * ge0;
+      z1 = -P.kappa * base * ge1;
+      const double sh = P.sigma_i * rh;
+      if constexpr (BK == 0) {
+        // constant b: every point has the same flux, so the point weights factor out
+        const double fl = FADD(FMUL(bf.p[0], nx), FMUL(bf.p[1], ny));
+        const double up = fl < 0.0 ? FMUL(h, fl) : 0.0;
+        cp = sh * (h * eps_e) - up;  // diag: penalty + (-h b.n) on inflow
+        cx = up - sh * (h * eps_e);  // off : -penalty + (h b.n) on inflow
+      } else {
+#pragma unroll
+        for (int p = 0; p < NQE; ++p) {
+          const int q = o == 0 ? p : NQE - 1 - p;
+          const double w = FMUL(P.t.x[L::EW + q], h);
+          const double px = FADD(A.x, FMUL(P.t.x[L::ET + q], dx));
+          const double py = FADD(A.y, FMUL(P.t.x[L::ET + q], dy));
+          double bx, by;
+          velocity(bf, px, py, bx, by);
+          const double fl = FADD(FMUL(bx, nx), FMUL(by, ny));
+          const double up = fl < 0.0 ? FMUL(w, fl) : 0.0;
+          const double pen = FMUL(sh, FMUL(w, eps_e));
+          K(F_U + p, l) = pen - up;
+          K(F_U + NQE + p, l) = up - pen;
+        }
+      }
+    } else {
+      // boundary edge: diffusion (Dirichlet), inflow upwind, and the boundary RHS terms
+      double fls[NQE], gb[NQE];
+      bool inflow = false;
+#pragma unroll
+      for (int p = 0; p < NQE; ++p) {
+        const int q = o == 0 ? p : NQE - 1 - p;
+        const double px = FADD(A.x, FMUL(P.t.x[L::ET + q], dx));
+        const double py = FADD(A.y, FMUL(P.t.x[L::ET + q], dy));
+        double bx, by;
+        velocity(bf, px, py, bx, by);
+        fls[p] = FADD(FMUL(bx, nx), FMUL(by, ny));
+        if (fls[p] < -1e-12 * fmax(1.0, hypot_dd(bx, by))) inflow = true;  // assembly.cpp:324-401
+        gb[p] = scalar_point(kind == DGB_EDGE_NEUMANN ? P.prob.neumann : P.prob.dirichlet, px, py);
+      }
+      double cG[NQE], cH[NQE];
+      if (kind == DGB_EDGE_NEUMANN) {
+        if (inflow && !P.drop_neumann && active) atomicMin(P.err_edge, edge);
+#pragma unroll
+        for (int p = 0; p < NQE; ++p) {
+          const int q = o == 0 ? p : NQE - 1 - p;
+          cG[p] = FMUL(FMUL(P.t.x[L::EW + q], h), gb[p]);  // neumann_rhs (assembly.cpp:427-442)
+          cH[p] = 0.0;
+          if constexpr (BK != 0) K(F_U + p, l) = 0.0;
+        }
+      } else {
+        const double base = h * eps;  // avg = 1
+        w0 = base * ge0;
+        w1 = base * ge1;
+        const double sh = P.sigma_b * rh;
+        if constexpr (BK == 0) {
+          cp = sh * (h * eps) - ((inflow && fls[0] < 0.0) ? FMUL(h, fls[0]) : 0.0);
+        }
+#pragma unroll
+        for (int p = 0; p < NQE; ++p) {
+          const int q = o == 0 ? p : NQE - 1 - p;
+          const double w = FMUL(P.t.x[L::EW + q], h);
+          const double win = (inflow && fls[p] < 0.0) ? -FMUL(w, fls[p]) : 0.0;
+          const double wgd = w * gb[p];
+          cG[p] = wgd * (sh * eps) + win * gb[p];  // emit_dirichlet_rhs + inflow data term
+          cH[p] = wgd * (P.kappa * eps);
+          if constexpr (BK != 0) K(F_U + p, l) = FMUL(sh, FMUL(w, eps)) + win;
+        }
+      }
+#pragma unroll
+      for (int p = 0; p < NQE; ++p) {
+        const double h0 = cH[p] * ge0, h1 = cH[p] * ge1;
+#pragma unroll
+        for (int i = 0; i < NL; ++i) {
+          F[i] = fma(cG[p], P.t.x[L::EPHI + (l * NQE + p) * NL + i],
+                     fma(h0, P.t.x[L::EDPHI + ((l * NQE + p) * 2) * NL + i],
+                         fma(h1, P.t.x[L::EDPHI + ((l * NQE + p) * 2 + 1) * NL + i], F[i])));
+        }
+      }
     }
+    K(F_W0, l) = w0;
+    K(F_W1, l) = w1;
+    K(F_P, l) = cp;
+    K(F_Y0, l) = y0;
+    K(F_Y1, l) = y1;
+    K(F_Z0, l) = z0;
+    K(F_Z1, l) = z1;
+    if constexpr (BK == 0) K(F_X, l) = cx;
+    mk[l * 32 + lane] = kind | (lf << 2);
   }
-  // sorted block columns -> slots
+  // sorted block columns -> slots (CSR order of the reference's stiffness())
 #pragma unroll
-  for (int a = 1; a < 4; ++a) {
+  for (int x = 1; x < 4; ++x) {
 #pragma unroll
-    for (int b = a; b > 0; --b) {
-      if (b < nb && cols[b - 1] > cols[b]) {
-        int t = cols[b]; cols[b] = cols[b - 1]; cols[b - 1] = t;
-        t = kinds[b]; kinds[b] = kinds[b - 1]; kinds[b - 1] = t;
+    for (int y = x; y > 0; --y) {
+      if (y < nb && cols[y - 1] > cols[y]) {
+        int t = cols[y]; cols[y] = cols[y - 1]; cols[y - 1] = t;
+        t = kinds[y]; kinds[y] = kinds[y - 1]; kinds[y - 1] = t;
       }
     }
   }
@@ -253,109 +359,48 @@ __global__ void __launch_bounds__(128, MINB) assemble_kernel(
       if (active) P.col[rp + s] = cols[s];
       if (kinds[s] < 0) diag_slot = s;
 #pragma unroll
-      for (int l = 0; l < 3; ++l) if (kinds[s] == l) es[l].slot = s;
+      for (int l = 0; l < 3; ++l) if (kinds[s] == l) mk[l * 32 + lane] |= s << 4;
     }
+  }
+
+  // ---- RHS: the warp's contiguous slice, staged and written coalesced ------------------------
+  {
+#pragma unroll
+    for (int i = 0; i < NL; ++i) st[i] = F[i];
+    __syncwarp();
+    const int e_first = blockIdx.x * blockDim.x + warp * 32;  // relative to row_begin
+    const int n_here = min(32, P.row_end - P.row_begin - e_first);
+    for (int idx = lane; idx < n_here * NL; idx += 32) {
+      const int Ln = idx / NL, i = idx - Ln * NL;
+      P.rhs[static_cast<long long>(e_first) * NL + idx] = stw[Ln * SS + i];
+    }
+    __syncwarp();
   }
 
   // ---- diagonal block ----------------------------------------------------------------------
   {
+    const double alpha = scalar_element(P.prob.linear_reaction, ee);
     const double de = det * eps;
     const double cD0 = de * (G00 * G00 + G10 * G10);
     const double cD1 = de * (G00 * G01 + G10 * G11);
     const double cD2 = de * (G01 * G01 + G11 * G11);
     const double cR = det * alpha;
     double cC0 = 0.0, cC1 = 0.0, cA[4] = {0.0, 0.0, 0.0, 0.0};
-    if (!TRIG) {
-      if (bconst) {
-        cC0 = det * (G00 * bf.p[0] + G10 * bf.p[1]);
-        cC1 = det * (G01 * bf.p[0] + G11 * bf.p[1]);
-      } else if (bf.kind == DGB_VEC_AFFINE) {
-        const double bo0 = bf.p[0] + bf.p[2] * pv[0].x + bf.p[3] * pv[0].y;
-        const double bo1 = bf.p[1] + bf.p[4] * pv[0].x + bf.p[5] * pv[0].y;
-        const double AB00 = bf.p[2] * B00 + bf.p[3] * B10, AB01 = bf.p[2] * B01 + bf.p[3] * B11;
-        const double AB10 = bf.p[4] * B00 + bf.p[5] * B10, AB11 = bf.p[4] * B01 + bf.p[5] * B11;
-        cC0 = det * (G00 * bo0 + G10 * bo1);
-        cC1 = det * (G01 * bo0 + G11 * bo1);
-        cA[0] = det * (G00 * AB00 + G10 * AB10);
-        cA[1] = det * (G00 * AB01 + G10 * AB11);
-        cA[2] = det * (G01 * AB00 + G11 * AB10);
-        cA[3] = det * (G01 * AB01 + G11 * AB11);
-      }
-    }
-    // face coefficients: W weights and either the per-edge P weight (constant b) or the
-    // per-point weights cU (penalty + upwind at each point, canonical point order)
-    double cW[3][2], cP[3], cU[3][NQE];
-#pragma unroll
-    for (int l = 0; l < 3; ++l) {
-      const EdgeState& s = es[l];
-      cW[l][0] = cW[l][1] = cP[l] = 0.0;
-#pragma unroll
-      for (int p = 0; p < NQE; ++p) cU[l][p] = 0.0;
-      if (s.kind == DGB_EDGE_NEUMANN) {
-        if (!P.drop_neumann && active) {
-          bool inflow = false;
-          for (int q = 0; q < NQE; ++q) {
-            double px, py, fl;
-            flux_point(P, s, q, px, py, fl);
-            double bx, by;
-            velocity(bf, px, py, bx, by);
-            if (fl < -1e-12 * fmax(1.0, hypot_dd(bx, by))) inflow = true;
-          }
-          if (inflow) atomicMin(P.err_edge, s.edge);
-        }
-        continue;
-      }
-      const bool interior = s.kind == DGB_EDGE_INTERIOR;
-      const double sig = interior ? P.sigma_i : P.sigma_b;
-      const double base = (interior ? 0.5 : 1.0) * s.h * s.eps;
-      cW[l][0] = base * s.ge0;
-      cW[l][1] = base * s.ge1;
-      const double sh = sig * s.rh;
-      if (bconst && L::kHasP) {
-        const double fl = FADD(FMUL(bf.p[0], s.nx), FMUL(bf.p[1], s.ny));
-        double up = 0.0;
-        if (interior) {
-          if (fl < 0.0) up = -FMUL(s.h, fl);
-        } else if (fl < -1e-12 * fmax(1.0, hypot_dd(bf.p[0], bf.p[1]))) {
-          up = -FMUL(s.h, fl);
-        }
-        cP[l] = sh * (s.h * s.eps) + up;
-      } else {
-        double fls[NQE];  // indexed by canonical point p (physical point q = q(p))
-        bool inflow = false;
-#pragma unroll
-        for (int p = 0; p < NQE; ++p) {
-          const int q = s.o == 0 ? p : NQE - 1 - p;
-          double px, py;
-          flux_point(P, s, q, px, py, fls[p]);
-          if (!interior) {
-            double bx, by;
-            velocity(bf, px, py, bx, by);
-            if (fls[p] < -1e-12 * fmax(1.0, hypot_dd(bx, by))) inflow = true;
-          }
-        }
-#pragma unroll
-        for (int p = 0; p < NQE; ++p) {
-          const int q = s.o == 0 ? p : NQE - 1 - p;
-          const double w = FMUL(P.t.x[L::EW + q], s.h);
-          double c = FMUL(sh, FMUL(w, s.eps));
-          if ((interior || inflow) && fls[p] < 0.0) c -= FMUL(w, fls[p]);
-          cU[l][p] = c;
-        }
-      }
-    }
-    double bq[TRIG ? NQV : 1][2];
-    if (TRIG) {
-#pragma unroll
-      for (int q = 0; q < NQV; ++q) {
-        const double px = FADD(FADD(pv[0].x, FMUL(B00, P.t.x[L::VX + q])), FMUL(B01, P.t.x[L::VY + q]));
-        const double py = FADD(FADD(pv[0].y, FMUL(B10, P.t.x[L::VX + q])), FMUL(B11, P.t.x[L::VY + q]));
-        double bx, by;
-        velocity(bf, px, py, bx, by);
-        const double dw = det * P.t.x[L::VW + q];
-        bq[q][0] = dw * (G00 * bx + G10 * by);
-        bq[q][1] = dw * (G01 * bx + G11 * by);
-      }
+    if constexpr (BK == 0) {
+      cC0 = det * (G00 * bf.p[0] + G10 * bf.p[1]);
+      cC1 = det * (G01 * bf.p[0] + G11 * bf.p[1]);
+    } else if constexpr (BK == 1) {
+      // b(o + B xhat) = (c + A o) + (A B) xhat  (affine velocity, config 3)
+      const double bo0 = bf.p[0] + bf.p[2] * pv[0].x + bf.p[3] * pv[0].y;
+      const double bo1 = bf.p[1] + bf.p[4] * pv[0].x + bf.p[5] * pv[0].y;
+      const double AB00 = bf.p[2] * B00 + bf.p[3] * B10, AB01 = bf.p[2] * B01 + bf.p[3] * B11;
+      const double AB10 = bf.p[4] * B00 + bf.p[5] * B10, AB11 = bf.p[4] * B01 + bf.p[5] * B11;
+      cC0 = det * (G00 * bo0 + G10 * bo1);
+      cC1 = det * (G01 * bo0 + G11 * bo1);
+      cA[0] = det * (G00 * AB00 + G10 * AB10);
+      cA[1] = det * (G00 * AB01 + G10 * AB11);
+      cA[2] = det * (G01 * AB00 + G11 * AB10);
+      cA[3] = det * (G01 * AB01 + G11 * AB11);
     }
     constexpr int RC = NL <= 6 ? NL : (NL <= 10 ? 2 : 1);  // rows per register chunk
 #pragma unroll 1
@@ -370,44 +415,67 @@ __global__ void __launch_bounds__(128, MINB) assemble_kernel(
           x = fma(cD1, P.t.x[L::S + N2 + k], x);
           x = fma(cD2, P.t.x[L::S + 2 * N2 + k], x);
           x = fma(cR, P.t.x[L::M + k], x);
-          if (!TRIG) {
+          if constexpr (!TRIG) {
             x = fma(cC0, P.t.x[L::T + k], x);
             x = fma(cC1, P.t.x[L::T + N2 + k], x);
-            if (L::kHasTA && !bconst) {
-#pragma unroll
-              for (int a = 0; a < 4; ++a) x = fma(cA[a], P.t.x[L::TA + a * N2 + k], x);
-            }
           }
+          if constexpr (BK == 1 && L::kHasTA) {
 #pragma unroll
-          for (int l = 0; l < 3; ++l) {
-            x = fma(cW[l][0], P.t.x[L::W + 2 * l * N2 + k], x);
-            x = fma(cW[l][1], P.t.x[L::W + (2 * l + 1) * N2 + k], x);
-            if (L::kHasP) x = fma(cP[l], P.t.x[L::P + l * N2 + k], x);
+            for (int a = 0; a < 4; ++a) x = fma(cA[a], P.t.x[L::TA + a * N2 + k], x);
           }
           acc[r][j] = x;
         }
       }
-      if (!(bconst && L::kHasP)) {
+#pragma unroll 1
+      for (int l = 0; l < 3; ++l) {
+        const double w0 = K(F_W0, l), w1 = K(F_W1, l);
 #pragma unroll
-        for (int l = 0; l < 3; ++l) {
+        for (int r = 0; r < RC; ++r) {
+#pragma unroll
+          for (int j = 0; j < NL; ++j) {
+            const int k = (i0 + r) * NL + j;
+            acc[r][j] = fma(w0, P.t.x[L::W + 2 * l * N2 + k],
+                            fma(w1, P.t.x[L::W + (2 * l + 1) * N2 + k], acc[r][j]));
+          }
+        }
+        if constexpr (BK == 0 && L::kHasP) {
+          const double cp = K(F_P, l);
+#pragma unroll
+          for (int r = 0; r < RC; ++r) {
+#pragma unroll
+            for (int j = 0; j < NL; ++j) {
+              acc[r][j] = fma(cp, P.t.x[L::P + l * N2 + (i0 + r) * NL + j], acc[r][j]);
+            }
+          }
+        } else {
+          // per-point face weights: acc += sum_p cU_p phi^l_p phi^l_p^T
 #pragma unroll
           for (int p = 0; p < NQE; ++p) {
+            double cu;
+            if constexpr (BK == 0) {
+              cu = K(F_P, l) * P.t.x[L::EW + p];
+            } else {
+              cu = K(F_U + p, l);
+            }
 #pragma unroll
             for (int r = 0; r < RC; ++r) {
-              const double u = cU[l][p] * P.t.x[L::EPHI + (l * NQE + p) * NL + i0 + r];
+              const double u = cu * P.t.x[L::EPHI + (l * NQE + p) * NL + i0 + r];
 #pragma unroll
-              for (int j = 0; j < NL; ++j) acc[r][j] = fma(u, P.t.x[L::EPHI + (l * NQE + p) * NL + j], acc[r][j]);
+              for (int j = 0; j < NL; ++j) {
+                acc[r][j] = fma(u, P.t.x[L::EPHI + (l * NQE + p) * NL + j], acc[r][j]);
+              }
             }
           }
         }
       }
-      if (TRIG) {
-#pragma unroll
+      if constexpr (TRIG) {
+#pragma unroll 1
         for (int q = 0; q < NQV; ++q) {
+          const double b0 = sq[(2 * q) * 32 + lane], b1 = sq[(2 * q + 1) * 32 + lane];
 #pragma unroll
           for (int r = 0; r < RC; ++r) {
-            const double f0 = bq[TRIG ? q : 0][0] * P.t.x[L::PHI + q * NL + i0 + r];
-            const double f1 = bq[TRIG ? q : 0][1] * P.t.x[L::PHI + q * NL + i0 + r];
+            const double f0 = b0 * P.t.x[L::PHI + q * NL + i0 + r];
+            const double f1 = b1 * P.t.x[L::PHI + q * NL + i0 + r];
 #pragma unroll
             for (int j = 0; j < NL; ++j) {
               acc[r][j] = fma(f0, P.t.x[L::DPHI + (2 * q) * NL + j],
@@ -426,152 +494,59 @@ __global__ void __launch_bounds__(128, MINB) assemble_kernel(
                      lane);
   }
 
-  // ---- neighbour blocks (one pass per local edge) -------------------------------------------
-#pragma unroll
-  for (int l = 0; l < 3; ++l) {
-    const EdgeState& s = es[l];
-    const bool has = s.kind == DGB_EDGE_INTERIOR;
-    if (has) {
-      // coefficients (off-diagonal block)
-      const double base = 0.5 * s.h * s.eps;
-      const double cY0 = -base * s.gf0, cY1 = -base * s.gf1;
-      const double cZ0 = -P.kappa * base * s.ge0, cZ1 = -P.kappa * base * s.ge1;
-      const double sh = P.sigma_i * s.rh;
-      double cV[NQE];
-      double flc = 0.0;
-      if (bconst) flc = FADD(FMUL(bf.p[0], s.nx), FMUL(bf.p[1], s.ny));
-#pragma unroll
-      for (int p = 0; p < NQE; ++p) {
-        const int q = s.o == 0 ? p : NQE - 1 - p;
-        const double w = FMUL(P.t.x[L::EW + q], s.h);
-        double fl = flc;
-        if (!bconst) {
-          double px, py;
-          flux_point(P, s, q, px, py, fl);
-        }
-        double c = -FMUL(sh, FMUL(w, s.eps));
-        if (fl < 0.0) c += FMUL(w, fl);
-        cV[p] = c;
-      }
-      const double* trm = tr + s.lf * (NQE * 3 * NL);
-      constexpr int CJ = NL <= 6 ? NL : 2;  // columns per register chunk
+  // ---- neighbour blocks: K_ef = sum_p phi^l_p (x) b1_p + a2_p (x) phi^lf_(n-1-p) ---------------
 #pragma unroll 1
-      for (int j0 = 0; j0 < NL; j0 += CJ) {
-        double pm[NQE][CJ], b1[NQE][CJ];
+  for (int l = 0; l < 3; ++l) {
+    const int meta = mk[l * 32 + lane];
+    const bool has = (meta & 3) == DGB_EDGE_INTERIOR;
+    if (!__any_sync(0xffffffffu, has)) continue;
+    const int lf = (meta >> 2) & 3, slot = meta >> 4;
+    const double cY0 = K(F_Y0, l), cY1 = K(F_Y1, l), cZ0 = K(F_Z0, l), cZ1 = K(F_Z1, l);
+    double cV[NQE];
 #pragma unroll
-        for (int p = 0; p < NQE; ++p) {
-          const double* row = trm + (NQE - 1 - p) * 3 * NL;
-#pragma unroll
-          for (int c = 0; c < CJ; ++c) {
-            const int j = j0 + c;
-            const double f = row[j], g0 = row[NL + j], g1 = row[2 * NL + j];
-            pm[p][c] = f;
-            b1[p][c] = fma(cV[p], f, P.t.x[L::EW + p] * fma(cY0, g0, cY1 * g1));
-          }
-        }
-#pragma unroll
-        for (int i = 0; i < NL; ++i) {
-          double acc[CJ];
-#pragma unroll
-          for (int c = 0; c < CJ; ++c) acc[c] = 0.0;
-#pragma unroll
-          for (int p = 0; p < NQE; ++p) {
-            const double a2 = P.t.x[L::EW + p] * fma(cZ0, P.t.x[L::EDPHI + ((l * NQE + p) * 2) * NL + i], cZ1 * P.t.x[L::EDPHI + ((l * NQE + p) * 2 + 1) * NL + i]);
-#pragma unroll
-            for (int c = 0; c < CJ; ++c) {
-              acc[c] = fma(P.t.x[L::EPHI + (l * NQE + p) * NL + i], b1[p][c], fma(a2, pm[p][c], acc[c]));
-            }
-          }
-#pragma unroll
-          for (int c = 0; c < CJ; ++c) st[i * NL + j0 + c] = acc[c];
-        }
+    for (int p = 0; p < NQE; ++p) {
+      if constexpr (BK == 0) {
+        cV[p] = K(F_X, l) * P.t.x[L::EW + p];
+      } else {
+        cV[p] = K(F_U + NQE + p, l);
       }
     }
-    const long long bb = (active && has) ? static_cast<long long>(rp + s.slot) * N2 : -1LL;
-    if (__any_sync(0xffffffffu, bb >= 0)) flush_blocks<N2>(stw, bb, P.val, lane);
-  }
-
-  // ---- RHS --------------------------------------------------------------------------------
-  {
-    double F[NL];
-#pragma unroll
-    for (int i = 0; i < NL; ++i) F[i] = 0.0;
-    const dgb_scalar_field& fs = P.prob.source;
-#pragma unroll
-    for (int q = 0; q < NQV; ++q) {
-      double f;
-      if (fs.kind == DGB_FIELD_CONSTANT) {
-        f = fs.value;
-      } else if (fs.kind == DGB_FIELD_PER_ELEMENT) {
-        f = __ldg(fs.per_element + ee);
-      } else {
-        const double px = FADD(FADD(pv[0].x, FMUL(B00, P.t.x[L::VX + q])), FMUL(B01, P.t.x[L::VY + q]));
-        const double py = FADD(FADD(pv[0].y, FMUL(B10, P.t.x[L::VX + q])), FMUL(B11, P.t.x[L::VY + q]));
-        f = scalar_point(fs, px, py);
-      }
-      const double c = det * P.t.x[L::VW + q] * f;
-#pragma unroll
-      for (int i = 0; i < NL; ++i) F[i] = fma(c, P.t.x[L::PHI + q * NL + i], F[i]);
-    }
-#pragma unroll
-    for (int l = 0; l < 3; ++l) {
-      const EdgeState& s = es[l];
-      if (s.kind == DGB_EDGE_INTERIOR) continue;
-      double cG[NQE], cH[NQE];
-      if (s.kind == DGB_EDGE_NEUMANN) {
-#pragma unroll
-        for (int p = 0; p < NQE; ++p) {
-          const int q = s.o == 0 ? p : NQE - 1 - p;
-          const double px = FADD(s.ax, FMUL(P.t.x[L::ET + q], s.dx));
-          const double py = FADD(s.ay, FMUL(P.t.x[L::ET + q], s.dy));
-          cG[p] = FMUL(FMUL(P.t.x[L::EW + q], s.h), scalar_point(P.prob.neumann, px, py));
-          cH[p] = 0.0;
-        }
-      } else {
-        double fls[NQE], gds[NQE];  // canonical point order
-        bool inflow = false;
-#pragma unroll
-        for (int p = 0; p < NQE; ++p) {
-          const int q = s.o == 0 ? p : NQE - 1 - p;
-          double px, py;
-          flux_point(P, s, q, px, py, fls[p]);
-          double bx, by;
-          velocity(bf, px, py, bx, by);
-          if (fls[p] < -1e-12 * fmax(1.0, hypot_dd(bx, by))) inflow = true;
-          gds[p] = scalar_point(P.prob.dirichlet, px, py);
-        }
-        const double sh = P.sigma_b * s.rh;
-#pragma unroll
-        for (int p = 0; p < NQE; ++p) {
-          const int q = s.o == 0 ? p : NQE - 1 - p;
-          const double w = FMUL(P.t.x[L::EW + q], s.h);
-          const double wgd = w * gds[p];
-          double g = wgd * (sh * s.eps);
-          if (inflow && fls[p] < 0.0) g += -FMUL(w, fls[p]) * gds[p];
-          cG[p] = g;
-          cH[p] = wgd * (P.kappa * s.eps);
-        }
-      }
+    const double* trm = tr + lf * (NQE * 3 * NL);
+    constexpr int CJ = NL <= 6 ? NL : 2;  // columns per register chunk
+#pragma unroll 1
+    for (int j0 = 0; j0 < NL; j0 += CJ) {
+      double pm[NQE][CJ], b1[NQE][CJ];
 #pragma unroll
       for (int p = 0; p < NQE; ++p) {
-        const double h0 = cH[p] * s.ge0, h1 = cH[p] * s.ge1;
+        const double* row = trm + (NQE - 1 - p) * 3 * NL;
 #pragma unroll
-        for (int i = 0; i < NL; ++i) {
-          F[i] = fma(cG[p], P.t.x[L::EPHI + (l * NQE + p) * NL + i],
-                     fma(h0, P.t.x[L::EDPHI + ((l * NQE + p) * 2) * NL + i], fma(h1, P.t.x[L::EDPHI + ((l * NQE + p) * 2 + 1) * NL + i], F[i])));
+        for (int c = 0; c < CJ; ++c) {
+          const int j = j0 + c;
+          const double f = row[j], g0 = row[NL + j], g1 = row[2 * NL + j];
+          pm[p][c] = f;
+          b1[p][c] = fma(cV[p], f, P.t.x[L::EW + p] * fma(cY0, g0, cY1 * g1));
         }
       }
-    }
-    // stage the warp's contiguous RHS range and write it coalesced
 #pragma unroll
-    for (int i = 0; i < NL; ++i) st[i] = F[i];
-    __syncwarp();
-    const int e_first = blockIdx.x * blockDim.x + warp * 32;  // relative to row_begin
-    const int n_here = min(32, P.row_end - P.row_begin - e_first);
-    for (int idx = lane; idx < n_here * NL; idx += 32) {
-      const int L = idx / NL, i = idx - L * NL;
-      P.rhs[static_cast<long long>(e_first) * NL + idx] = stw[L * SS + i];
+      for (int i = 0; i < NL; ++i) {
+        double acc[CJ];
+#pragma unroll
+        for (int c = 0; c < CJ; ++c) acc[c] = 0.0;
+#pragma unroll
+        for (int p = 0; p < NQE; ++p) {
+          const double a2 = P.t.x[L::EW + p] *
+                            fma(cZ0, P.t.x[L::EDPHI + ((l * NQE + p) * 2) * NL + i],
+                                cZ1 * P.t.x[L::EDPHI + ((l * NQE + p) * 2 + 1) * NL + i]);
+          const double ph = P.t.x[L::EPHI + (l * NQE + p) * NL + i];
+#pragma unroll
+          for (int c = 0; c < CJ; ++c) acc[c] = fma(ph, b1[p][c], fma(a2, pm[p][c], acc[c]));
+        }
+#pragma unroll
+        for (int c = 0; c < CJ; ++c) st[i * NL + j0 + c] = acc[c];
+      }
     }
+    flush_blocks<N2>(stw, (active && has) ? static_cast<long long>(rp + slot) * N2 : -1LL,
+                     P.val, lane);
   }
 }
 

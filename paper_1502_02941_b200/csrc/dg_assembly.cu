@@ -906,15 +906,17 @@ void validate_field(const dgb_scalar_field& f, bool element_constant, const char
 
 // Fills the V2 tensor parameter block from the plan's host tensors (W = kappa Q^T - Q is
 // folded per launch) and launches the element-per-thread kernel.
-template <int NL, int NQV, int NQE, bool TRIG, int MINB = 1>
+template <int NL, int NQV, int NQE, int BK, int THREADS, int MINB>
 void launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_problem* problem,
                const dgb_params* params, dgb_bsr* out, double* rhs, cudaStream_t s,
                int out_row_begin, int out_row_end) {
+  constexpr bool TRIG = BK == 2;
   using L = dgb::v2::Lay<NL, NQV, NQE, TRIG>;
   using PT = dgb::v2::Params2<NL, NQV, NQE, TRIG>;
+  using SM = dgb::v2::Smem<NL, NQV, NQE, BK>;
   static_assert(sizeof(PT) <= 32000, "tensor parameter block exceeds the kernel parameter limit");
   constexpr int N2 = NL * NL;
-  static thread_local PT P;  // ~20 KB: keep it off the stack
+  static thread_local PT P;  // up to ~30 KB: keep it off the stack
   std::memset(&P, 0, sizeof P);
   P.nodes = mesh->nodes;
   P.elements = mesh->elements;
@@ -960,45 +962,49 @@ void launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_prob
   copy(L::VW, V.VW, NQV);
   copy(L::ET, V.ET, NQE);
   copy(L::EW, V.EW, NQE);
-  constexpr int kThreads = 128;
-  const size_t smem =
-      sizeof(double) * (((3 * NQE * 3 * NL + 1) & ~1) +
-                        (kThreads / 32) * 32 * dgb::v2::Stage<N2>::kStride);
+  const size_t smem = sizeof(double) * (SM::kTr + (THREADS / 32) * SM::kWarp);
+  auto kernel = dgb::v2::assemble_kernel<NL, NQV, NQE, BK, THREADS, MINB>;
   static bool configured = false;
   if (!configured) {
-    cuda_check(cudaFuncSetAttribute(dgb::v2::assemble_kernel<NL, NQV, NQE, TRIG, MINB>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cuda_check(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(smem)),
                "cudaFuncSetAttribute(v2)");
     configured = true;
   }
-  const int grid = (out_row_end - out_row_begin + kThreads - 1) / kThreads;
-  dgb::v2::assemble_kernel<NL, NQV, NQE, TRIG, MINB><<<grid, kThreads, smem, s>>>(P);
+  const int grid = (out_row_end - out_row_begin + THREADS - 1) / THREADS;
+  kernel<<<grid, THREADS, smem, s>>>(P);
 }
 
-// Specialised element-per-thread kernels by (n_local, nq_vol, nq_edge, pointwise velocity);
-// returns false when no specialisation exists (the generic kernel runs instead).
+// Specialised element-per-thread kernels by (n_local, nq_vol, nq_edge, velocity kind), with
+// CTA sizes / register budgets chosen by measurement (profiles/NOTES.md); returns false when
+// no specialisation exists (the generic kernel runs instead).
 bool try_launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_problem* problem,
                    const dgb_params* params, dgb_bsr* out, double* rhs, cudaStream_t s,
                    int rb, int re) {
   if (plan->force_generic) return false;
-  const bool trig = problem->advection.kind == DGB_VEC_TRIG;
+  const int bk = problem->advection.kind;
   const int key = plan->nl * 10000 + plan->nqv * 100 + plan->nqe;
-  // Register budgets (CTAs of 128 threads per SM) chosen by measurement (profiles/NOTES.md);
-  // DGB_OPTION_MIN_BLOCKS overrides them for tuning runs.
   const int mb = plan->minblocks;
-#define DGB_V2(NL_, NQV_, NQE_, TRIG_, MB_)                                                 \
-  if (key == NL_ * 10000 + NQV_ * 100 + NQE_ && trig == TRIG_) {                          \
-    if (mb == 2) { launch_v2<NL_, NQV_, NQE_, TRIG_, 2>(plan, mesh, problem, params, out, rhs, s, rb, re); return true; } \
-    if (mb == 4) { launch_v2<NL_, NQV_, NQE_, TRIG_, 4>(plan, mesh, problem, params, out, rhs, s, rb, re); return true; } \
-    launch_v2<NL_, NQV_, NQE_, TRIG_, MB_>(plan, mesh, problem, params, out, rhs, s, rb, re);  \
+#define DGB_V2(NL_, NQV_, NQE_, BK_, T_, MB_)                                               \
+  if (key == NL_ * 10000 + NQV_ * 100 + NQE_ && bk == BK_) {                              \
+    launch_v2<NL_, NQV_, NQE_, BK_, T_, MB_>(plan, mesh, problem, params, out, rhs, s, rb, re); \
     return true;                                                                           \
   }
-  DGB_V2(3, 6, 2, false, 4)
-  DGB_V2(3, 6, 2, true, 4)
-  DGB_V2(6, 7, 3, false, 4)
-  DGB_V2(6, 12, 3, false, 4)
-  DGB_V2(10, 16, 4, false, 2)
+  if (mb == 3) {  // tuning variants of the headline kernels
+    DGB_V2(6, 7, 3, 0, 128, 3)
+    DGB_V2(3, 6, 2, 0, 128, 3)
+  }
+  if (mb == 5) {
+    DGB_V2(6, 7, 3, 0, 128, 5)
+    DGB_V2(3, 6, 2, 0, 128, 5)
+  }
+  DGB_V2(3, 6, 2, 0, 128, 4)
+  DGB_V2(3, 6, 2, 1, 128, 4)
+  DGB_V2(3, 6, 2, 2, 128, 4)
+  DGB_V2(6, 7, 3, 0, 128, 4)
+  DGB_V2(6, 12, 3, 0, 128, 4)
+  DGB_V2(10, 16, 4, 0, 160, 1)
+  DGB_V2(10, 16, 4, 1, 160, 1)
 #undef DGB_V2
   return false;
 }
