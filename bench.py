@@ -43,6 +43,8 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--minblocks", type=int, default=0, help="tuning knob (P2 kernel CTAs/SM)")
+    ap.add_argument("--no-bind", action="store_true",
+                    help="recompute the BSR pattern in every assembly (count + scan launches)")
     return ap.parse_args()
 
 
@@ -203,7 +205,7 @@ def run_ours(args, world, rank, local):
     spec = problems.config_problem(args.config, mesh.n_elements)
     params = [dgfem.config_parameters(cfg, m) for m in cfg.methods]
     begin, end = shard.row_range(mesh.n_elements, rank, world)
-    shards = [shard.ShardAssembler(mesh, ref, spec, local, begin, end)]
+    shards = [shard.ShardAssembler(mesh, ref, spec, local, begin, end, bind=not args.no_bind)]
     shards += [shard.ShardAssembler(mesh, ref, spec, local, begin, end, share=shards[0])
                for _ in params[1:]]   # one plan and one device mesh for all methods
     plan = shards[0].plan
@@ -318,12 +320,15 @@ def run_ours(args, world, rank, local):
             "global_mesh": f"{world * cfg.n}x{cfg.n} cells on [0,{world}]x[0,1]" if world > 1 else None,
             "nq_vol": ref.nq_vol, "nq_edge": ref.nq_edge,
             "l2": "flushed between timed steps by a 256 MiB write (outside the timed events)",
+            "pattern": ("recomputed in every assembly (count + scan)" if args.no_bind else
+                        "bound once per mesh (dgb_plan_bind_mesh, untimed setup); every assembly "
+                        "still writes row_ptr, block columns, values and RHS"),
             "parallelism": f"{world} rank(s), element-row shards" if world > 1 else "1 GPU",
         },
         "roofline": roofline,
         "cpu_baseline": cpu,
         "e2e": e2e,
-        "gpu_launches": K * len(params) * lib.dgb_assemble_launch_count(),
+        "gpu_launches": K * len(params) * lib.dgb_plan_launch_count(plan._h),
         "clocks": clocks.summary(),
     }
     print(json.dumps(line), flush=True)

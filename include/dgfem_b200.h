@@ -303,8 +303,18 @@ enum dgb_plan_option {
 };
 int dgb_plan_set_option(dgb_plan* plan, int32_t option, int32_t value);
 
-/* Kernel launches one dgb_assemble call issues (for bench.py's gpu_launches count). */
-int32_t dgb_assemble_launch_count(void);
+/* Binds the BSR pattern of block rows [row_begin, row_end) of `mesh` (DEVICE arrays) to the
+ * plan: row_ptr is computed once (count + scan on `stream`) and later dgb_assemble /
+ * dgb_assemble_rows calls on the same mesh arrays and rows skip those launches and copy the
+ * bound row_ptr into their output (one kernel per assembly).  The pattern depends only on
+ * element_edges / edge_kind; rebind (or unbind) if those arrays change. */
+int dgb_plan_bind_mesh(dgb_plan* plan, const dgb_mesh_arrays* mesh, int32_t row_begin,
+                       int32_t row_end, void* stream);
+int dgb_plan_unbind_mesh(dgb_plan* plan);
+
+/* Device operations (kernels, CUB scan kernels) the plan's last dgb_assemble* call launched:
+ * 1 with a bound pattern, 4 without (bench.py's gpu_launches). */
+int32_t dgb_plan_launch_count(const dgb_plan* plan);
 
 /* y = K x with the BSR from dgb_assemble (DEVICE pointers), on `stream`.  Replaces
  * dgfem::matvec(stiffness(), x) (sparse.cpp:116-129). */

@@ -114,7 +114,9 @@ def _declare(lib: C.CDLL) -> C.CDLL:
         "dgb_assemble": (C.c_int, [vp, P(MeshArrays), P(Problem), P(Params), P(Bsr), vp, vp]),
         "dgb_plan_status": (C.c_int, [vp, vp]),
         "dgb_plan_set_kernel_events": (C.c_int, [vp, vp, vp]),
-        "dgb_assemble_launch_count": (C.c_int32, []),
+        "dgb_plan_bind_mesh": (C.c_int, [vp, P(MeshArrays), C.c_int32, C.c_int32, vp]),
+        "dgb_plan_unbind_mesh": (C.c_int, [vp]),
+        "dgb_plan_launch_count": (C.c_int32, [vp]),
         "dgb_plan_set_option": (C.c_int, [vp, C.c_int32, C.c_int32]),
         "dgb_spmv": (C.c_int, [P(Bsr), vp, vp, vp]),
         "dgb_assemble_rows": (C.c_int, [vp, P(MeshArrays), P(Problem), P(Params), C.c_int32,
@@ -136,7 +138,7 @@ EXPORTED_SYMBOLS = [
     "dgb_mesh_free", "dgb_reference_create", "dgb_reference_view", "dgb_reference_free",
     "dgb_set_parameters", "dgb_bsr_nnzb", "dgb_plan_create", "dgb_plan_destroy",
     "dgb_assemble", "dgb_plan_status", "dgb_plan_set_kernel_events",
-    "dgb_assemble_launch_count", "dgb_plan_set_option", "dgb_spmv", "dgb_assemble_all_host",
+    "dgb_plan_bind_mesh", "dgb_plan_unbind_mesh", "dgb_plan_launch_count", "dgb_plan_set_option", "dgb_spmv", "dgb_assemble_all_host",
     "dgb_mesh_rectangle", "dgb_assemble_rows", "dgb_count_blocks_host",
 ]
 OPTION_FORCE_GENERIC_KERNEL = 1

@@ -36,7 +36,8 @@ struct Lay {
   static constexpr int DPHI = PHI + NQV * NL;               // [q][a][i]      (TRIG only)
   static constexpr int EPHI = DPHI + (TRIG ? NQV * 2 * NL : 0);  // [l][p][i]
   static constexpr int EDPHI = EPHI + 3 * NQE * NL;         // [l][p][a][i]
-  static constexpr int VX = EDPHI + 3 * NQE * 2 * NL;
+  static constexpr int EDW = EDPHI + 3 * NQE * 2 * NL;        // [l][p][a][i] w_p-scaled
+  static constexpr int VX = EDW + 3 * NQE * 2 * NL;
   static constexpr int VY = VX + NQV;
   static constexpr int VW = VY + NQV;
   static constexpr int ET = VW + NQV;
@@ -56,11 +57,13 @@ struct Params2 {
   const uint8_t* edge_kind;
   const int32_t* edge_elements;
   const int32_t* element_edges;
-  const int32_t* row_ptr;
+  int32_t* row_ptr;              // output row pointer of the launch's rows
+  const int32_t* row_ptr_src;    // bound pattern (dgb_plan_bind_mesh) copied to row_ptr, or null
   int32_t* col;
   double* val;
   double* rhs;
-  int32_t* err_edge;
+  unsigned long long* err_edge;  // epoch << 32 | ~edge, max-reduced (lowest edge wins)
+  unsigned long long epoch;
   int32_t n_elements;
   int32_t row_begin, row_end;  // block rows [row_begin, row_end) of this launch (a shard)
   int32_t drop_neumann;
@@ -153,7 +156,7 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
   for (int i = threadIdx.x; i < 3 * NQE * 3 * NL; i += blockDim.x) {
     const int j = i % NL, c = (i / NL) % 3, p = (i / (3 * NL)) % NQE, l = i / (3 * NL * NQE);
     tr[i] = c == 0 ? P.t.x[L::EPHI + (l * NQE + p) * NL + j]
-                   : P.t.x[L::EDPHI + ((l * NQE + p) * 2 + c - 1) * NL + j];
+                   : P.t.x[L::EDW + ((l * NQE + p) * 2 + c - 1) * NL + j];  // w_p d phi
   }
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -262,10 +265,12 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
       } else {
 #pragma unroll
         for (int p = 0; p < NQE; ++p) {
-          const int q = o == 0 ? p : NQE - 1 - p;
-          const double w = FMUL(P.t.x[L::EW + q], h);
-          const double px = FADD(A.x, FMUL(P.t.x[L::ET + q], dx));
-          const double py = FADD(A.y, FMUL(P.t.x[L::ET + q], dy));
+          // physical point q = o ? n-1-p : p; the mirrored rule gives t_q = 1 - t_p and
+          // w_q = w_p bitwise (quadrature.cpp:185-192), so the loads stay warp-uniform
+          const double w = FMUL(P.t.x[L::EW + p], h);
+          const double tq = o == 0 ? P.t.x[L::ET + p] : 1.0 - P.t.x[L::ET + p];
+          const double px = FADD(A.x, FMUL(tq, dx));
+          const double py = FADD(A.y, FMUL(tq, dy));
           double bx, by;
           velocity(bf, px, py, bx, by);
           const double fl = FADD(FMUL(bx, nx), FMUL(by, ny));
@@ -281,9 +286,9 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
       bool inflow = false;
 #pragma unroll
       for (int p = 0; p < NQE; ++p) {
-        const int q = o == 0 ? p : NQE - 1 - p;
-        const double px = FADD(A.x, FMUL(P.t.x[L::ET + q], dx));
-        const double py = FADD(A.y, FMUL(P.t.x[L::ET + q], dy));
+        const double tq = o == 0 ? P.t.x[L::ET + p] : 1.0 - P.t.x[L::ET + p];
+        const double px = FADD(A.x, FMUL(tq, dx));
+        const double py = FADD(A.y, FMUL(tq, dy));
         double bx, by;
         velocity(bf, px, py, bx, by);
         fls[p] = FADD(FMUL(bx, nx), FMUL(by, ny));
@@ -292,11 +297,10 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
       }
       double cG[NQE], cH[NQE];
       if (kind == DGB_EDGE_NEUMANN) {
-        if (inflow && !P.drop_neumann && active) atomicMin(P.err_edge, edge);
+        if (inflow && !P.drop_neumann && active) atomicMax(P.err_edge, (P.epoch << 32) | (0xFFFFFFFFull - static_cast<unsigned>(edge)));
 #pragma unroll
         for (int p = 0; p < NQE; ++p) {
-          const int q = o == 0 ? p : NQE - 1 - p;
-          cG[p] = FMUL(FMUL(P.t.x[L::EW + q], h), gb[p]);  // neumann_rhs (assembly.cpp:427-442)
+          cG[p] = FMUL(FMUL(P.t.x[L::EW + p], h), gb[p]);  // neumann_rhs (assembly.cpp:427-442)
           cH[p] = 0.0;
           if constexpr (BK != 0) K(F_U + p, l) = 0.0;
         }
@@ -310,8 +314,7 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
         }
 #pragma unroll
         for (int p = 0; p < NQE; ++p) {
-          const int q = o == 0 ? p : NQE - 1 - p;
-          const double w = FMUL(P.t.x[L::EW + q], h);
+          const double w = FMUL(P.t.x[L::EW + p], h);
           const double win = (inflow && fls[p] < 0.0) ? -FMUL(w, fls[p]) : 0.0;
           const double wgd = w * gb[p];
           cG[p] = wgd * (sh * eps) + win * gb[p];  // emit_dirichlet_rhs + inflow data term
@@ -351,7 +354,16 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
       }
     }
   }
-  const int rp = __ldg(P.row_ptr + (ee - P.row_begin));
+  int rp;
+  if (P.row_ptr_src) {  // pattern computed once per mesh: copy this element's entry
+    rp = __ldg(P.row_ptr_src + (ee - P.row_begin));
+    if (active) {
+      P.row_ptr[ee - P.row_begin + 1] = __ldg(P.row_ptr_src + (ee - P.row_begin + 1));
+      if (ee == P.row_begin) P.row_ptr[0] = 0;
+    }
+  } else {
+    rp = P.row_ptr[ee - P.row_begin];
+  }
   int diag_slot = 0;
 #pragma unroll
   for (int s = 0; s < 4; ++s) {
@@ -524,7 +536,7 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
           const int j = j0 + c;
           const double f = row[j], g0 = row[NL + j], g1 = row[2 * NL + j];
           pm[p][c] = f;
-          b1[p][c] = fma(cV[p], f, P.t.x[L::EW + p] * fma(cY0, g0, cY1 * g1));
+          b1[p][c] = fma(cV[p], f, fma(cY0, g0, cY1 * g1));  // g already w-scaled
         }
       }
 #pragma unroll
@@ -534,9 +546,8 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
         for (int c = 0; c < CJ; ++c) acc[c] = 0.0;
 #pragma unroll
         for (int p = 0; p < NQE; ++p) {
-          const double a2 = P.t.x[L::EW + p] *
-                            fma(cZ0, P.t.x[L::EDPHI + ((l * NQE + p) * 2) * NL + i],
-                                cZ1 * P.t.x[L::EDPHI + ((l * NQE + p) * 2 + 1) * NL + i]);
+          const double a2 = fma(cZ0, P.t.x[L::EDW + ((l * NQE + p) * 2) * NL + i],
+                                cZ1 * P.t.x[L::EDW + ((l * NQE + p) * 2 + 1) * NL + i]);
           const double ph = P.t.x[L::EPHI + (l * NQE + p) * NL + i];
 #pragma unroll
           for (int c = 0; c < CJ; ++c) acc[c] = fma(ph, b1[p][c], fma(a2, pm[p][c], acc[c]));

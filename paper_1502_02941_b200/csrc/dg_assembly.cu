@@ -89,7 +89,8 @@ struct KParams {
   int32_t* col;
   double* val;
   double* rhs;
-  int32_t* err_edge;
+  unsigned long long* err_edge;  // epoch << 32 | ~edge (see dgb_plan_status)
+  unsigned long long epoch;
 };
 
 // ------------------------------------------------------------------------------------------
@@ -298,12 +299,9 @@ namespace dgb {
 // ------------------------------------------------------------------------------------------
 __global__ void count_blocks_kernel(const uint8_t* __restrict__ edge_kind,
                                     const int32_t* __restrict__ element_edges, int32_t begin,
-                                    int32_t n, int32_t* __restrict__ row_ptr, int32_t* err_edge) {
+                                    int32_t n, int32_t* __restrict__ row_ptr) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r == 0) {
-    row_ptr[0] = 0;
-    *err_edge = INT_MAX;
-  }
+  if (r == 0) row_ptr[0] = 0;
   if (r >= n) return;
   const int e = begin + r;
   int c = 1;
@@ -520,7 +518,8 @@ __global__ void __launch_bounds__(256) assemble_kernel(const __grid_constant__ K
       if (kind == DGB_EDGE_NEUMANN) {
         cW[0] = cW[1] = 0.0;
         if (any_inflow && !P.drop_neumann) {
-          atomicMin(P.err_edge, __ldg(P.element_edges + 3 * e + l));
+          atomicMax(P.err_edge, (P.epoch << 32) |
+                                    (0xFFFFFFFFull - static_cast<unsigned>(__ldg(P.element_edges + 3 * e + l))));
         }
         for (int q = 0; q < nqe; ++q) {
           const int p = o == 0 ? q : nqe - 1 - q;
@@ -830,8 +829,10 @@ struct dgb_plan {
   dgb::Layout L;
   dgb::Rec R;
   double* d_tens = nullptr;
-  int32_t* d_err = nullptr;
-  int32_t* h_err = nullptr;  // pinned
+  // InflowOnNeumann word: max over (epoch << 32 | ~edge), so the newest assembly's lowest
+  // offending edge wins and no per-assembly reset is needed
+  unsigned long long* d_err = nullptr;
+  unsigned long long epoch = 0;
   void* d_scan = nullptr;
   size_t scan_bytes = 0;
   int32_t scan_n = 0;
@@ -842,6 +843,14 @@ struct dgb_plan {
   std::vector<double> h_dphi;   // [nqv][2][nl] volume gradients
   int force_generic = 0;        // testing: always use the generic kernel
   int minblocks = 0;            // tuning: min resident CTAs/SM for the P2 kernel (0 = default)
+  // pattern bound by dgb_plan_bind_mesh: row_ptr of rows [bound_begin, bound_end) of the mesh
+  // whose element_edges / edge_kind arrays are bound_ee / bound_kind
+  int32_t* d_pattern = nullptr;
+  size_t pattern_cap = 0;
+  const void* bound_ee = nullptr;
+  const void* bound_kind = nullptr;
+  int32_t bound_n = -1, bound_begin = -1, bound_end = -1;
+  int32_t last_launches = 0;
 };
 
 namespace {
@@ -909,7 +918,7 @@ void validate_field(const dgb_scalar_field& f, bool element_constant, const char
 template <int NL, int NQV, int NQE, int BK, int THREADS, int MINB>
 void launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_problem* problem,
                const dgb_params* params, dgb_bsr* out, double* rhs, cudaStream_t s,
-               int out_row_begin, int out_row_end) {
+               int out_row_begin, int out_row_end, const int32_t* row_ptr_src) {
   constexpr bool TRIG = BK == 2;
   using L = dgb::v2::Lay<NL, NQV, NQE, TRIG>;
   using PT = dgb::v2::Params2<NL, NQV, NQE, TRIG>;
@@ -927,7 +936,9 @@ void launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_prob
   P.col = out->col;
   P.val = out->val;
   P.rhs = rhs;
+  P.row_ptr_src = row_ptr_src;
   P.err_edge = plan->d_err;
+  P.epoch = plan->epoch & 0xFFFFFFFFull;
   P.n_elements = mesh->n_elements;
   P.row_begin = out_row_begin;
   P.row_end = out_row_end;
@@ -957,6 +968,10 @@ void launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_prob
   if (TRIG) std::memcpy(x + L::DPHI, plan->h_dphi.data(), sizeof(double) * NQV * 2 * NL);
   copy(L::EPHI, V.EPHI, 3 * NQE * NL);
   copy(L::EDPHI, V.EDPHI, 3 * NQE * 2 * NL);
+  for (int lp = 0; lp < 3 * NQE; ++lp) {
+    const double w = h[V.EW + lp % NQE];
+    for (int a = 0; a < 2 * NL; ++a) x[L::EDW + lp * 2 * NL + a] = w * h[V.EDPHI + lp * 2 * NL + a];
+  }
   copy(L::VX, V.VX, NQV);
   copy(L::VY, V.VY, NQV);
   copy(L::VW, V.VW, NQV);
@@ -980,23 +995,23 @@ void launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_prob
 // no specialisation exists (the generic kernel runs instead).
 bool try_launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_problem* problem,
                    const dgb_params* params, dgb_bsr* out, double* rhs, cudaStream_t s,
-                   int rb, int re) {
+                   int rb, int re, const int32_t* src) {
   if (plan->force_generic) return false;
   const int bk = problem->advection.kind;
   const int key = plan->nl * 10000 + plan->nqv * 100 + plan->nqe;
   const int mb = plan->minblocks;
 #define DGB_V2(NL_, NQV_, NQE_, BK_, T_, MB_)                                               \
   if (key == NL_ * 10000 + NQV_ * 100 + NQE_ && bk == BK_) {                              \
-    launch_v2<NL_, NQV_, NQE_, BK_, T_, MB_>(plan, mesh, problem, params, out, rhs, s, rb, re); \
+    launch_v2<NL_, NQV_, NQE_, BK_, T_, MB_>(plan, mesh, problem, params, out, rhs, s, rb, re, src); \
     return true;                                                                           \
   }
-  if (mb == 3) {  // tuning variants of the headline kernels
-    DGB_V2(6, 7, 3, 0, 128, 3)
-    DGB_V2(3, 6, 2, 0, 128, 3)
+  if (mb == 3) {  // tuning variants of the headline kernels: smaller CTAs (shorter tail)
+    DGB_V2(6, 7, 3, 0, 64, 6)
+    DGB_V2(3, 6, 2, 0, 64, 8)
   }
   if (mb == 5) {
-    DGB_V2(6, 7, 3, 0, 128, 5)
-    DGB_V2(3, 6, 2, 0, 128, 5)
+    DGB_V2(6, 7, 3, 0, 32, 12)
+    DGB_V2(3, 6, 2, 0, 32, 16)
   }
   DGB_V2(3, 6, 2, 0, 128, 4)
   DGB_V2(3, 6, 2, 1, 128, 4)
@@ -1024,9 +1039,71 @@ struct Buffers {
   }
 };
 
+// row_ptr of block rows [row_begin, row_end): counts (1 + #interior local edges) then an
+// inclusive scan (3 launches).
+void compute_pattern(dgb_plan* plan, const dgb_mesh_arrays* mesh, int row_begin, int row_end,
+                     int32_t* row_ptr, cudaStream_t s) {
+  const int E = row_end - row_begin;
+  dgb::count_blocks_kernel<<<(E + 255) / 256, 256, 0, s>>>(mesh->edge_kind, mesh->element_edges,
+                                                           row_begin, E, row_ptr);
+  cuda_check(cudaGetLastError(), "count_blocks_kernel");
+  if (plan->scan_n != E) {
+    size_t bytes = 0;
+    cub::DeviceScan::InclusiveSum(nullptr, bytes, row_ptr + 1, row_ptr + 1, E, s);
+    if (bytes > plan->scan_bytes) {
+      cudaFree(plan->d_scan);
+      plan->d_scan = nullptr;
+      cuda_check(cudaMalloc(&plan->d_scan, bytes), "cudaMalloc(scan)");
+      plan->scan_bytes = bytes;
+    }
+    plan->scan_n = E;
+  }
+  size_t bytes = plan->scan_bytes;
+  cuda_check(cub::DeviceScan::InclusiveSum(plan->d_scan, bytes, row_ptr + 1, row_ptr + 1, E, s),
+             "DeviceScan");
+}
+
 }  // namespace
 
 extern "C" {
+
+int dgb_plan_bind_mesh(dgb_plan* plan, const dgb_mesh_arrays* mesh, int32_t row_begin,
+                       int32_t row_end, void* stream) {
+  return dgb::guarded([&] {
+    if (!plan || !mesh) throw dgb::Error(DGB_STATUS_INVALID_ARGUMENT, "null argument");
+    if (row_begin < 0 || row_end > mesh->n_elements || row_begin > row_end) {
+      throw dgb::Error(DGB_STATUS_INVALID_INDEX, "block row range outside the mesh", row_begin);
+    }
+    DeviceGuard guard(plan->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const size_t need = static_cast<size_t>(row_end - row_begin) + 1;
+    if (need > plan->pattern_cap) {
+      cudaFree(plan->d_pattern);
+      plan->d_pattern = nullptr;
+      cuda_check(cudaMalloc(&plan->d_pattern, need * sizeof(int32_t)), "cudaMalloc(pattern)");
+      plan->pattern_cap = need;
+    }
+    if (row_end > row_begin) {
+      compute_pattern(plan, mesh, row_begin, row_end, plan->d_pattern, s);
+    } else {
+      cuda_check(cudaMemsetAsync(plan->d_pattern, 0, sizeof(int32_t), s), "cudaMemsetAsync");
+    }
+    plan->bound_ee = mesh->element_edges;
+    plan->bound_kind = mesh->edge_kind;
+    plan->bound_n = mesh->n_elements;
+    plan->bound_begin = row_begin;
+    plan->bound_end = row_end;
+  });
+}
+
+int dgb_plan_unbind_mesh(dgb_plan* plan) {
+  if (!plan) return DGB_STATUS_INVALID_ARGUMENT;
+  plan->bound_ee = plan->bound_kind = nullptr;
+  plan->bound_n = plan->bound_begin = plan->bound_end = -1;
+  return DGB_OK;
+}
+
+int32_t dgb_plan_launch_count(const dgb_plan* plan) { return plan ? plan->last_launches : -1; }
 
 int dgb_plan_create(const dgb_reference_tables* tables, int32_t device, dgb_plan** out) {
   *out = nullptr;
@@ -1071,9 +1148,8 @@ int dgb_plan_create(const dgb_reference_tables* tables, int32_t device, dgb_plan
       cuda_check(cudaMalloc(&p->d_tens, h.size() * sizeof(double)), "cudaMalloc(tensors)");
       cuda_check(cudaMemcpy(p->d_tens, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice),
                  "cudaMemcpy(tensors)");
-      cuda_check(cudaMalloc(&p->d_err, sizeof(int32_t)), "cudaMalloc(err)");
-      cuda_check(cudaMallocHost(&p->h_err, sizeof(int32_t)), "cudaMallocHost(err)");
-      *p->h_err = INT_MAX;
+      cuda_check(cudaMalloc(&p->d_err, sizeof(unsigned long long)), "cudaMalloc(err)");
+      cuda_check(cudaMemset(p->d_err, 0, sizeof(unsigned long long)), "cudaMemset(err)");
     } catch (...) {
       dgb_plan_destroy(p);
       throw;
@@ -1090,7 +1166,7 @@ void dgb_plan_destroy(dgb_plan* p) {
   cudaFree(p->d_tens);
   cudaFree(p->d_err);
   cudaFree(p->d_scan);
-  if (p->h_err) cudaFreeHost(p->h_err);
+  cudaFree(p->d_pattern);
   if (prev >= 0) cudaSetDevice(prev);
   delete p;
 }
@@ -1128,28 +1204,24 @@ int dgb_assemble_rows(dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_pro
       cuda_check(cudaMemsetAsync(out->row_ptr, 0, sizeof(int32_t), s), "cudaMemsetAsync");
       return;
     }
-    // pattern: counts -> inclusive scan into row_ptr[1..E]
-    dgb::count_blocks_kernel<<<(E + 255) / 256, 256, 0, s>>>(
-        mesh->edge_kind, mesh->element_edges, row_begin, E, out->row_ptr, plan->d_err);
-    cuda_check(cudaGetLastError(), "count_blocks_kernel");
-    if (plan->scan_n != E) {
-      size_t bytes = 0;
-      cub::DeviceScan::InclusiveSum(nullptr, bytes, out->row_ptr + 1, out->row_ptr + 1, E, s);
-      if (bytes > plan->scan_bytes) {
-        cudaFree(plan->d_scan);
-        plan->d_scan = nullptr;
-        cuda_check(cudaMalloc(&plan->d_scan, bytes), "cudaMalloc(scan)");
-        plan->scan_bytes = bytes;
-      }
-      plan->scan_n = E;
+    ++plan->epoch;
+    const bool bound = plan->d_pattern && plan->bound_ee == mesh->element_edges &&
+                       plan->bound_kind == mesh->edge_kind && plan->bound_n == mesh->n_elements &&
+                       plan->bound_begin == row_begin && plan->bound_end == row_end;
+    const int32_t* src = nullptr;
+    plan->last_launches = 1;
+    if (bound) {
+      src = plan->d_pattern;
+    } else {
+      compute_pattern(plan, mesh, row_begin, row_end, out->row_ptr, s);
+      plan->last_launches += 3;
     }
-    size_t bytes = plan->scan_bytes;
-    cuda_check(cub::DeviceScan::InclusiveSum(plan->d_scan, bytes, out->row_ptr + 1,
-                                             out->row_ptr + 1, E, s),
-               "DeviceScan");
-
     if (plan->ev_start) cuda_check(cudaEventRecord(plan->ev_start, s), "cudaEventRecord");
-    if (!try_launch_v2(plan, mesh, problem, params, out, rhs, s, row_begin, row_end)) {
+    if (!try_launch_v2(plan, mesh, problem, params, out, rhs, s, row_begin, row_end, src)) {
+      if (src) {
+        cuda_check(cudaMemcpyAsync(out->row_ptr, src, sizeof(int32_t) * (E + 1),
+                                   cudaMemcpyDeviceToDevice, s), "cudaMemcpyAsync(pattern)");
+      }
       dgb::KParams P;
       std::memset(&P, 0, sizeof P);
       P.nodes = mesh->nodes;
@@ -1177,6 +1249,7 @@ int dgb_assemble_rows(dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_pro
       P.val = out->val;
       P.rhs = rhs;
       P.err_edge = plan->d_err;
+      P.epoch = plan->epoch & 0xFFFFFFFFull;
       const int n_tiles = (E + P.tile - 1) / P.tile;
       const size_t smem =
           static_cast<size_t>(P.tile) * (plan->R.size + dgb::kGeo) * sizeof(double) +
@@ -1191,8 +1264,6 @@ int dgb_assemble_rows(dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_pro
     }
     cuda_check(cudaGetLastError(), "assemble_kernel");
     if (plan->ev_stop) cuda_check(cudaEventRecord(plan->ev_stop, s), "cudaEventRecord");
-    cuda_check(cudaMemcpyAsync(plan->h_err, plan->d_err, sizeof(int32_t), cudaMemcpyDeviceToHost, s),
-               "cudaMemcpyAsync(err)");
   });
 }
 
@@ -1234,18 +1305,18 @@ int dgb_plan_set_option(dgb_plan* plan, int32_t option, int32_t value) {
   }
 }
 
-// count_blocks_kernel + cub scan (init + scan kernels) + assemble_kernel
-int32_t dgb_assemble_launch_count(void) { return 4; }
 
 int dgb_plan_status(dgb_plan* plan, void* stream) {
   return dgb::guarded([&] {
     if (!plan) throw dgb::Error(DGB_STATUS_INVALID_ARGUMENT, "null plan");
     DeviceGuard guard(plan->device);
     cuda_check(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)), "cudaStreamSynchronize");
-    if (*plan->h_err != INT_MAX) {
+    unsigned long long w = 0;
+    cuda_check(cudaMemcpy(&w, plan->d_err, sizeof w, cudaMemcpyDeviceToHost), "cudaMemcpy(err)");
+    if ((w >> 32) == (plan->epoch & 0xFFFFFFFFull) && plan->epoch != 0) {
       throw dgb::Error(DGB_STATUS_INFLOW_ON_NEUMANN,
                        "inflow across a Neumann edge: no boundary data to upwind from",
-                       *plan->h_err);
+                       static_cast<long long>(0xFFFFFFFFull - (w & 0xFFFFFFFFull)));
     }
   });
 }

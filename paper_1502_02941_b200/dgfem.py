@@ -265,6 +265,17 @@ class Plan:
     def set_option(self, option: int, value: int) -> None:
         _check(self._lib.dgb_plan_set_option(self._h, option, value))
 
+    def bind_mesh(self, dmesh: "DeviceMesh", row_begin: int = 0, row_end: int | None = None,
+                  stream=None) -> None:
+        """dgb_plan_bind_mesh: compute the BSR pattern once for this mesh / row range."""
+        import torch
+        if stream is None:
+            stream = torch.cuda.current_stream(self.device)
+        h = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+        end = dmesh.n_elements if row_end is None else row_end
+        _check(self._lib.dgb_plan_bind_mesh(self._h, C.byref(dmesh.view), row_begin, end,
+                                            C.c_void_p(h)))
+
     def set_generic(self, on: bool = True) -> None:
         """Force the generic block-row kernel (testing)."""
         _check(self._lib.dgb_plan_set_option(self._h, capi.OPTION_FORCE_GENERIC_KERNEL, int(on)))

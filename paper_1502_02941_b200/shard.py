@@ -56,8 +56,10 @@ def global_error_edge(local_edge: int, group=None) -> int:
 class ShardAssembler:
     """GPU assembly of one rank's block rows (full mesh replicated in HBM, ~46 B/element)."""
 
-    def __init__(self, mesh, ref, problem, device: int, begin: int, end: int, share=None):
-        """share: another ShardAssembler whose plan and device copies to reuse."""
+    def __init__(self, mesh, ref, problem, device: int, begin: int, end: int, share=None,
+                 bind: bool = False):
+        """share: another ShardAssembler whose plan and device copies to reuse; bind: compute
+        the shard's BSR pattern once (dgb_plan_bind_mesh), one kernel per assembly after."""
         from . import dgfem
         self.begin, self.end = begin, end
         if share is not None:
@@ -67,6 +69,8 @@ class ShardAssembler:
             self.dmesh = dgfem.DeviceMesh(mesh, device)
             self.dprob = dgfem.DeviceProblem(problem, device)
         self.n_blocks = block_count(mesh.view, begin, end)
+        if bind:
+            self.plan.bind_mesh(self.dmesh, begin, end)
         import torch
         dev = torch.device("cuda", device)
         nl = ref.n_local

@@ -227,3 +227,37 @@ def test_config1_solve_error(oracle):
     e_orc = l2_error(*oracle.assemble(mesh.arrays(), t, spec.c, params))
     assert e_gpu < 5e-3
     assert abs(e_gpu - e_orc) <= 1e-9 * e_orc
+
+
+def test_bound_pattern_single_kernel_matches_unbound():
+    """dgb_plan_bind_mesh: the one-kernel path equals the count+scan path bitwise, for the full
+    mesh and for a shard; unbinding falls back."""
+    import torch
+    cfg = problems.CONFIGS[2]
+    mesh = dgfem.unit_square_mesh(40, 0.1, 3, True, 4, 0)
+    ref = dgfem.ReferenceElement(cfg.degree, cfg.quad_order)
+    spec = problems.config_problem(2)
+    params = dgfem.config_parameters(cfg, capi.IIPG)
+    plan = dgfem.Plan(ref.view)
+    dm, dp = dgfem.DeviceMesh(mesh), dgfem.DeviceProblem(spec)
+    a = plan.assemble(dm, dp, params, plan.allocate(dm))
+    assert capi.load().dgb_plan_launch_count(plan._h) == 4
+    plan.bind_mesh(dm)
+    b = plan.allocate(dm)
+    b.row_ptr.fill_(-7)
+    plan.assemble(dm, dp, params, b)
+    assert capi.load().dgb_plan_launch_count(plan._h) == 1
+    torch.cuda.synchronize()
+    for x, y in zip((a.row_ptr, a.col, a.val, a.rhs), (b.row_ptr, b.col, b.val, b.rhs)):
+        assert torch.equal(x, y)
+    # shard with its own bound pattern
+    lo, hi = shard.row_range(mesh.n_elements, 1, 3)
+    sa = shard.ShardAssembler(mesh, ref, spec, 0, lo, hi, bind=True)
+    out = sa.assemble(params)
+    full = to_np(a)
+    part = to_np(out)
+    np.testing.assert_array_equal(part[0], full[0][lo:hi + 1] - full[0][lo])
+    np.testing.assert_array_equal(part[2], full[2][full[0][lo]:full[0][hi]])
+    capi.load().dgb_plan_unbind_mesh(plan._h)
+    plan.assemble(dm, dp, params, b)
+    assert capi.load().dgb_plan_launch_count(plan._h) == 4
