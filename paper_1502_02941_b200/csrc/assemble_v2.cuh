@@ -78,6 +78,33 @@ struct Stage {
   static constexpr int kStride = (N2 % 2 == 0) ? N2 + 2 : N2 + 1;
 };
 
+// Bulk asynchronous shared -> global copies (the TMA engine; SASS UBLKCP).  Each lane hands
+// its own contiguous staged block to the copy engine and later waits only on its own group.
+__device__ __forceinline__ unsigned smem_addr(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void bulk_store(void* g, const void* sm, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n"
+               :: "l"(g), "r"(smem_addr(sm)), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+}
+__device__ __forceinline__ void fence_smem_to_async() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+
+// Writes this lane's staged block (N2 doubles at `st`) to val[base ..] (base < 0: none).
+// Even N2: one bulk copy per lane (block starts are 16-byte aligned: N2 * 8 % 16 == 0);
+// odd N2: the warp-cooperative flush below.
+template <int N2>
+__device__ __forceinline__ void write_block(const double* stw, const double* st, long long base,
+                                            double* val, int lane);
+
 // Warp-cooperative write of one staged block kind: lane L's block (if base_L >= 0) goes to
 // val[base_L .. base_L + N2).  Even N2: 16-byte moves (block starts are 16-byte aligned since
 // N2 * 8 is a multiple of 16); odd N2: 8-byte moves.
@@ -127,6 +154,17 @@ __device__ __forceinline__ void flush_blocks(const double* st, long long base, d
 }
 
 // Per-warp shared-memory layout of the block-row kernel (doubles).
+template <int N2>
+__device__ __forceinline__ void write_block(const double* stw, const double* st, long long base,
+                                            double* val, int lane) {
+  if constexpr (N2 % 2 == 0) {
+    fence_smem_to_async();
+    if (base >= 0) bulk_store(val + base, st, N2 * sizeof(double));
+  } else {
+    flush_blocks<N2>(stw, base, val, lane);
+  }
+}
+
 template <int NL, int NQV, int NQE, int BK>
 struct Smem {
   static constexpr int N2 = NL * NL;
@@ -136,7 +174,8 @@ struct Smem {
   static constexpr int kStash = 3 * NF * 32;
   static constexpr int kMeta = 3 * 32 / 2;                     // 3 ints per lane
   static constexpr int kTrig = BK == 2 ? 2 * NQV * 32 : 0;     // pointwise transport weights
-  static constexpr int kWarp = kStage + kStash + kMeta + kTrig;
+  static constexpr int kRhs = (32 * NL + 1) & ~1;               // packed RHS slice of the warp
+  static constexpr int kWarp = kStage + kStash + kMeta + kTrig + kRhs;
   static constexpr int kTr = (3 * NQE * 3 * NL + 1) & ~1;      // trace table (per CTA)
 };
 
@@ -165,6 +204,7 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
   double* sk = stw + SM::kStage;                     // stash [NF][3][32]
   int* mk = reinterpret_cast<int*>(sk + SM::kStash); // meta [3][32]: kind | lf << 2 | slot << 4
   double* sq = sk + SM::kStash + SM::kMeta;          // TRIG: [NQV][2][32]
+  double* srhs = sq + SM::kTrig;                     // [32][NL] packed RHS
   auto K = [&](int f, int l) -> double& { return sk[(f * 3 + l) * 32 + lane]; };
 
   const int e = P.row_begin + blockIdx.x * blockDim.x + threadIdx.x;
@@ -375,18 +415,20 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
     }
   }
 
-  // ---- RHS: the warp's contiguous slice, staged and written coalesced ------------------------
+  // ---- RHS: the warp's contiguous slice, packed in shared memory and written in one go ------
   {
 #pragma unroll
-    for (int i = 0; i < NL; ++i) st[i] = F[i];
+    for (int i = 0; i < NL; ++i) srhs[lane * NL + i] = F[i];
     __syncwarp();
     const int e_first = blockIdx.x * blockDim.x + warp * 32;  // relative to row_begin
     const int n_here = min(32, P.row_end - P.row_begin - e_first);
-    for (int idx = lane; idx < n_here * NL; idx += 32) {
-      const int Ln = idx / NL, i = idx - Ln * NL;
-      P.rhs[static_cast<long long>(e_first) * NL + idx] = stw[Ln * SS + i];
+    double* dst = P.rhs + static_cast<long long>(e_first) * NL;
+    const int bulk = (n_here * NL) & ~1;  // 16-byte multiple (warp slices start 16-B aligned)
+    if (lane == 0 && bulk > 0) {
+      fence_smem_to_async();
+      bulk_store(dst, srhs, bulk * sizeof(double));
     }
-    __syncwarp();
+    for (int idx = bulk + lane; idx < n_here * NL; idx += 32) dst[idx] = srhs[idx];
   }
 
   // ---- diagonal block ----------------------------------------------------------------------
@@ -502,8 +544,8 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
         for (int j = 0; j < NL; ++j) st[(i0 + r) * NL + j] = acc[r][j];
       }
     }
-    flush_blocks<N2>(stw, active ? static_cast<long long>(rp + diag_slot) * N2 : -1LL, P.val,
-                     lane);
+    write_block<N2>(stw, st, active ? static_cast<long long>(rp + diag_slot) * N2 : -1LL, P.val,
+                    lane);
   }
 
   // ---- neighbour blocks: K_ef = sum_p phi^l_p (x) b1_p + a2_p (x) phi^lf_(n-1-p) ---------------
@@ -524,6 +566,7 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
       }
     }
     const double* trm = tr + lf * (NQE * 3 * NL);
+    if constexpr (N2 % 2 == 0) bulk_wait_read();  // previous block copy has left the staging
     constexpr int CJ = NL <= 6 ? NL : 2;  // columns per register chunk
 #pragma unroll 1
     for (int j0 = 0; j0 < NL; j0 += CJ) {
@@ -556,9 +599,11 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
         for (int c = 0; c < CJ; ++c) st[i * NL + j0 + c] = acc[c];
       }
     }
-    flush_blocks<N2>(stw, (active && has) ? static_cast<long long>(rp + slot) * N2 : -1LL,
-                     P.val, lane);
+    write_block<N2>(stw, st, (active && has) ? static_cast<long long>(rp + slot) * N2 : -1LL,
+                    P.val, lane);
   }
+  if constexpr (N2 % 2 == 0) bulk_wait_all();  // shared memory must outlive the copies
+  if (lane == 0) bulk_wait_all();
 }
 
 }  // namespace v2
