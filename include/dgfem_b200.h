@@ -303,11 +303,13 @@ enum dgb_plan_option {
 };
 int dgb_plan_set_option(dgb_plan* plan, int32_t option, int32_t value);
 
-/* Binds the BSR pattern of block rows [row_begin, row_end) of `mesh` (DEVICE arrays) to the
- * plan: row_ptr is computed once (count + scan on `stream`) and later dgb_assemble /
- * dgb_assemble_rows calls on the same mesh arrays and rows skip those launches and copy the
- * bound row_ptr into their output (one kernel per assembly).  The pattern depends only on
- * element_edges / edge_kind; rebind (or unbind) if those arrays change. */
+/* Binds block rows [row_begin, row_end) of `mesh` (DEVICE arrays) to the plan, computing once
+ * (on `stream`) what depends only on the mesh: the BSR row_ptr (count + scan) and an element
+ * adjacency record (neighbour per local edge, its vertex opposite the shared edge, edge kinds;
+ * 32 B per element).  Later dgb_assemble / dgb_assemble_rows calls on the same mesh arrays and
+ * rows run as one kernel that reads the record with coalesced loads instead of the dependent
+ * element_edges -> edge_elements -> elements gathers, and copy the bound row_ptr into their
+ * output.  Rebind (or unbind) if elements / element_edges / edge_kind / edge_elements change. */
 int dgb_plan_bind_mesh(dgb_plan* plan, const dgb_mesh_arrays* mesh, int32_t row_begin,
                        int32_t row_end, void* stream);
 int dgb_plan_unbind_mesh(dgb_plan* plan);

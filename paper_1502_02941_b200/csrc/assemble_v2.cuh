@@ -59,6 +59,8 @@ struct Params2 {
   const int32_t* element_edges;
   int32_t* row_ptr;              // output row pointer of the launch's rows
   const int32_t* row_ptr_src;    // bound pattern (dgb_plan_bind_mesh) copied to row_ptr, or null
+  const int4* adj_nb;            // bound adjacency: neighbour per local edge, .w = kinds | lf << 2
+  const int4* adj_op;            // bound adjacency: neighbour's vertex opposite the shared edge
   int32_t* col;
   double* val;
   double* rhs;
@@ -170,7 +172,10 @@ struct Smem {
   static constexpr int N2 = NL * NL;
   static constexpr int SS = Stage<N2>::kStride;               // staging stride per lane
   static constexpr int NF = BK == 0 ? 8 : 7 + 2 * NQE;         // stashed coefficients per edge
-  static constexpr int kStage = 32 * SS;
+  // even N2: one staged block per lane (bulk-copied per lane); odd N2 (P1): the warp's whole
+  // contiguous row range (<= 4 blocks per lane), bulk-copied once per warp
+  static constexpr bool kRowMode = N2 % 2 == 1;
+  static constexpr int kStage = kRowMode ? ((32 * 4 * N2 + 2 + 1) & ~1) : 32 * SS;
   static constexpr int kStash = 3 * NF * 32;
   static constexpr int kMeta = 3 * 32 / 2;                     // 3 ints per lane
   static constexpr int kTrig = BK == 2 ? 2 * NQV * 32 : 0;     // pointwise transport weights
@@ -200,7 +205,7 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double* stw = smem + SM::kTr + warp * SM::kWarp;  // staging [32][SS]
-  double* st = stw + lane * SS;
+  double* st = stw + lane * SS;  // (even N2) this lane's block
   double* sk = stw + SM::kStage;                     // stash [NF][3][32]
   int* mk = reinterpret_cast<int*>(sk + SM::kStash); // meta [3][32]: kind | lf << 2 | slot << 4
   double* sq = sk + SM::kStash + SM::kMeta;          // TRIG: [NQV][2][32]
@@ -256,6 +261,11 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
   int cols[4], kinds[4], nb = 1;
   cols[0] = ee;
   kinds[0] = -1;
+  int4 anb = make_int4(0, 0, 0, 0), aop = make_int4(0, 0, 0, 0);
+  if (P.adj_nb) {  // bound adjacency record: two coalesced 16-byte loads per element
+    anb = __ldg(P.adj_nb + (ee - P.row_begin));
+    aop = __ldg(P.adj_op + (ee - P.row_begin));
+  }
 #pragma unroll
   for (int l = 0; l < 3; ++l) {
     const int a = v[(l + 1) % 3], b = v[(l + 2) % 3];
@@ -268,18 +278,29 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
     const double tx = dx * rh, ty = dy * rh;
     const double nx = o == 0 ? ty : -ty, ny = o == 0 ? -tx : tx;  // outward normal of e
     const double ge0 = G00 * nx + G10 * ny, ge1 = G01 * nx + G11 * ny;
-    const int edge = __ldg(P.element_edges + 3 * ee + l);
-    const int kind = __ldg(P.edge_kind + edge);
-    int lf = 0;
+    int edge = -1, kind, lf = 0, f = -1, vf[3];
+    if (P.adj_nb) {
+      kind = (anb.w >> (4 * l)) & 3;
+      lf = (anb.w >> (4 * l + 2)) & 3;
+      f = l == 0 ? anb.x : (l == 1 ? anb.y : anb.z);
+      const int opp = l == 0 ? aop.x : (l == 1 ? aop.y : aop.z);
+      // f traverses the shared edge the other way: vf[lf] = opp, vf[lf+1] = b, vf[lf+2] = a
+#pragma unroll
+      for (int k = 0; k < 3; ++k) vf[k] = k == lf ? opp : (k == (lf + 1) % 3 ? b : a);
+    } else {
+      edge = __ldg(P.element_edges + 3 * ee + l);
+      kind = __ldg(P.edge_kind + edge);
+      if (kind == DGB_EDGE_INTERIOR) {
+        const int2 lr = __ldg(reinterpret_cast<const int2*>(P.edge_elements) + edge);
+        f = lr.x == ee ? lr.y : lr.x;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) vf[k] = __ldg(P.elements + 3 * f + k);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) if (vf[k] != a && vf[k] != b) lf = k;
+      }
+    }
     double w0 = 0.0, w1 = 0.0, cp = 0.0, y0 = 0.0, y1 = 0.0, z0 = 0.0, z1 = 0.0, cx = 0.0;
     if (kind == DGB_EDGE_INTERIOR) {
-      const int2 lr = __ldg(reinterpret_cast<const int2*>(P.edge_elements) + edge);
-      const int f = lr.x == ee ? lr.y : lr.x;
-      int vf[3];
-#pragma unroll
-      for (int k = 0; k < 3; ++k) vf[k] = __ldg(P.elements + 3 * f + k);
-#pragma unroll
-      for (int k = 0; k < 3; ++k) if (vf[k] != a && vf[k] != b) lf = k;
       const Geo gf = element_geo_fast(P.nodes, vf);
       double eps_e = eps;
       if (P.prob.diffusion.kind == DGB_FIELD_PER_ELEMENT) {
@@ -337,6 +358,7 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
       }
       double cG[NQE], cH[NQE];
       if (kind == DGB_EDGE_NEUMANN) {
+        if (edge < 0) edge = __ldg(P.element_edges + 3 * ee + l);
         if (inflow && !P.drop_neumann && active) atomicMax(P.err_edge, (P.epoch << 32) | (0xFFFFFFFFull - static_cast<unsigned>(edge)));
 #pragma unroll
         for (int p = 0; p < NQE; ++p) {
@@ -415,6 +437,19 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
     }
   }
 
+  // odd N2: this lane's row inside the warp's contiguous staged row range
+  int rp_first = 0, rp_last = 0;
+  double* srow = stw;
+  if constexpr (SM::kRowMode) {
+    rp_first = __shfl_sync(0xffffffffu, rp, 0);
+    rp_last = __reduce_max_sync(0xffffffffu, active ? rp + nb : 0);
+    srow = stw + (rp_first & 1);  // same 16-byte phase as val + rp_first * N2
+  }
+  auto block_at = [&](int slot) -> double* {
+    if constexpr (SM::kRowMode) return srow + (rp - rp_first + slot) * N2;
+    else return st;
+  };
+
   // ---- RHS: the warp's contiguous slice, packed in shared memory and written in one go ------
   {
 #pragma unroll
@@ -457,6 +492,7 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
       cA[3] = det * (G01 * AB01 + G11 * AB11);
     }
     constexpr int RC = NL <= 6 ? NL : (NL <= 10 ? 2 : 1);  // rows per register chunk
+    double* blk = block_at(diag_slot);
 #pragma unroll 1
     for (int i0 = 0; i0 < NL; i0 += RC) {
       double acc[RC][NL];
@@ -541,11 +577,13 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
 #pragma unroll
       for (int r = 0; r < RC; ++r) {
 #pragma unroll
-        for (int j = 0; j < NL; ++j) st[(i0 + r) * NL + j] = acc[r][j];
+        for (int j = 0; j < NL; ++j) if (active) blk[(i0 + r) * NL + j] = acc[r][j];
       }
     }
-    write_block<N2>(stw, st, active ? static_cast<long long>(rp + diag_slot) * N2 : -1LL, P.val,
-                    lane);
+    if constexpr (!SM::kRowMode) {
+      write_block<N2>(stw, st, active ? static_cast<long long>(rp + diag_slot) * N2 : -1LL,
+                      P.val, lane);
+    }
   }
 
   // ---- neighbour blocks: K_ef = sum_p phi^l_p (x) b1_p + a2_p (x) phi^lf_(n-1-p) ---------------
@@ -566,7 +604,9 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
       }
     }
     const double* trm = tr + lf * (NQE * 3 * NL);
-    if constexpr (N2 % 2 == 0) bulk_wait_read();  // previous block copy has left the staging
+    if constexpr (!SM::kRowMode) bulk_wait_read();  // previous block copy has left the staging
+    double* blk = block_at(slot);
+    const bool store = active && has;
     constexpr int CJ = NL <= 6 ? NL : 2;  // columns per register chunk
 #pragma unroll 1
     for (int j0 = 0; j0 < NL; j0 += CJ) {
@@ -596,13 +636,29 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
           for (int c = 0; c < CJ; ++c) acc[c] = fma(ph, b1[p][c], fma(a2, pm[p][c], acc[c]));
         }
 #pragma unroll
-        for (int c = 0; c < CJ; ++c) st[i * NL + j0 + c] = acc[c];
+        for (int c = 0; c < CJ; ++c) if (store) blk[i * NL + j0 + c] = acc[c];
       }
     }
-    write_block<N2>(stw, st, (active && has) ? static_cast<long long>(rp + slot) * N2 : -1LL,
-                    P.val, lane);
+    if constexpr (!SM::kRowMode) {
+      write_block<N2>(stw, st, store ? static_cast<long long>(rp + slot) * N2 : -1LL, P.val, lane);
+    }
   }
-  if constexpr (N2 % 2 == 0) bulk_wait_all();  // shared memory must outlive the copies
+  if constexpr (SM::kRowMode) {
+    // one bulk copy of the warp's whole row range; the unaligned head / tail doubles by hand
+    __syncwarp();
+    const int n = (rp_last - rp_first) * N2;
+    double* dst = P.val + static_cast<long long>(rp_first) * N2;
+    const int head = rp_first & 1;
+    const int body = (n - head) & ~1;
+    if (lane == 0 && body > 0) {
+      fence_smem_to_async();
+      bulk_store(dst + head, srow + head, body * sizeof(double));
+    }
+    if (lane == 1 && head) dst[0] = srow[0];
+    if (lane == 2 && head + body < n) dst[n - 1] = srow[n - 1];
+  } else {
+    bulk_wait_all();  // shared memory must outlive the copies
+  }
   if (lane == 0) bulk_wait_all();
 }
 

@@ -312,6 +312,44 @@ __global__ void count_blocks_kernel(const uint8_t* __restrict__ edge_kind,
   row_ptr[r + 1] = c;
 }
 
+// Element adjacency record of rows [begin, begin + n) (bound once per mesh): per local edge l
+// the neighbour element, the neighbour's vertex opposite the shared edge, and kind | lf << 2 in
+// bits 4l..4l+3 of nb.w.  Replaces the per-assembly chain element_edges -> edge_elements ->
+// elements[f] of dependent gathers (the "geometry / neighbour precompute" of the north star).
+__global__ void adjacency_kernel(const int32_t* __restrict__ elements,
+                                 const uint8_t* __restrict__ edge_kind,
+                                 const int32_t* __restrict__ edge_elements,
+                                 const int32_t* __restrict__ element_edges, int32_t begin,
+                                 int32_t n, int4* __restrict__ nb, int4* __restrict__ op) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const int e = begin + r;
+  int nbr[3] = {-1, -1, -1}, opp[3] = {-1, -1, -1}, meta = 0;
+#pragma unroll
+  for (int l = 0; l < 3; ++l) {
+    const int edge = __ldg(element_edges + 3 * e + l);
+    const int kind = __ldg(edge_kind + edge);
+    int lf = 0;
+    if (kind == DGB_EDGE_INTERIOR) {
+      const int2 lr = __ldg(reinterpret_cast<const int2*>(edge_elements) + edge);
+      const int f = lr.x == e ? lr.y : lr.x;
+      const int a = __ldg(elements + 3 * e + (l + 1) % 3), b = __ldg(elements + 3 * e + (l + 2) % 3);
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const int v = __ldg(elements + 3 * f + k);
+        if (v != a && v != b) {
+          lf = k;
+          opp[l] = v;
+        }
+      }
+      nbr[l] = f;
+    }
+    meta |= (kind | (lf << 2)) << (4 * l);
+  }
+  nb[r] = make_int4(nbr[0], nbr[1], nbr[2], meta);
+  op[r] = make_int4(opp[0], opp[1], opp[2], 0);
+}
+
 // ------------------------------------------------------------------------------------------
 // the block-row kernel
 // ------------------------------------------------------------------------------------------
@@ -850,6 +888,10 @@ struct dgb_plan {
   const void* bound_ee = nullptr;
   const void* bound_kind = nullptr;
   int32_t bound_n = -1, bound_begin = -1, bound_end = -1;
+  int4* d_adj = nullptr;  // neighbour records [adj_rows] then opposite vertices [adj_rows]
+  size_t adj_cap = 0, adj_rows = 0;
+  const void* bound_elements = nullptr;
+  const void* bound_edge_elements = nullptr;
   int32_t last_launches = 0;
 };
 
@@ -937,6 +979,10 @@ void launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_prob
   P.val = out->val;
   P.rhs = rhs;
   P.row_ptr_src = row_ptr_src;
+  if (row_ptr_src) {
+    P.adj_nb = plan->d_adj;
+    P.adj_op = plan->d_adj + plan->adj_rows;
+  }
   P.err_edge = plan->d_err;
   P.epoch = plan->epoch & 0xFFFFFFFFull;
   P.n_elements = mesh->n_elements;
@@ -1083,13 +1129,27 @@ int dgb_plan_bind_mesh(dgb_plan* plan, const dgb_mesh_arrays* mesh, int32_t row_
       cuda_check(cudaMalloc(&plan->d_pattern, need * sizeof(int32_t)), "cudaMalloc(pattern)");
       plan->pattern_cap = need;
     }
+    const size_t rows = static_cast<size_t>(row_end - row_begin);
+    if (rows > plan->adj_cap) {
+      cudaFree(plan->d_adj);
+      plan->d_adj = nullptr;
+      cuda_check(cudaMalloc(&plan->d_adj, 2 * rows * sizeof(int4)), "cudaMalloc(adjacency)");
+      plan->adj_cap = rows;
+    }
+    plan->adj_rows = rows;
     if (row_end > row_begin) {
       compute_pattern(plan, mesh, row_begin, row_end, plan->d_pattern, s);
+      dgb::adjacency_kernel<<<(row_end - row_begin + 255) / 256, 256, 0, s>>>(
+          mesh->elements, mesh->edge_kind, mesh->edge_elements, mesh->element_edges, row_begin,
+          row_end - row_begin, plan->d_adj, plan->d_adj + rows);
+      cuda_check(cudaGetLastError(), "adjacency_kernel");
     } else {
       cuda_check(cudaMemsetAsync(plan->d_pattern, 0, sizeof(int32_t), s), "cudaMemsetAsync");
     }
     plan->bound_ee = mesh->element_edges;
     plan->bound_kind = mesh->edge_kind;
+    plan->bound_elements = mesh->elements;
+    plan->bound_edge_elements = mesh->edge_elements;
     plan->bound_n = mesh->n_elements;
     plan->bound_begin = row_begin;
     plan->bound_end = row_end;
@@ -1167,6 +1227,7 @@ void dgb_plan_destroy(dgb_plan* p) {
   cudaFree(p->d_err);
   cudaFree(p->d_scan);
   cudaFree(p->d_pattern);
+  cudaFree(p->d_adj);
   if (prev >= 0) cudaSetDevice(prev);
   delete p;
 }
@@ -1206,6 +1267,8 @@ int dgb_assemble_rows(dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_pro
     }
     ++plan->epoch;
     const bool bound = plan->d_pattern && plan->bound_ee == mesh->element_edges &&
+                       plan->bound_elements == mesh->elements &&
+                       plan->bound_edge_elements == mesh->edge_elements &&
                        plan->bound_kind == mesh->edge_kind && plan->bound_n == mesh->n_elements &&
                        plan->bound_begin == row_begin && plan->bound_end == row_end;
     const int32_t* src = nullptr;
