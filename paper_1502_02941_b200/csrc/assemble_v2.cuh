@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
       const double px = FADD(FADD(pv[0].x, FMUL(B00, P.t.x[L::VX + q])), FMUL(B01, P.t.x[L::VY + q]));
       const double py = FADD(FADD(pv[0].y, FMUL(B10, P.t.x[L::VX + q])), FMUL(B11, P.t.x[L::VY + q]));
       const double f = fs.kind == DGB_FIELD_PER_ELEMENT ? __ldg(fs.per_element + ee)
-                                                        : scalar_point(fs, px, py);
+                                                        : scalar_point_inline(fs, px, py);
       const double dw = det * P.t.x[L::VW + q];
       const double c = dw * f;
 #pragma unroll
@@ -516,7 +516,7 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
           acc[r][j] = x;
         }
       }
-#pragma unroll 1
+#pragma unroll(NL <= 6 ? 3 : 1)
       for (int l = 0; l < 3; ++l) {
         const double w0 = K(F_W0, l), w1 = K(F_W1, l);
 #pragma unroll
@@ -587,7 +587,7 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
   }
 
   // ---- neighbour blocks: K_ef = sum_p phi^l_p (x) b1_p + a2_p (x) phi^lf_(n-1-p) ---------------
-#pragma unroll 1
+#pragma unroll(NL <= 6 ? 3 : 1)  // small blocks: compile-time l (LDCU.128 immediates)
   for (int l = 0; l < 3; ++l) {
     const int meta = mk[l * 32 + lane];
     const bool has = (meta & 3) == DGB_EDGE_INTERIOR;

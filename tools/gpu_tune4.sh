@@ -1,0 +1,9 @@
+#!/bin/bash
+cd "$(dirname "$0")/.."
+mkdir -p gpurun_out
+for c in 2 3 4; do
+  python bench.py --config $c --steps 10 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/tune_c${c}.json 2>&1
+  python bench.py --config $c --steps 10 --warmup 3 --no-e2e --no-cpu-baseline --no-bind > gpurun_out/tune_c${c}_nobind.json 2>&1
+done
+for f in gpurun_out/tune_c*.json; do python -c "
+import json; d=json.load(open('$f')); r=d['roofline']; print('$f', round(d['value']/1e6,1), 'Mel/s', r['kernel_ms'], 'ms', r['achieved'], 'GB/s', r['frac'])" 2>/dev/null || (echo $f; tail -3 $f); done
