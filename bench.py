@@ -43,6 +43,9 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--minblocks", type=int, default=0, help="tuning knob (P2 kernel CTAs/SM)")
+    ap.add_argument("--l2-policy", type=int, default=-1,
+                    help="plan L2 policy bits (1: persist nodes, 2: evict-first output); "
+                         "-1: the default for the config")
     ap.add_argument("--no-bind", action="store_true",
                     help="recompute the BSR pattern in every assembly (count + scan launches)")
     return ap.parse_args()
@@ -205,7 +208,11 @@ def run_ours(args, world, rank, local):
     spec = problems.config_problem(args.config, mesh.n_elements)
     params = [dgfem.config_parameters(cfg, m) for m in cfg.methods]
     begin, end = shard.row_range(mesh.n_elements, rank, world)
-    shards = [shard.ShardAssembler(mesh, ref, spec, local, begin, end, bind=not args.no_bind)]
+    l2 = args.l2_policy if args.l2_policy >= 0 else (1 if cfg.permute else 2)  # measured
+    shards = [shard.ShardAssembler(mesh, ref, spec, local, begin, end, bind=False)]
+    shards[0].plan.set_option(capi.OPTION_L2_POLICY, l2)
+    if not args.no_bind:
+        shards[0].plan.bind_mesh(shards[0].dmesh, begin, end)
     shards += [shard.ShardAssembler(mesh, ref, spec, local, begin, end, share=shards[0])
                for _ in params[1:]]   # one plan and one device mesh for all methods
     plan = shards[0].plan
@@ -320,6 +327,8 @@ def run_ours(args, world, rank, local):
             "global_mesh": f"{world * cfg.n}x{cfg.n} cells on [0,{world}]x[0,1]" if world > 1 else None,
             "nq_vol": ref.nq_vol, "nq_edge": ref.nq_edge,
             "l2": "flushed between timed steps by a 256 MiB write (outside the timed events)",
+            "l2_policy": {0: "default", 1: "node coordinates persisting in L2",
+                          2: "evict-first output", 3: "persisting nodes + evict-first output"}[l2],
             "pattern": ("recomputed in every assembly (count + scan)" if args.no_bind else
                         "bound once per mesh (dgb_plan_bind_mesh, untimed setup); every assembly "
                         "still writes row_ptr, block columns, values and RHS"),

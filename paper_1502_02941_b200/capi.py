@@ -143,6 +143,7 @@ EXPORTED_SYMBOLS = [
 ]
 OPTION_FORCE_GENERIC_KERNEL = 1
 OPTION_MIN_BLOCKS = 2
+OPTION_L2_POLICY = 3
 
 _lib = None
 

@@ -69,6 +69,7 @@ struct Params2 {
   int32_t n_elements;
   int32_t row_begin, row_end;  // block rows [row_begin, row_end) of this launch (a shard)
   int32_t drop_neumann;
+  int32_t evict_first;           // L2 evict-first hint on the output stream
   double kappa, sigma_i, sigma_b;
   dgb_problem prob;
   Tab<NL, NQV, NQE, TRIG> t;
@@ -85,9 +86,22 @@ struct Stage {
 __device__ __forceinline__ unsigned smem_addr(const void* p) {
   return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
-__device__ __forceinline__ void bulk_store(void* g, const void* sm, unsigned bytes) {
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n"
-               :: "l"(g), "r"(smem_addr(sm)), "r"(bytes) : "memory");
+// L2 policy for the output stream: written once, never re-read by the kernel -> evict first,
+// so the stream does not push the mesh arrays (gathered again by neighbours) out of L2.
+__device__ __forceinline__ unsigned long long evict_first_policy() {
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void bulk_store(void* g, const void* sm, unsigned bytes,
+                                           bool evict_first = false) {
+  if (evict_first) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;\n"
+                 :: "l"(g), "r"(smem_addr(sm)), "r"(bytes), "l"(evict_first_policy()) : "memory");
+  } else {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n"
+                 :: "l"(g), "r"(smem_addr(sm)), "r"(bytes) : "memory");
+  }
   asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
 }
 __device__ __forceinline__ void bulk_wait_read() {
@@ -158,10 +172,10 @@ __device__ __forceinline__ void flush_blocks(const double* st, long long base, d
 // Per-warp shared-memory layout of the block-row kernel (doubles).
 template <int N2>
 __device__ __forceinline__ void write_block(const double* stw, const double* st, long long base,
-                                            double* val, int lane) {
+                                            double* val, int lane, bool ef = false) {
   if constexpr (N2 % 2 == 0) {
     fence_smem_to_async();
-    if (base >= 0) bulk_store(val + base, st, N2 * sizeof(double));
+    if (base >= 0) bulk_store(val + base, st, N2 * sizeof(double), ef);
   } else {
     flush_blocks<N2>(stw, base, val, lane);
   }
@@ -461,7 +475,7 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
     const int bulk = (n_here * NL) & ~1;  // 16-byte multiple (warp slices start 16-B aligned)
     if (lane == 0 && bulk > 0) {
       fence_smem_to_async();
-      bulk_store(dst, srhs, bulk * sizeof(double));
+      bulk_store(dst, srhs, bulk * sizeof(double), P.evict_first);
     }
     for (int idx = bulk + lane; idx < n_here * NL; idx += 32) dst[idx] = srhs[idx];
   }
@@ -582,7 +596,7 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
     }
     if constexpr (!SM::kRowMode) {
       write_block<N2>(stw, st, active ? static_cast<long long>(rp + diag_slot) * N2 : -1LL,
-                      P.val, lane);
+                      P.val, lane, P.evict_first);
     }
   }
 
@@ -640,7 +654,8 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
       }
     }
     if constexpr (!SM::kRowMode) {
-      write_block<N2>(stw, st, store ? static_cast<long long>(rp + slot) * N2 : -1LL, P.val, lane);
+      write_block<N2>(stw, st, store ? static_cast<long long>(rp + slot) * N2 : -1LL, P.val, lane,
+                      P.evict_first);
     }
   }
   if constexpr (SM::kRowMode) {
@@ -652,7 +667,7 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
     const int body = (n - head) & ~1;
     if (lane == 0 && body > 0) {
       fence_smem_to_async();
-      bulk_store(dst + head, srow + head, body * sizeof(double));
+      bulk_store(dst + head, srow + head, body * sizeof(double), P.evict_first);
     }
     if (lane == 1 && head) dst[0] = srow[0];
     if (lane == 2 && head + body < n) dst[n - 1] = srow[n - 1];

@@ -893,6 +893,10 @@ struct dgb_plan {
   const void* bound_elements = nullptr;
   const void* bound_edge_elements = nullptr;
   int32_t last_launches = 0;
+  size_t l2_persist_bytes = 0;  // persisting-L2 carve-out available to the node window
+  size_t l2_window_max = 0;     // cudaDevAttrMaxAccessPolicyWindowSize
+  size_t l2_persist_max = 0;    // cudaDevAttrMaxPersistingL2CacheSize
+  int l2_policy = 0;            // bit 0: persist nodes in L2, bit 1: evict-first output
 };
 
 namespace {
@@ -989,6 +993,7 @@ void launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_prob
   P.row_begin = out_row_begin;
   P.row_end = out_row_end;
   P.drop_neumann = params->neumann_inflow == DGB_INFLOW_DROP;
+  P.evict_first = (plan->l2_policy & 2) != 0;
   P.kappa = params->kappa;
   P.sigma_i = params->sigma_interior;
   P.sigma_b = params->sigma_boundary;
@@ -1033,7 +1038,30 @@ void launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_prob
     configured = true;
   }
   const int grid = (out_row_end - out_row_begin + THREADS - 1) / THREADS;
-  kernel<<<grid, THREADS, smem, s>>>(P);
+  // Keep the node coordinates (gathered by every element and its neighbours, in random order
+  // for permuted meshes) persisting in L2 while the output streams through with evict-first.
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  int nattr = 0;
+  const size_t node_bytes = sizeof(double) * 2 * static_cast<size_t>(mesh->n_nodes);
+  if ((plan->l2_policy & 1) && plan->l2_persist_bytes > 0 && node_bytes > 0) {
+    attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
+    attr[0].val.accessPolicyWindow.base_ptr = const_cast<double*>(mesh->nodes);
+    attr[0].val.accessPolicyWindow.num_bytes = std::min(node_bytes, plan->l2_window_max);
+    attr[0].val.accessPolicyWindow.hitRatio =
+        static_cast<float>(std::min(1.0, double(plan->l2_persist_bytes) /
+                                             double(attr[0].val.accessPolicyWindow.num_bytes)));
+    attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    nattr = 1;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = nattr;
+  cuda_check(cudaLaunchKernelEx(&cfg, kernel, P), "cudaLaunchKernelEx(v2)");
 }
 
 // Specialised element-per-thread kernels by (n_local, nq_vol, nq_edge, velocity kind), with
@@ -1146,6 +1174,28 @@ int dgb_plan_bind_mesh(dgb_plan* plan, const dgb_mesh_arrays* mesh, int32_t row_
     } else {
       cuda_check(cudaMemsetAsync(plan->d_pattern, 0, sizeof(int32_t), s), "cudaMemsetAsync");
     }
+    {
+      // L2 policy: permuted (gather-heavy) meshes keep their nodes persisting in L2; the
+      // carve-out is sized to the node array, never more (it is taken from the write stream).
+      static bool carve_out_is_ours = false;
+      const size_t node_bytes = sizeof(double) * 2 * static_cast<size_t>(mesh->n_nodes);
+      const size_t want = (plan->l2_policy & 1) ? std::min(node_bytes, plan->l2_persist_max) : 0;
+      plan->l2_persist_bytes = 0;
+      if (want == 0 && carve_out_is_ours) {
+        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);
+        carve_out_is_ours = false;
+        cudaGetLastError();
+      }
+      if (want > 0) {
+        carve_out_is_ours = true;
+        size_t cur = 0;
+        cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+        if (cur != want) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
+        cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+        plan->l2_persist_bytes = cur;
+        cudaGetLastError();
+      }
+    }
     plan->bound_ee = mesh->element_edges;
     plan->bound_kind = mesh->edge_kind;
     plan->bound_elements = mesh->elements;
@@ -1209,6 +1259,14 @@ int dgb_plan_create(const dgb_reference_tables* tables, int32_t device, dgb_plan
       cuda_check(cudaMemcpy(p->d_tens, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice),
                  "cudaMemcpy(tensors)");
       cuda_check(cudaMalloc(&p->d_err, sizeof(unsigned long long)), "cudaMalloc(err)");
+      {
+        int max_persist = 0, max_window = 0;
+        cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, device);
+        cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, device);
+        p->l2_persist_max = static_cast<size_t>(max_persist);
+        p->l2_window_max = static_cast<size_t>(max_window);
+        cudaGetLastError();
+      }
       cuda_check(cudaMemset(p->d_err, 0, sizeof(unsigned long long)), "cudaMemset(err)");
     } catch (...) {
       dgb_plan_destroy(p);
@@ -1364,6 +1422,7 @@ int dgb_plan_set_option(dgb_plan* plan, int32_t option, int32_t value) {
   switch (option) {
     case DGB_OPTION_FORCE_GENERIC_KERNEL: plan->force_generic = value; return DGB_OK;
     case DGB_OPTION_MIN_BLOCKS: plan->minblocks = value; return DGB_OK;
+    case DGB_OPTION_L2_POLICY: plan->l2_policy = value; return DGB_OK;
     default: return DGB_STATUS_INVALID_ARGUMENT;
   }
 }
