@@ -61,6 +61,7 @@ struct Params2 {
   const int32_t* row_ptr_src;    // bound pattern (dgb_plan_bind_mesh) copied to row_ptr, or null
   const int4* adj_nb;            // bound adjacency: neighbour per local edge, .w = kinds | lf << 2
   const int4* adj_op;            // bound adjacency: neighbour's vertex opposite the shared edge
+  const double* bfrag;           // DMMA B fragments of the diagonal terms [ks][nt][lane]
   int32_t* col;
   double* val;
   double* rhs;
@@ -196,7 +197,28 @@ struct Smem {
   static constexpr int kRhs = (32 * NL + 1) & ~1;               // packed RHS slice of the warp
   static constexpr int kWarp = kStage + kStash + kMeta + kTrig + kRhs;
   static constexpr int kTr = (3 * NQE * 3 * NL + 1) & ~1;      // trace table (per CTA)
+  // FP64 tensor-core (DMMA m8n8k4) diagonal block for P2 with constant velocity: 15 terms
+  static constexpr bool kMmaDiag = NL == 6 && BK == 0;
+  static constexpr int kTerms = 15;                              // S0 S1 S2 M T0 T1 W[6] P[3]
+  static constexpr int kKS = (kTerms + 3) / 4, kNT = (N2 + 7) / 8;
+  static constexpr int kBt = kMmaDiag ? kKS * kNT * 32 : 0;     // B fragments (global table)
 };
+
+// Offset (doubles) of diagonal term k in the tensor parameter block (MMA path, P2, const b).
+template <typename L>
+__device__ __forceinline__ int diag_term_offset(int k) {
+  constexpr int N2 = L::N2;
+  if (k < 3) return L::S + k * N2;
+  if (k == 3) return L::M;
+  if (k < 6) return L::T + (k - 4) * N2;
+  if (k < 12) return L::W + (k - 6) * N2;
+  return L::P + (k - 12) * N2;
+}
+
+__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+}
 
 // Stash field indices (per edge l, per lane): see the diagonal / neighbour passes.
 enum { F_W0 = 0, F_W1, F_P, F_Y0, F_Y1, F_Z0, F_Z1, F_X, F_U = 7 };
@@ -505,6 +527,50 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
       cA[2] = det * (G01 * AB00 + G11 * AB10);
       cA[3] = det * (G01 * AB01 + G11 * AB11);
     }
+    if constexpr (SM::kMmaDiag) {
+      // D[32 elements x 36 entries] = C[32 x 16 coefficients] . T[16 x 36] on the FP64 tensor
+      // cores: coefficients are transposed through this warp's (still unused) staging area,
+      // results land directly in each element's staging row.
+      constexpr int CS = 4 * SM::kKS + 2;  // coefficient row stride (doubles)
+      double cv[4 * SM::kKS];
+      cv[0] = cD0; cv[1] = cD1; cv[2] = cD2; cv[3] = cR; cv[4] = cC0; cv[5] = cC1;
+#pragma unroll
+      for (int l = 0; l < 3; ++l) {
+        cv[6 + 2 * l] = K(F_W0, l);
+        cv[7 + 2 * l] = K(F_W1, l);
+        cv[12 + l] = K(F_P, l);
+      }
+#pragma unroll
+      for (int k = SM::kTerms; k < 4 * SM::kKS; ++k) cv[k] = 0.0;
+#pragma unroll
+      for (int k = 0; k < 4 * SM::kKS; ++k) stw[lane * CS + k] = cv[k];
+      __syncwarp();
+      const int g = lane >> 2, t = lane & 3;
+      double af[4][SM::kKS];
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+#pragma unroll
+        for (int ks = 0; ks < SM::kKS; ++ks) af[m][ks] = stw[(8 * m + g) * CS + 4 * ks + t];
+      }
+      __syncwarp();
+#pragma unroll
+      for (int nt = 0; nt < SM::kNT; ++nt) {
+        double bf_[SM::kKS];
+#pragma unroll
+        for (int ks = 0; ks < SM::kKS; ++ks) bf_[ks] = __ldg(P.bfrag + (ks * SM::kNT + nt) * 32 + lane);
+        const int n0 = 8 * nt + 2 * t;
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+          for (int ks = 0; ks < SM::kKS; ++ks) dmma_8x8x4(d0, d1, af[m][ks], bf_[ks]);
+          if (n0 < N2) {
+            *reinterpret_cast<double2*>(stw + (8 * m + g) * SS + n0) = make_double2(d0, d1);
+          }
+        }
+      }
+      __syncwarp();
+    } else {
     constexpr int RC = NL <= 6 ? NL : (NL <= 10 ? 2 : 1);  // rows per register chunk
     double* blk = block_at(diag_slot);
 #pragma unroll 1
@@ -594,6 +660,7 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
         for (int j = 0; j < NL; ++j) if (active) blk[(i0 + r) * NL + j] = acc[r][j];
       }
     }
+    }  // register path
     if constexpr (!SM::kRowMode) {
       write_block<N2>(stw, st, active ? static_cast<long long>(rp + diag_slot) * N2 : -1LL,
                       P.val, lane, P.evict_first);

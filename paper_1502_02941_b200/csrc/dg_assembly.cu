@@ -897,6 +897,8 @@ struct dgb_plan {
   size_t l2_window_max = 0;     // cudaDevAttrMaxAccessPolicyWindowSize
   size_t l2_persist_max = 0;    // cudaDevAttrMaxPersistingL2CacheSize
   int l2_policy = 0;            // bit 0: persist nodes in L2, bit 1: evict-first output
+  // DMMA B fragments of the diagonal terms, one table per kappa (W depends on kappa)
+  std::vector<std::pair<double, double*>> bfrag_cache;
 };
 
 namespace {
@@ -1029,6 +1031,38 @@ void launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_prob
   copy(L::ET, V.ET, NQE);
   copy(L::EW, V.EW, NQE);
   const size_t smem = sizeof(double) * (SM::kTr + (THREADS / 32) * SM::kWarp);
+  if constexpr (SM::kMmaDiag) {
+    // B fragments of the diagonal terms in mma.m8n8k4 layout: lane (g, t) of tile (ks, nt)
+    // holds term 4 ks + t at entry 8 nt + g; built once per (plan, kappa) on the host.
+    dgb_plan* mp = const_cast<dgb_plan*>(plan);
+    double* frag = nullptr;
+    for (auto& c : mp->bfrag_cache) {
+      if (c.first == params->kappa) frag = c.second;
+    }
+    if (!frag) {  // first assembly with this kappa: build and upload (stream-ordered) once
+      std::vector<double> hb(SM::kBt, 0.0);
+      for (int i = 0; i < SM::kBt; ++i) {
+        const int ln = i & 31, tile = i >> 5;
+        const int ks = tile / SM::kNT, nt = tile - ks * SM::kNT;
+        const int k = 4 * ks + (ln & 3), n = 8 * nt + (ln >> 2);
+        if (k < SM::kTerms && n < N2) {
+          int off;
+          if (k < 3) off = L::S + k * N2;
+          else if (k == 3) off = L::M;
+          else if (k < 6) off = L::T + (k - 4) * N2;
+          else if (k < 12) off = L::W + (k - 6) * N2;
+          else off = L::P + (k - 12) * N2;
+          hb[i] = x[off + n];
+        }
+      }
+      cuda_check(cudaMalloc(&frag, hb.size() * sizeof(double)), "cudaMalloc(bfrag)");
+      cuda_check(cudaMemcpyAsync(frag, hb.data(), hb.size() * sizeof(double),
+                                 cudaMemcpyHostToDevice, s), "cudaMemcpyAsync(bfrag)");
+      cuda_check(cudaStreamSynchronize(s), "cudaStreamSynchronize(bfrag)");
+      mp->bfrag_cache.emplace_back(params->kappa, frag);
+    }
+    P.bfrag = frag;
+  }
   auto kernel = dgb::v2::assemble_kernel<NL, NQV, NQE, BK, THREADS, MINB>;
   static bool configured = false;
   if (!configured) {
@@ -1286,6 +1320,7 @@ void dgb_plan_destroy(dgb_plan* p) {
   cudaFree(p->d_scan);
   cudaFree(p->d_pattern);
   cudaFree(p->d_adj);
+  for (auto& c : p->bfrag_cache) cudaFree(c.second);
   if (prev >= 0) cudaSetDevice(prev);
   delete p;
 }
