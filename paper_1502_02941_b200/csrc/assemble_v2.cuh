@@ -190,18 +190,23 @@ struct Smem {
   // even N2: one staged block per lane (bulk-copied per lane); odd N2 (P1): the warp's whole
   // contiguous row range (<= 4 blocks per lane), bulk-copied once per warp
   static constexpr bool kRowMode = N2 % 2 == 1;
-  static constexpr int kStage = kRowMode ? ((32 * 4 * N2 + 2 + 1) & ~1) : 32 * SS;
+  // FP64 tensor-core (DMMA m8n8k4) path for P2 with constant velocity: every block (diagonal:
+  // 15 terms; neighbour: 5 terms x 3 possible lf, zero-padded) is one [32 x 16] . [16 x 36]
+  // product whose fragments are stored straight to global -- no block staging at all
+  static constexpr bool kMma = NL == 6 && BK == 0;
+  static constexpr int kTerms = 15;                              // S0 S1 S2 M T0 T1 W[6] P[3]
+  static constexpr int kKS = (kTerms + 3) / 4, kNT = (N2 + 7) / 8;
+  static constexpr int kCT = 36;                                 // coefficient table stride [k][lane]
+  static constexpr int kStage = kMma ? 4 * kKS * kCT
+                                     : (kRowMode ? ((32 * 4 * N2 + 2 + 1) & ~1) : 32 * SS);
   static constexpr int kStash = 3 * NF * 32;
   static constexpr int kMeta = 3 * 32 / 2;                     // 3 ints per lane
   static constexpr int kTrig = BK == 2 ? 2 * NQV * 32 : 0;     // pointwise transport weights
   static constexpr int kRhs = (32 * NL + 1) & ~1;               // packed RHS slice of the warp
   static constexpr int kWarp = kStage + kStash + kMeta + kTrig + kRhs;
   static constexpr int kTr = (3 * NQE * 3 * NL + 1) & ~1;      // trace table (per CTA)
-  // FP64 tensor-core (DMMA m8n8k4) diagonal block for P2 with constant velocity: 15 terms
-  static constexpr bool kMmaDiag = NL == 6 && BK == 0;
-  static constexpr int kTerms = 15;                              // S0 S1 S2 M T0 T1 W[6] P[3]
-  static constexpr int kKS = (kTerms + 3) / 4, kNT = (N2 + 7) / 8;
-  static constexpr int kBt = kMmaDiag ? kKS * kNT * 32 : 0;     // B fragments (global table)
+  static constexpr int kFragTile = kKS * kNT * 32;               // one B operand, fragment order
+  static constexpr int kBt = kMma ? 4 * kFragTile : 0;           // diagonal + neighbour l = 0..2
 };
 
 // Offset (doubles) of diagonal term k in the tensor parameter block (MMA path, P2, const b).
@@ -218,6 +223,57 @@ __device__ __forceinline__ int diag_term_offset(int k) {
 __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ unsigned long long output_policy(bool evict_first) {
+  unsigned long long pol;
+  if (evict_first) {
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
+  } else {
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;\n" : "=l"(pol));
+  }
+  return pol;
+}
+__device__ __forceinline__ void store_pair(double* g, double a, double b, unsigned long long pol) {
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;\n"
+               :: "l"(g), "d"(a), "d"(b), "l"(pol) : "memory");
+}
+
+// One warp-wide block product on the FP64 tensor cores: D[32 elements x N2] = C . B, where
+// C[lane][k] sits in the warp's coefficient table ct[k * kCT + lane] and B is a fragment-ordered
+// table in global memory ([ks][nt][lane], lane (g, t) holding B[4 ks + t][8 nt + g]).  Lane
+// (g, t) ends up with D[8 m + g][8 nt + 2 t .. +1] and stores that 16-byte pair straight to
+// val[base(8 m + g) + 8 nt + 2 t]: each store instruction writes 64 contiguous bytes of eight
+// element blocks.  base < 0: the element has no such block.
+template <int KS, int NT, int N2, int CT>
+__device__ __forceinline__ void mma_block_store(const double* ct, const double* __restrict__ frag,
+                                                long long base, double* val, int lane,
+                                                unsigned long long pol) {
+  const int g = lane >> 2, t = lane & 3;
+  double af[4][KS];
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) af[m][ks] = ct[(4 * ks + t) * CT + 8 * m + g];
+  }
+  long long bm[4];
+#pragma unroll
+  for (int m = 0; m < 4; ++m) bm[m] = __shfl_sync(0xffffffffu, base, 8 * m + g);
+  __syncwarp();  // the coefficient table may be rewritten from here on
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) {
+    double bf[KS];
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) bf[ks] = __ldg(frag + (ks * NT + nt) * 32 + lane);
+    const int n0 = 8 * nt + 2 * t;
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) dmma_8x8x4(d0, d1, af[m][ks], bf[ks]);
+      if ((N2 % 8 == 0 || n0 < N2) && bm[m] >= 0) store_pair(val + bm[m] + n0, d0, d1, pol);
+    }
+  }
 }
 
 // Stash field indices (per edge l, per lane): see the diagonal / neighbour passes.
@@ -486,6 +542,7 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
     else return st;
   };
 
+  const unsigned long long pol = output_policy(P.evict_first);
   // ---- RHS: the warp's contiguous slice, packed in shared memory and written in one go ------
   {
 #pragma unroll
@@ -527,11 +584,9 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
       cA[2] = det * (G01 * AB00 + G11 * AB10);
       cA[3] = det * (G01 * AB01 + G11 * AB11);
     }
-    if constexpr (SM::kMmaDiag) {
+    if constexpr (SM::kMma) {
       // D[32 elements x 36 entries] = C[32 x 16 coefficients] . T[16 x 36] on the FP64 tensor
-      // cores: coefficients are transposed through this warp's (still unused) staging area,
-      // results land directly in each element's staging row.
-      constexpr int CS = 4 * SM::kKS + 2;  // coefficient row stride (doubles)
+      // cores, stored from the fragments
       double cv[4 * SM::kKS];
       cv[0] = cD0; cv[1] = cD1; cv[2] = cD2; cv[3] = cR; cv[4] = cC0; cv[5] = cC1;
 #pragma unroll
@@ -543,33 +598,11 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
 #pragma unroll
       for (int k = SM::kTerms; k < 4 * SM::kKS; ++k) cv[k] = 0.0;
 #pragma unroll
-      for (int k = 0; k < 4 * SM::kKS; ++k) stw[lane * CS + k] = cv[k];
+      for (int k = 0; k < 4 * SM::kKS; ++k) stw[k * SM::kCT + lane] = cv[k];
       __syncwarp();
-      const int g = lane >> 2, t = lane & 3;
-      double af[4][SM::kKS];
-#pragma unroll
-      for (int m = 0; m < 4; ++m) {
-#pragma unroll
-        for (int ks = 0; ks < SM::kKS; ++ks) af[m][ks] = stw[(8 * m + g) * CS + 4 * ks + t];
-      }
-      __syncwarp();
-#pragma unroll
-      for (int nt = 0; nt < SM::kNT; ++nt) {
-        double bf_[SM::kKS];
-#pragma unroll
-        for (int ks = 0; ks < SM::kKS; ++ks) bf_[ks] = __ldg(P.bfrag + (ks * SM::kNT + nt) * 32 + lane);
-        const int n0 = 8 * nt + 2 * t;
-#pragma unroll
-        for (int m = 0; m < 4; ++m) {
-          double d0 = 0.0, d1 = 0.0;
-#pragma unroll
-          for (int ks = 0; ks < SM::kKS; ++ks) dmma_8x8x4(d0, d1, af[m][ks], bf_[ks]);
-          if (n0 < N2) {
-            *reinterpret_cast<double2*>(stw + (8 * m + g) * SS + n0) = make_double2(d0, d1);
-          }
-        }
-      }
-      __syncwarp();
+      mma_block_store<SM::kKS, SM::kNT, N2, SM::kCT>(
+          stw, P.bfrag, active ? static_cast<long long>(rp + diag_slot) * N2 : -1LL, P.val, lane,
+          pol);
     } else {
     constexpr int RC = NL <= 6 ? NL : (NL <= 10 ? 2 : 1);  // rows per register chunk
     double* blk = block_at(diag_slot);
@@ -661,7 +694,7 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
       }
     }
     }  // register path
-    if constexpr (!SM::kRowMode) {
+    if constexpr (!SM::kRowMode && !SM::kMma) {
       write_block<N2>(stw, st, active ? static_cast<long long>(rp + diag_slot) * N2 : -1LL,
                       P.val, lane, P.evict_first);
     }
@@ -674,6 +707,20 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
     const bool has = (meta & 3) == DGB_EDGE_INTERIOR;
     if (!__any_sync(0xffffffffu, has)) continue;
     const int lf = (meta >> 2) & 3, slot = meta >> 4;
+    if constexpr (SM::kMma) {
+      // neighbour terms X, Y0, Y1, Z0, Z1 of edge l against every possible lf, zero except lf
+      const bool store = active && has;
+      const double c5[5] = {K(F_X, l), K(F_Y0, l), K(F_Y1, l), K(F_Z0, l), K(F_Z1, l)};
+#pragma unroll
+      for (int k = 0; k < 4 * SM::kKS; ++k) {
+        stw[k * SM::kCT + lane] = (k < 15 && k / 5 == lf) ? c5[k % 5] : 0.0;
+      }
+      __syncwarp();
+      mma_block_store<SM::kKS, SM::kNT, N2, SM::kCT>(
+          stw, P.bfrag + (1 + l) * SM::kFragTile,
+          store ? static_cast<long long>(rp + slot) * N2 : -1LL, P.val, lane, pol);
+      continue;
+    }
     const double cY0 = K(F_Y0, l), cY1 = K(F_Y1, l), cZ0 = K(F_Z0, l), cZ1 = K(F_Z1, l);
     double cV[NQE];
 #pragma unroll

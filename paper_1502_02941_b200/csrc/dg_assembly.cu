@@ -1031,21 +1031,30 @@ void launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_prob
   copy(L::ET, V.ET, NQE);
   copy(L::EW, V.EW, NQE);
   const size_t smem = sizeof(double) * (SM::kTr + (THREADS / 32) * SM::kWarp);
-  if constexpr (SM::kMmaDiag) {
-    // B fragments of the diagonal terms in mma.m8n8k4 layout: lane (g, t) of tile (ks, nt)
-    // holds term 4 ks + t at entry 8 nt + g; built once per (plan, kappa) on the host.
+  if constexpr (SM::kMma) {
+    // B operands in mma.m8n8k4 fragment order: lane (g, t) of tile (ks, nt) holds term 4 ks + t
+    // at entry 8 nt + g.  Tile 0: the diagonal terms; tile 1 + l: the neighbour terms of local
+    // edge l against the neighbour's local edge lf' = k / 5,
+    //   X  = sum_p w_p phi^l_p (x) phi^lf'_(n-1-p)      Y_a = sum_p phi^l_p (x) w dphi_a^lf'_(n-1-p)
+    //   Z_a = sum_p w dphi_a^l_p (x) phi^lf'_(n-1-p)
+    // (the factored neighbour block of the CUDA-core path, expanded).  Built once per
+    // (plan, kappa) on the host.
     dgb_plan* mp = const_cast<dgb_plan*>(plan);
     double* frag = nullptr;
     for (auto& c : mp->bfrag_cache) {
       if (c.first == params->kappa) frag = c.second;
     }
     if (!frag) {  // first assembly with this kappa: build and upload (stream-ordered) once
+      auto ephi = [&](int l, int p, int i) { return x[L::EPHI + (l * NQE + p) * NL + i]; };
+      auto edw = [&](int l, int p, int a, int i) { return x[L::EDW + ((l * NQE + p) * 2 + a) * NL + i]; };
       std::vector<double> hb(SM::kBt, 0.0);
       for (int i = 0; i < SM::kBt; ++i) {
-        const int ln = i & 31, tile = i >> 5;
+        const int which = i / SM::kFragTile, r = i % SM::kFragTile;
+        const int ln = r & 31, tile = r >> 5;
         const int ks = tile / SM::kNT, nt = tile - ks * SM::kNT;
         const int k = 4 * ks + (ln & 3), n = 8 * nt + (ln >> 2);
-        if (k < SM::kTerms && n < N2) {
+        if (k >= SM::kTerms || n >= N2) continue;
+        if (which == 0) {
           int off;
           if (k < 3) off = L::S + k * N2;
           else if (k == 3) off = L::M;
@@ -1053,6 +1062,20 @@ void launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_prob
           else if (k < 12) off = L::W + (k - 6) * N2;
           else off = L::P + (k - 12) * N2;
           hb[i] = x[off + n];
+        } else {
+          const int l = which - 1, lf = k / 5, term = k % 5, bi = n / NL, bj = n % NL;
+          double acc = 0.0;
+          for (int p = 0; p < NQE; ++p) {
+            const int q = NQE - 1 - p;
+            switch (term) {
+              case 0: acc += x[L::EW + p] * ephi(l, p, bi) * ephi(lf, q, bj); break;
+              case 1: acc += ephi(l, p, bi) * edw(lf, q, 0, bj); break;
+              case 2: acc += ephi(l, p, bi) * edw(lf, q, 1, bj); break;
+              case 3: acc += edw(l, p, 0, bi) * ephi(lf, q, bj); break;
+              default: acc += edw(l, p, 1, bi) * ephi(lf, q, bj); break;
+            }
+          }
+          hb[i] = acc;
         }
       }
       cuda_check(cudaMalloc(&frag, hb.size() * sizeof(double)), "cudaMalloc(bfrag)");
