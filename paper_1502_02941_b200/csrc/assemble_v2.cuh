@@ -197,9 +197,10 @@ struct Smem {
   static constexpr int kTerms = 15;                              // S0 S1 S2 M T0 T1 W[6] P[3]
   static constexpr int kKS = (kTerms + 3) / 4, kNT = (N2 + 7) / 8;
   static constexpr int kCT = 36;                                 // coefficient table stride [k][lane]
-  static constexpr int kStage = kMma ? 4 * kKS * kCT
-                                     : (kRowMode ? ((32 * 4 * N2 + 2 + 1) & ~1) : 32 * SS);
-  static constexpr int kStash = 3 * NF * 32;
+  static constexpr int kStage = kMma ? 0 : (kRowMode ? ((32 * 4 * N2 + 2 + 1) & ~1) : 32 * SS);
+  // MMA path: the stash is the A operand itself, [term][lane] rows of stride kCT: diagonal
+  // terms 0..15 (15 = zero pad), then the neighbour terms [l][X Y0 Y1 Z0 Z1]
+  static constexpr int kStash = kMma ? (16 + 15) * kCT : 3 * NF * 32;
   static constexpr int kMeta = 3 * 32 / 2;                     // 3 ints per lane
   static constexpr int kTrig = BK == 2 ? 2 * NQV * 32 : 0;     // pointwise transport weights
   static constexpr int kRhs = (32 * NL + 1) & ~1;               // packed RHS slice of the warp
@@ -240,13 +241,13 @@ __device__ __forceinline__ void store_pair(double* g, double a, double b, unsign
 }
 
 // One warp-wide block product on the FP64 tensor cores: D[32 elements x N2] = C . B, where
-// C[lane][k] sits in the warp's coefficient table ct[k * kCT + lane] and B is a fragment-ordered
+// a_at(m, ks) returns C[8 m + g][4 ks + t] for this lane (g, t) and B is a fragment-ordered
 // table in global memory ([ks][nt][lane], lane (g, t) holding B[4 ks + t][8 nt + g]).  Lane
 // (g, t) ends up with D[8 m + g][8 nt + 2 t .. +1] and stores that 16-byte pair straight to
 // val[base(8 m + g) + 8 nt + 2 t]: each store instruction writes 64 contiguous bytes of eight
 // element blocks.  base < 0: the element has no such block.
-template <int KS, int NT, int N2, int CT>
-__device__ __forceinline__ void mma_block_store(const double* ct, const double* __restrict__ frag,
+template <int KS, int NT, int N2, class AF>
+__device__ __forceinline__ void mma_block_store(AF a_at, const double* __restrict__ frag,
                                                 long long base, double* val, int lane,
                                                 unsigned long long pol) {
   const int g = lane >> 2, t = lane & 3;
@@ -254,12 +255,11 @@ __device__ __forceinline__ void mma_block_store(const double* ct, const double* 
 #pragma unroll
   for (int m = 0; m < 4; ++m) {
 #pragma unroll
-    for (int ks = 0; ks < KS; ++ks) af[m][ks] = ct[(4 * ks + t) * CT + 8 * m + g];
+    for (int ks = 0; ks < KS; ++ks) af[m][ks] = a_at(m, ks);
   }
   long long bm[4];
 #pragma unroll
   for (int m = 0; m < 4; ++m) bm[m] = __shfl_sync(0xffffffffu, base, 8 * m + g);
-  __syncwarp();  // the coefficient table may be rewritten from here on
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt) {
     double bf[KS];
@@ -302,7 +302,16 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
   int* mk = reinterpret_cast<int*>(sk + SM::kStash); // meta [3][32]: kind | lf << 2 | slot << 4
   double* sq = sk + SM::kStash + SM::kMeta;          // TRIG: [NQV][2][32]
   double* srhs = sq + SM::kTrig;                     // [32][NL] packed RHS
-  auto K = [&](int f, int l) -> double& { return sk[(f * 3 + l) * 32 + lane]; };
+  auto K = [&](int f, int l) -> double& {
+    if constexpr (SM::kMma) {
+      constexpr int CT = SM::kCT;
+      const int row = f == F_W0 ? 6 + 2 * l : f == F_W1 ? 7 + 2 * l : f == F_P ? 12 + l
+                    : 16 + 5 * l + (f == F_X ? 0 : f - F_Y0 + 1);
+      return sk[row * CT + lane];
+    } else {
+      return sk[(f * 3 + l) * 32 + lane];
+    }
+  };
 
   const int e = P.row_begin + blockIdx.x * blockDim.x + threadIdx.x;
   const bool active = e < P.row_end;
@@ -350,9 +359,7 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
   }
 
   // ---- phase A2: per local edge -> stashed coefficient record, boundary RHS --------------------
-  int cols[4], kinds[4], nb = 1;
-  cols[0] = ee;
-  kinds[0] = -1;
+  int fcol[3] = {-1, -1, -1};  // neighbour across local edge l (interior edges only)
   int4 anb = make_int4(0, 0, 0, 0), aop = make_int4(0, 0, 0, 0);
   if (P.adj_nb) {  // bound adjacency record: two coalesced 16-byte loads per element
     anb = __ldg(P.adj_nb + (ee - P.row_begin));
@@ -399,8 +406,7 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
         const double ef = __ldg(P.prob.diffusion.per_element + f);
         eps_e = ee < f ? 0.5 * (eps + ef) : 0.5 * (ef + eps);
       }
-      cols[nb] = f;
-      kinds[nb++] = l;
+      fcol[l] = f;
       const double base = 0.5 * h * eps_e;  // avg * h * eps
       w0 = base * ge0;
       w1 = base * ge1;
@@ -497,16 +503,20 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
     if constexpr (BK == 0) K(F_X, l) = cx;
     mk[l * 32 + lane] = kind | (lf << 2);
   }
-  // sorted block columns -> slots (CSR order of the reference's stiffness())
+  // sorted block columns -> slots (CSR order of the reference's stiffness()): each block's
+  // slot is its rank among the row's columns (all distinct), computed without indexed arrays
+  int slot_of[4], nb = 1;
+  {
+    const int cx[4] = {ee, fcol[0], fcol[1], fcol[2]};
 #pragma unroll
-  for (int x = 1; x < 4; ++x) {
+    for (int i = 0; i < 4; ++i) {
+      int r = 0;
 #pragma unroll
-    for (int y = x; y > 0; --y) {
-      if (y < nb && cols[y - 1] > cols[y]) {
-        int t = cols[y]; cols[y] = cols[y - 1]; cols[y - 1] = t;
-        t = kinds[y]; kinds[y] = kinds[y - 1]; kinds[y - 1] = t;
-      }
+      for (int j = 0; j < 4; ++j) r += (j != i && cx[j] >= 0 && cx[j] < cx[i]) ? 1 : 0;
+      slot_of[i] = r;
     }
+#pragma unroll
+    for (int l = 0; l < 3; ++l) nb += fcol[l] >= 0 ? 1 : 0;
   }
   int rp;
   if (P.row_ptr_src) {  // pattern computed once per mesh: copy this element's entry
@@ -518,14 +528,13 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
   } else {
     rp = P.row_ptr[ee - P.row_begin];
   }
-  int diag_slot = 0;
+  const int diag_slot = slot_of[0];
+  if (active) P.col[rp + diag_slot] = ee;
 #pragma unroll
-  for (int s = 0; s < 4; ++s) {
-    if (s < nb) {
-      if (active) P.col[rp + s] = cols[s];
-      if (kinds[s] < 0) diag_slot = s;
-#pragma unroll
-      for (int l = 0; l < 3; ++l) if (kinds[s] == l) mk[l * 32 + lane] |= s << 4;
+  for (int l = 0; l < 3; ++l) {
+    if (fcol[l] >= 0) {
+      if (active) P.col[rp + slot_of[1 + l]] = fcol[l];
+      mk[l * 32 + lane] |= slot_of[1 + l] << 4;
     }
   }
 
@@ -587,21 +596,14 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
     if constexpr (SM::kMma) {
       // D[32 elements x 36 entries] = C[32 x 16 coefficients] . T[16 x 36] on the FP64 tensor
       // cores, stored from the fragments
-      double cv[4 * SM::kKS];
-      cv[0] = cD0; cv[1] = cD1; cv[2] = cD2; cv[3] = cR; cv[4] = cC0; cv[5] = cC1;
+      const double cv[6] = {cD0, cD1, cD2, cR, cC0, cC1};
 #pragma unroll
-      for (int l = 0; l < 3; ++l) {
-        cv[6 + 2 * l] = K(F_W0, l);
-        cv[7 + 2 * l] = K(F_W1, l);
-        cv[12 + l] = K(F_P, l);
-      }
-#pragma unroll
-      for (int k = SM::kTerms; k < 4 * SM::kKS; ++k) cv[k] = 0.0;
-#pragma unroll
-      for (int k = 0; k < 4 * SM::kKS; ++k) stw[k * SM::kCT + lane] = cv[k];
+      for (int k = 0; k < 6; ++k) sk[k * SM::kCT + lane] = cv[k];
+      sk[15 * SM::kCT + lane] = 0.0;
       __syncwarp();
-      mma_block_store<SM::kKS, SM::kNT, N2, SM::kCT>(
-          stw, P.bfrag, active ? static_cast<long long>(rp + diag_slot) * N2 : -1LL, P.val, lane,
+      const int g = lane >> 2, t = lane & 3;
+      mma_block_store<SM::kKS, SM::kNT, N2>(
+          [&](int m, int ks) { return sk[(4 * ks + t) * SM::kCT + 8 * m + g]; }, P.bfrag, active ? static_cast<long long>(rp + diag_slot) * N2 : -1LL, P.val, lane,
           pol);
     } else {
     constexpr int RC = NL <= 6 ? NL : (NL <= 10 ? 2 : 1);  // rows per register chunk
@@ -710,14 +712,19 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
     if constexpr (SM::kMma) {
       // neighbour terms X, Y0, Y1, Z0, Z1 of edge l against every possible lf, zero except lf
       const bool store = active && has;
-      const double c5[5] = {K(F_X, l), K(F_Y0, l), K(F_Y1, l), K(F_Z0, l), K(F_Z1, l)};
+      // lane (g, t) needs term k = 4 ks + t of element 8 m + g: nonzero only if k / 5 is that
+      // element's lf
+      const int g = lane >> 2, t = lane & 3;
+      int lfm[4];
 #pragma unroll
-      for (int k = 0; k < 4 * SM::kKS; ++k) {
-        stw[k * SM::kCT + lane] = (k < 15 && k / 5 == lf) ? c5[k % 5] : 0.0;
-      }
-      __syncwarp();
-      mma_block_store<SM::kKS, SM::kNT, N2, SM::kCT>(
-          stw, P.bfrag + (1 + l) * SM::kFragTile,
+      for (int m = 0; m < 4; ++m) lfm[m] = (mk[l * 32 + 8 * m + g] >> 2) & 3;
+      const double* so = sk + (16 + 5 * l) * SM::kCT + g;
+      mma_block_store<SM::kKS, SM::kNT, N2>(
+          [&](int m, int ks) {
+            const int k = 4 * ks + t;
+            return (k < 15 && k / 5 == lfm[m]) ? so[(k % 5) * SM::kCT + 8 * m] : 0.0;
+          },
+          P.bfrag + (1 + l) * SM::kFragTile,
           store ? static_cast<long long>(rp + slot) * N2 : -1LL, P.val, lane, pol);
       continue;
     }

@@ -2,7 +2,7 @@
 # Parity suite + short bench lines for configs 2-4 (tuning loop).
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
-python -m pytest tests -m gpu -x -q 2>&1 | tail -4
+python -m pytest tests -m gpu -x -q 2>&1 | grep -E "passed|failed|Error|assert" | tail -8
 for c in ${CONFIGS:-2 3 4}; do
   python bench.py --config $c --steps 10 --warmup 3 --no-e2e --no-cpu-baseline $BENCH_ARGS > gpurun_out/q_c${c}.json 2>&1
 done
