@@ -201,13 +201,15 @@ struct Smem {
   // MMA path: the stash is the A operand itself, [term][lane] rows of stride kCT: diagonal
   // terms 0..15 (15 = zero pad), then the neighbour terms [l][X Y0 Y1 Z0 Z1]
   static constexpr int kStash = kMma ? (16 + 15) * kCT : 3 * NF * 32;
-  static constexpr int kMeta = 3 * 32 / 2;                     // 3 ints per lane
+  static constexpr int kMeta = (3 * 32 + (kMma ? 48 : 0)) / 2; // 3 ints per lane (+ MMA row map)
   static constexpr int kTrig = BK == 2 ? 2 * NQV * 32 : 0;     // pointwise transport weights
   static constexpr int kRhs = (32 * NL + 1) & ~1;               // packed RHS slice of the warp
   static constexpr int kWarp = kStage + kStash + kMeta + kTrig + kRhs;
   static constexpr int kTr = (3 * NQE * 3 * NL + 1) & ~1;      // trace table (per CTA)
   static constexpr int kFragTile = kKS * kNT * 32;               // one B operand, fragment order
-  static constexpr int kBt = kMma ? 4 * kFragTile : 0;           // diagonal + neighbour l = 0..2
+  // neighbour operands per (l, lf): K = 8 (5 terms), fragment order [ks 2][nt][lane]
+  static constexpr int kOffTile = 2 * kNT * 32;
+  static constexpr int kBt = kMma ? kFragTile + 9 * kOffTile : 0;
 };
 
 // Offset (doubles) of diagonal term k in the tensor parameter block (MMA path, P2, const b).
@@ -710,22 +712,51 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
     if (!__any_sync(0xffffffffu, has)) continue;
     const int lf = (meta >> 2) & 3, slot = meta >> 4;
     if constexpr (SM::kMma) {
-      // neighbour terms X, Y0, Y1, Z0, Z1 of edge l against every possible lf, zero except lf
+      // neighbour terms X, Y0, Y1, Z0, Z1 of edge l.  The B operand depends on the
+      // neighbour's local edge lf, so the warp's elements are regrouped into 8-row m-tiles of
+      // equal lf (rows are independent in D = C . B): ceil(n_lf / 8) tiles per lf value, each
+      // an m8 x n(N2) x k8 product (5 terms) against that lf's operand.
       const bool store = active && has;
-      // lane (g, t) needs term k = 4 ks + t of element 8 m + g: nonzero only if k / 5 is that
-      // element's lf
       const int g = lane >> 2, t = lane & 3;
-      int lfm[4];
+      const unsigned lt = (1u << lane) - 1u;
+      const unsigned m0 = __ballot_sync(0xffffffffu, has && lf == 0);
+      const unsigned m1 = __ballot_sync(0xffffffffu, has && lf == 1);
+      const unsigned m2 = __ballot_sync(0xffffffffu, has && lf == 2);
+      const int t1 = (__popc(m0) + 7) >> 3, t2 = t1 + ((__popc(m1) + 7) >> 3);
+      const int ntiles = t2 + ((__popc(m2) + 7) >> 3);
+      int* pmap = mk + 96;  // sorted row -> lane (-1: padding row)
+      pmap[lane] = -1;
+      if (lane < 16) pmap[32 + lane] = -1;
+      __syncwarp();
+      if (has) {
+        const unsigned mv = lf == 0 ? m0 : (lf == 1 ? m1 : m2);
+        const int tv = lf == 0 ? 0 : (lf == 1 ? t1 : t2);
+        pmap[8 * tv + __popc(mv & lt)] = lane;
+      }
+      __syncwarp();
+      const long long my_base = store ? static_cast<long long>(rp + slot) * N2 : -1LL;
+      const double* so = sk + (16 + 5 * l) * SM::kCT;
+#pragma unroll 1
+      for (int r = 0; r < ntiles; ++r) {
+        const int v = r < t1 ? 0 : (r < t2 ? 1 : 2);
+        const int src = pmap[8 * r + g];
+        const int sl = src < 0 ? 0 : src;
+        const double a0 = src < 0 ? 0.0 : so[t * SM::kCT + sl];
+        const double a1 = (src < 0 || t != 0) ? 0.0 : so[4 * SM::kCT + sl];
+        long long bm = __shfl_sync(0xffffffffu, my_base, sl);
+        if (src < 0) bm = -1;
+        const double* fr = P.bfrag + SM::kFragTile + (l * 3 + v) * SM::kOffTile + lane;
 #pragma unroll
-      for (int m = 0; m < 4; ++m) lfm[m] = (mk[l * 32 + 8 * m + g] >> 2) & 3;
-      const double* so = sk + (16 + 5 * l) * SM::kCT + g;
-      mma_block_store<SM::kKS, SM::kNT, N2>(
-          [&](int m, int ks) {
-            const int k = 4 * ks + t;
-            return (k < 15 && k / 5 == lfm[m]) ? so[(k % 5) * SM::kCT + 8 * m] : 0.0;
-          },
-          P.bfrag + (1 + l) * SM::kFragTile,
-          store ? static_cast<long long>(rp + slot) * N2 : -1LL, P.val, lane, pol);
+        for (int nt = 0; nt < SM::kNT; ++nt) {
+          const double b0 = __ldg(fr + nt * 32), b1 = __ldg(fr + (SM::kNT + nt) * 32);
+          double d0 = 0.0, d1 = 0.0;
+          dmma_8x8x4(d0, d1, a0, b0);
+          dmma_8x8x4(d0, d1, a1, b1);
+          const int n0 = 8 * nt + 2 * t;
+          if ((N2 % 8 == 0 || n0 < N2) && bm >= 0) store_pair(P.val + bm + n0, d0, d1, pol);
+        }
+      }
+      __syncwarp();  // the row map is rebuilt for the next l
       continue;
     }
     const double cY0 = K(F_Y0, l), cY1 = K(F_Y1, l), cZ0 = K(F_Z0, l), cZ1 = K(F_Z1, l);

@@ -1033,10 +1033,10 @@ void launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_prob
   const size_t smem = sizeof(double) * (SM::kTr + (THREADS / 32) * SM::kWarp);
   if constexpr (SM::kMma) {
     // B operands in mma.m8n8k4 fragment order: lane (g, t) of tile (ks, nt) holds term 4 ks + t
-    // at entry 8 nt + g.  Tile 0: the diagonal terms; tile 1 + l: the neighbour terms of local
-    // edge l against the neighbour's local edge lf' = k / 5,
-    //   X  = sum_p w_p phi^l_p (x) phi^lf'_(n-1-p)      Y_a = sum_p phi^l_p (x) w dphi_a^lf'_(n-1-p)
-    //   Z_a = sum_p w dphi_a^l_p (x) phi^lf'_(n-1-p)
+    // at entry 8 nt + g.  First the diagonal terms (K = 16), then per (l, lf) the five
+    // neighbour terms of local edge l against the neighbour's local edge lf (K = 8),
+    //   X  = sum_p w_p phi^l_p (x) phi^lf_(n-1-p)      Y_a = sum_p phi^l_p (x) w dphi_a^lf_(n-1-p)
+    //   Z_a = sum_p w dphi_a^l_p (x) phi^lf_(n-1-p)
     // (the factored neighbour block of the CUDA-core path, expanded).  Built once per
     // (plan, kappa) on the host.
     dgb_plan* mp = const_cast<dgb_plan*>(plan);
@@ -1049,11 +1049,13 @@ void launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_prob
       auto edw = [&](int l, int p, int a, int i) { return x[L::EDW + ((l * NQE + p) * 2 + a) * NL + i]; };
       std::vector<double> hb(SM::kBt, 0.0);
       for (int i = 0; i < SM::kBt; ++i) {
-        const int which = i / SM::kFragTile, r = i % SM::kFragTile;
+        const bool diag = i < SM::kFragTile;
+        const int which = diag ? 0 : 1 + (i - SM::kFragTile) / SM::kOffTile;  // 1 + l * 3 + lf
+        const int r = diag ? i : (i - SM::kFragTile) % SM::kOffTile;
         const int ln = r & 31, tile = r >> 5;
         const int ks = tile / SM::kNT, nt = tile - ks * SM::kNT;
         const int k = 4 * ks + (ln & 3), n = 8 * nt + (ln >> 2);
-        if (k >= SM::kTerms || n >= N2) continue;
+        if (k >= (diag ? SM::kTerms : 5) || n >= N2) continue;
         if (which == 0) {
           int off;
           if (k < 3) off = L::S + k * N2;
@@ -1063,7 +1065,7 @@ void launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_prob
           else off = L::P + (k - 12) * N2;
           hb[i] = x[off + n];
         } else {
-          const int l = which - 1, lf = k / 5, term = k % 5, bi = n / NL, bj = n % NL;
+          const int l = (which - 1) / 3, lf = (which - 1) % 3, term = k, bi = n / NL, bj = n % NL;
           double acc = 0.0;
           for (int p = 0; p < NQE; ++p) {
             const int q = NQE - 1 - p;
@@ -1140,9 +1142,13 @@ bool try_launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_
     DGB_V2(6, 7, 3, 0, 64, 6)
     DGB_V2(3, 6, 2, 0, 64, 8)
   }
-  if (mb == 5) {
-    DGB_V2(6, 7, 3, 0, 32, 12)
-    DGB_V2(3, 6, 2, 0, 32, 16)
+  if (mb == 5) {  // register-capped variants (more resident warps)
+    DGB_V2(6, 7, 3, 0, 128, 5)
+    DGB_V2(3, 6, 2, 0, 128, 5)
+  }
+  if (mb == 6) {
+    DGB_V2(6, 7, 3, 0, 128, 6)
+    DGB_V2(3, 6, 2, 0, 128, 6)
   }
   DGB_V2(3, 6, 2, 0, 128, 4)
   DGB_V2(3, 6, 2, 1, 128, 4)
