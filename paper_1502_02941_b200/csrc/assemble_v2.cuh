@@ -278,6 +278,22 @@ __device__ __forceinline__ void mma_block_store(AF a_at, const double* __restric
   }
 }
 
+// Velocity of the kernel's specialised kind (BK = dgb_vector_field kind): no dead branches,
+// so a constant-velocity kernel carries no call into the trigonometric form.
+template <int BK>
+__device__ __forceinline__ void velocity_k(const dgb_vector_field& b, double x, double y,
+                                           double& bx, double& by) {
+  if constexpr (BK == DGB_VEC_CONSTANT) {
+    bx = b.p[0];
+    by = b.p[1];
+  } else if constexpr (BK == DGB_VEC_AFFINE) {
+    bx = FADD(FADD(b.p[0], FMUL(b.p[2], x)), FMUL(b.p[3], y));
+    by = FADD(FADD(b.p[1], FMUL(b.p[4], x)), FMUL(b.p[5], y));
+  } else {
+    velocity_trig(b.p[0], b.p[1], x, y, bx, by);
+  }
+}
+
 // Stash field indices (per edge l, per lane): see the diagonal / neighbour passes.
 enum { F_W0 = 0, F_W1, F_P, F_Y0, F_Y1, F_Z0, F_Z1, F_X, F_U = 7 };
 
@@ -353,7 +369,7 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
       for (int i = 0; i < NL; ++i) F[i] = fma(c, P.t.x[L::PHI + q * NL + i], F[i]);
       if constexpr (TRIG) {
         double bx, by;
-        velocity(bf, px, py, bx, by);
+        velocity_k<BK>(bf, px, py, bx, by);
         sq[(2 * q) * 32 + lane] = dw * (G00 * bx + G10 * by);
         sq[(2 * q + 1) * 32 + lane] = dw * (G01 * bx + G11 * by);
       }
@@ -433,7 +449,7 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
           const double px = FADD(A.x, FMUL(tq, dx));
           const double py = FADD(A.y, FMUL(tq, dy));
           double bx, by;
-          velocity(bf, px, py, bx, by);
+          velocity_k<BK>(bf, px, py, bx, by);
           const double fl = FADD(FMUL(bx, nx), FMUL(by, ny));
           const double up = fl < 0.0 ? FMUL(w, fl) : 0.0;
           const double pen = FMUL(sh, FMUL(w, eps_e));
@@ -451,7 +467,7 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
         const double px = FADD(A.x, FMUL(tq, dx));
         const double py = FADD(A.y, FMUL(tq, dy));
         double bx, by;
-        velocity(bf, px, py, bx, by);
+        velocity_k<BK>(bf, px, py, bx, by);
         fls[p] = FADD(FMUL(bx, nx), FMUL(by, ny));
         if (fls[p] < -1e-12 * fmax(1.0, hypot_dd(bx, by))) inflow = true;  // assembly.cpp:324-401
         gb[p] = scalar_point(kind == DGB_EDGE_NEUMANN ? P.prob.neumann : P.prob.dirichlet, px, py);
