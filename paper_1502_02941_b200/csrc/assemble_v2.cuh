@@ -752,24 +752,43 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
       __syncwarp();
       const long long my_base = store ? static_cast<long long>(rp + slot) * N2 : -1LL;
       const double* so = sk + (16 + 5 * l) * SM::kCT;
-#pragma unroll 1
-      for (int r = 0; r < ntiles; ++r) {
-        const int v = r < t1 ? 0 : (r < t2 ? 1 : 2);
+      // class-major: each lf's operand is loaded once into registers, and the next tile's
+      // row operands are fetched while the current tile's products run
+      auto tile_rows = [&](int r, double& a0, double& a1, long long& bm) {
         const int src = pmap[8 * r + g];
         const int sl = src < 0 ? 0 : src;
-        const double a0 = src < 0 ? 0.0 : so[t * SM::kCT + sl];
-        const double a1 = (src < 0 || t != 0) ? 0.0 : so[4 * SM::kCT + sl];
-        long long bm = __shfl_sync(0xffffffffu, my_base, sl);
+        a0 = src < 0 ? 0.0 : so[t * SM::kCT + sl];
+        a1 = (src < 0 || t != 0) ? 0.0 : so[4 * SM::kCT + sl];
+        bm = __shfl_sync(0xffffffffu, my_base, sl);
         if (src < 0) bm = -1;
+      };
+      double a0, a1;
+      long long bm;
+      if (ntiles > 0) tile_rows(0, a0, a1, bm);
+#pragma unroll
+      for (int v = 0; v < 3; ++v) {
+        const int tb = v == 0 ? 0 : (v == 1 ? t1 : t2), te = v == 0 ? t1 : (v == 1 ? t2 : ntiles);
+        if (tb == te) continue;
         const double* fr = P.bfrag + SM::kFragTile + (l * 3 + v) * SM::kOffTile + lane;
+        double bv[2][SM::kNT];
 #pragma unroll
         for (int nt = 0; nt < SM::kNT; ++nt) {
-          const double b0 = __ldg(fr + nt * 32), b1 = __ldg(fr + (SM::kNT + nt) * 32);
-          double d0 = 0.0, d1 = 0.0;
-          dmma_8x8x4(d0, d1, a0, b0);
-          dmma_8x8x4(d0, d1, a1, b1);
-          const int n0 = 8 * nt + 2 * t;
-          if ((N2 % 8 == 0 || n0 < N2) && bm >= 0) store_pair(P.val + bm + n0, d0, d1, pol);
+          bv[0][nt] = __ldg(fr + nt * 32);
+          bv[1][nt] = __ldg(fr + (SM::kNT + nt) * 32);
+        }
+#pragma unroll 1
+        for (int r = tb; r < te; ++r) {
+          const double c0 = a0, c1 = a1;
+          const long long cb = bm;
+          if (r + 1 < ntiles) tile_rows(r + 1, a0, a1, bm);
+#pragma unroll
+          for (int nt = 0; nt < SM::kNT; ++nt) {
+            double d0 = 0.0, d1 = 0.0;
+            dmma_8x8x4(d0, d1, c0, bv[0][nt]);
+            dmma_8x8x4(d0, d1, c1, bv[1][nt]);
+            const int n0 = 8 * nt + 2 * t;
+            if ((N2 % 8 == 0 || n0 < N2) && cb >= 0) store_pair(P.val + cb + n0, d0, d1, pol);
+          }
         }
       }
       __syncwarp();  // the row map is rebuilt for the next l
