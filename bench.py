@@ -43,6 +43,8 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--minblocks", type=int, default=0, help="tuning knob (P2 kernel CTAs/SM)")
+    ap.add_argument("--ablate", type=int, default=0,
+                    help="profiling only, results wrong: skip kernel parts (see dg_assembly.cu)")
     ap.add_argument("--l2-policy", type=int, default=-1,
                     help="plan L2 policy bits (1: persist nodes, 2: evict-first output); "
                          "-1: the default for the config")
@@ -218,6 +220,8 @@ def run_ours(args, world, rank, local):
     plan = shards[0].plan
     if args.minblocks:
         plan.set_option(capi.OPTION_MIN_BLOCKS, args.minblocks)
+    if args.ablate:
+        plan.set_option(1000, args.ablate)
     stream = torch.cuda.current_stream(local)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=f"cuda:{local}")  # 256 MiB > L2
 

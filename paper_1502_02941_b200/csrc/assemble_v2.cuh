@@ -20,19 +20,22 @@
 namespace dgb {
 namespace v2 {
 
-// Flat layout of the tensor parameter block (offsets in doubles, all compile-time).
-template <int NL, int NQV, int NQE, bool TRIG>
+// Flat layout of the tensor parameter block (offsets in doubles, all compile-time).  FULL =
+// false (the tensor-core P2 kernel): the element-matrix tensors S .. P live in the B-operand
+// table instead, and the parameter block keeps only the basis / quadrature tables -- a large
+// __grid_constant__ block is re-read at every CTA launch (tools/microbench/launch_cost.cu).
+template <int NL, int NQV, int NQE, bool TRIG, bool FULL = true>
 struct Lay {
   static constexpr int N2 = NL * NL;
-  static constexpr bool kHasP = !TRIG && NL <= 10;   // face mass tensors (constant b)
-  static constexpr bool kHasTA = !TRIG && NL <= 10;  // affine transport tensors
-  static constexpr int S = 0;                               // 3: S00, S01 + S10, S11
-  static constexpr int M = S + 3 * N2;                      // 1: mass
-  static constexpr int W = M + N2;                          // 6: kappa Q^T - Q  [l][a]
-  static constexpr int T = W + 6 * N2;                      // 2: transport (constant b)
-  static constexpr int TA = T + (TRIG ? 0 : 2) * N2;        // 4: affine transport [a][c]
-  static constexpr int P = TA + (kHasTA ? 4 : 0) * N2;      // 3: face mass [l]
-  static constexpr int PHI = P + (kHasP ? 3 : 0) * N2;      // [q][i]
+  static constexpr bool kHasP = FULL && !TRIG && NL <= 10;   // face mass tensors (constant b)
+  static constexpr bool kHasTA = FULL && !TRIG && NL <= 10;  // affine transport tensors
+  static constexpr int S = 0;                                   // 3: S00, S01 + S10, S11
+  static constexpr int M = S + (FULL ? 3 : 0) * N2;             // 1: mass
+  static constexpr int W = M + (FULL ? 1 : 0) * N2;             // 6: kappa Q^T - Q  [l][a]
+  static constexpr int T = W + (FULL ? 6 : 0) * N2;             // 2: transport (constant b)
+  static constexpr int TA = T + (FULL && !TRIG ? 2 : 0) * N2;   // 4: affine transport [a][c]
+  static constexpr int P = TA + (kHasTA ? 4 : 0) * N2;          // 3: face mass [l]
+  static constexpr int PHI = P + (kHasP ? 3 : 0) * N2;          // [q][i]
   static constexpr int DPHI = PHI + NQV * NL;               // [q][a][i]      (TRIG only)
   static constexpr int EPHI = DPHI + (TRIG ? NQV * 2 * NL : 0);  // [l][p][i]
   static constexpr int EDPHI = EPHI + 3 * NQE * NL;         // [l][p][a][i]
@@ -45,12 +48,15 @@ struct Lay {
   static constexpr int TOTAL = EW + NQE;
 };
 
-template <int NL, int NQV, int NQE, bool TRIG>
+template <int NL, int NQV, int NQE, bool TRIG, bool FULL>
 struct Tab {
-  double x[Lay<NL, NQV, NQE, TRIG>::TOTAL];
+  double x[Lay<NL, NQV, NQE, TRIG, FULL>::TOTAL];
 };
 
-template <int NL, int NQV, int NQE, bool TRIG>
+// The tensor-core kernel (P2, constant velocity) takes the compact parameter block.
+constexpr bool full_tensors(int NL, int BK) { return !(NL == 6 && BK == 0); }
+
+template <int NL, int NQV, int NQE, bool TRIG, bool FULL>
 struct Params2 {
   const double* nodes;
   const int32_t* elements;
@@ -71,9 +77,10 @@ struct Params2 {
   int32_t row_begin, row_end;  // block rows [row_begin, row_end) of this launch (a shard)
   int32_t drop_neumann;
   int32_t evict_first;           // L2 evict-first hint on the output stream
+  int32_t ablate;                // profiling diagnostics only (wrong results): see dg_assembly.cu
   double kappa, sigma_i, sigma_b;
   dgb_problem prob;
-  Tab<NL, NQV, NQE, TRIG> t;
+  Tab<NL, NQV, NQE, TRIG, FULL> t;
 };
 
 // Staging stride (doubles) per lane: even, so 16-byte chunks stay aligned.
@@ -299,10 +306,10 @@ enum { F_W0 = 0, F_W1, F_P, F_Y0, F_Y1, F_Z0, F_Z1, F_X, F_U = 7 };
 
 template <int NL, int NQV, int NQE, int BK, int THREADS, int MINB>
 __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
-    const __grid_constant__ Params2<NL, NQV, NQE, BK == 2> P) {
+    const __grid_constant__ Params2<NL, NQV, NQE, BK == 2, full_tensors(NL, BK)> P) {
   constexpr bool TRIG = BK == 2;
   constexpr int N2 = NL * NL;
-  using L = Lay<NL, NQV, NQE, TRIG>;
+  using L = Lay<NL, NQV, NQE, TRIG, full_tensors(NL, BK)>;
   using SM = Smem<NL, NQV, NQE, BK>;
   constexpr int SS = SM::SS, NF = SM::NF;
   extern __shared__ double smem[];
@@ -313,6 +320,7 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
                    : P.t.x[L::EDW + ((l * NQE + p) * 2 + c - 1) * NL + j];  // w_p d phi
   }
   __syncthreads();
+  if (P.ablate & 16) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double* stw = smem + SM::kTr + warp * SM::kWarp;  // staging [32][SS]
   double* st = stw + lane * SS;  // (even N2) this lane's block
@@ -350,6 +358,10 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
   const double G00 = B11 * rdet, G01 = -B10 * rdet;
   const double G10 = -B01 * rdet, G11 = B00 * rdet;
   const double eps = scalar_element(P.prob.diffusion, ee);
+  if (P.ablate & 32) {
+    if (active) P.rhs[ee - P.row_begin] = det;
+    return;
+  }
 
   // ---- phase A1: RHS volume term and pointwise transport weights (few live registers) -------
   double F[NL];
@@ -362,7 +374,7 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
       const double px = FADD(FADD(pv[0].x, FMUL(B00, P.t.x[L::VX + q])), FMUL(B01, P.t.x[L::VY + q]));
       const double py = FADD(FADD(pv[0].y, FMUL(B10, P.t.x[L::VX + q])), FMUL(B11, P.t.x[L::VY + q]));
       const double f = fs.kind == DGB_FIELD_PER_ELEMENT ? __ldg(fs.per_element + ee)
-                                                        : scalar_point_inline(fs, px, py);
+                       : (P.ablate & 2) ? px : scalar_point_inline(fs, px, py);
       const double dw = det * P.t.x[L::VW + q];
       const double c = dw * f;
 #pragma unroll
@@ -620,9 +632,12 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
       sk[15 * SM::kCT + lane] = 0.0;
       __syncwarp();
       const int g = lane >> 2, t = lane & 3;
-      mma_block_store<SM::kKS, SM::kNT, N2>(
-          [&](int m, int ks) { return sk[(4 * ks + t) * SM::kCT + 8 * m + g]; }, P.bfrag, active ? static_cast<long long>(rp + diag_slot) * N2 : -1LL, P.val, lane,
-          pol);
+      if (!(P.ablate & 8)) {
+        mma_block_store<SM::kKS, SM::kNT, N2>(
+            [&](int m, int ks) { return sk[(4 * ks + t) * SM::kCT + 8 * m + g]; }, P.bfrag,
+            (active && !(P.ablate & 1)) ? static_cast<long long>(rp + diag_slot) * N2 : -1LL,
+            P.val, lane, pol);
+      }
     } else {
     constexpr int RC = NL <= 6 ? NL : (NL <= 10 ? 2 : 1);  // rows per register chunk
     double* blk = block_at(diag_slot);
@@ -728,6 +743,7 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
     if (!__any_sync(0xffffffffu, has)) continue;
     const int lf = (meta >> 2) & 3, slot = meta >> 4;
     if constexpr (SM::kMma) {
+      if (P.ablate & 4) continue;
       // neighbour terms X, Y0, Y1, Z0, Z1 of edge l.  The B operand depends on the
       // neighbour's local edge lf, so the warp's elements are regrouped into 8-row m-tiles of
       // equal lf (rows are independent in D = C . B): ceil(n_lf / 8) tiles per lf value, each
@@ -787,7 +803,7 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
             dmma_8x8x4(d0, d1, c0, bv[0][nt]);
             dmma_8x8x4(d0, d1, c1, bv[1][nt]);
             const int n0 = 8 * nt + 2 * t;
-            if ((N2 % 8 == 0 || n0 < N2) && cb >= 0) store_pair(P.val + cb + n0, d0, d1, pol);
+            if ((N2 % 8 == 0 || n0 < N2) && cb >= 0 && !(P.ablate & 1)) store_pair(P.val + cb + n0, d0, d1, pol);
           }
         }
       }

@@ -899,6 +899,7 @@ struct dgb_plan {
   int l2_policy = 0;            // bit 0: persist nodes in L2, bit 1: evict-first output
   // DMMA B fragments of the diagonal terms, one table per kappa (W depends on kappa)
   std::vector<std::pair<double, double*>> bfrag_cache;
+  int ablate = 0;  // profiling diagnostics (dgb_plan_set_option 1000)
 };
 
 namespace {
@@ -968,8 +969,10 @@ void launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_prob
                const dgb_params* params, dgb_bsr* out, double* rhs, cudaStream_t s,
                int out_row_begin, int out_row_end, const int32_t* row_ptr_src) {
   constexpr bool TRIG = BK == 2;
-  using L = dgb::v2::Lay<NL, NQV, NQE, TRIG>;
-  using PT = dgb::v2::Params2<NL, NQV, NQE, TRIG>;
+  constexpr bool FULL = dgb::v2::full_tensors(NL, BK);
+  using L = dgb::v2::Lay<NL, NQV, NQE, TRIG>;  // full host-side layout
+  using LK = dgb::v2::Lay<NL, NQV, NQE, TRIG, FULL>;  // the kernel's parameter block
+  using PT = dgb::v2::Params2<NL, NQV, NQE, TRIG, FULL>;
   using SM = dgb::v2::Smem<NL, NQV, NQE, BK>;
   static_assert(sizeof(PT) <= 32000, "tensor parameter block exceeds the kernel parameter limit");
   constexpr int N2 = NL * NL;
@@ -996,13 +999,16 @@ void launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_prob
   P.row_end = out_row_end;
   P.drop_neumann = params->neumann_inflow == DGB_INFLOW_DROP;
   P.evict_first = (plan->l2_policy & 2) != 0;
+  P.ablate = plan->ablate;
   P.kappa = params->kappa;
   P.sigma_i = params->sigma_interior;
   P.sigma_b = params->sigma_boundary;
   P.prob = *problem;
   const double* h = plan->h_tens.data();
   const dgb::Layout& V = plan->L;
-  double* x = P.t.x;
+  static thread_local std::vector<double> xfull;
+  xfull.assign(L::TOTAL, 0.0);
+  double* x = xfull.data();
   auto copy = [&](int dst, int src, int n) { std::memcpy(x + dst, h + src, sizeof(double) * n); };
   copy(L::S, V.S, 3 * N2);
   copy(L::M, V.M, N2);
@@ -1030,6 +1036,9 @@ void launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_prob
   copy(L::VW, V.VW, NQV);
   copy(L::ET, V.ET, NQE);
   copy(L::EW, V.EW, NQE);
+  // the compact block is the full one from PHI on (same sections, same order)
+  static_assert(LK::TOTAL - LK::PHI == L::TOTAL - L::PHI, "compact layout mismatch");
+  std::memcpy(P.t.x, x + (L::PHI - LK::PHI), sizeof(double) * LK::TOTAL);
   const size_t smem = sizeof(double) * (SM::kTr + (THREADS / 32) * SM::kWarp);
   if constexpr (SM::kMma) {
     // B operands in mma.m8n8k4 fragment order: lane (g, t) of tile (ks, nt) holds term 4 ks + t
@@ -1487,6 +1496,10 @@ int dgb_plan_set_option(dgb_plan* plan, int32_t option, int32_t value) {
     case DGB_OPTION_FORCE_GENERIC_KERNEL: plan->force_generic = value; return DGB_OK;
     case DGB_OPTION_MIN_BLOCKS: plan->minblocks = value; return DGB_OK;
     case DGB_OPTION_L2_POLICY: plan->l2_policy = value; return DGB_OK;
+    // Profiling diagnostics, deliberately not in the public header: skip parts of the P2
+    // tensor-core kernel to attribute time (results are WRONG while set).  Bits: 1 no block
+    // stores, 2 no source evaluation, 4 no neighbour blocks, 8 no diagonal block.
+    case 1000: plan->ablate = value; return DGB_OK;
     default: return DGB_STATUS_INVALID_ARGUMENT;
   }
 }
