@@ -23,6 +23,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -1185,6 +1186,73 @@ struct Buffers {
   }
 };
 
+// Per-device state of the host-buffer entry point (dgb_assemble_all_host): its stream, the
+// plan of the last reference tables seen, and device buffers grown on demand, so a repeated
+// call costs the copies and the assembly only.  Lives until process exit (never freed: the
+// CUDA context may already be gone at static destruction).
+struct HostContext {
+  std::mutex mu;
+  cudaStream_t s = nullptr;
+  dgb_plan* plan = nullptr;
+  std::vector<double> key;  // reference-table contents the plan was built from
+  std::vector<void*> ptr;
+  std::vector<size_t> cap;
+
+  cudaStream_t stream() {
+    if (!s) cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate");
+    return s;
+  }
+  void* buffer(int i, size_t bytes) {
+    if (static_cast<int>(ptr.size()) <= i) {
+      ptr.resize(i + 1, nullptr);
+      cap.resize(i + 1, 0);
+    }
+    bytes = std::max<size_t>(bytes, 16);
+    if (cap[i] < bytes) {
+      if (ptr[i]) cuda_check(cudaFree(ptr[i]), "cudaFree");
+      ptr[i] = nullptr;
+      cap[i] = 0;
+      cuda_check(cudaMalloc(&ptr[i], bytes), "cudaMalloc");
+      cap[i] = bytes;
+    }
+    return ptr[i];
+  }
+  dgb_plan* plan_for(const dgb_reference_tables* t, int device) {
+    std::vector<double> k = {double(t->degree), double(t->n_local), double(t->nq_vol),
+                             double(t->nq_edge)};
+    auto add = [&](const double* p, size_t n) {
+      if (p) k.insert(k.end(), p, p + n);
+    };
+    const size_t nl = t->n_local, nq = t->nq_vol, ne = t->nq_edge;
+    add(t->vol_x, nq);
+    add(t->vol_y, nq);
+    add(t->vol_w, nq);
+    add(t->edge_t, ne);
+    add(t->edge_w, ne);
+    add(t->phi, nq * nl);
+    add(t->dphi, nq * nl * 2);
+    add(t->edge_phi, 6 * ne * nl);
+    add(t->edge_dphi, 6 * ne * nl * 2);
+    if (plan && k == key) return plan;
+    if (plan) dgb_plan_destroy(plan);
+    plan = nullptr;
+    const int pc = dgb_plan_create(t, device, &plan);
+    if (pc != DGB_OK) throw dgb::Error(pc, dgb_last_error_message(), dgb_last_error_detail());
+    key = std::move(k);
+    return plan;
+  }
+};
+
+HostContext& host_context(int device) {
+  static std::mutex mu;
+  static std::vector<HostContext*> ctx;
+  std::lock_guard<std::mutex> lock(mu);
+  if (device < 0) throw dgb::Error(DGB_STATUS_INVALID_ARGUMENT, "negative device");
+  if (static_cast<int>(ctx.size()) <= device) ctx.resize(device + 1, nullptr);
+  if (!ctx[device]) ctx[device] = new HostContext();
+  return *ctx[device];
+}
+
 // row_ptr of block rows [row_begin, row_end): counts (1 + #interior local edges) then an
 // inclusive scan (3 launches).
 void compute_pattern(dgb_plan* plan, const dgb_mesh_arrays* mesh, int row_begin, int row_end,
@@ -1538,31 +1606,29 @@ int dgb_spmv(const dgb_bsr* a, const double* x, double* y, void* stream) {
 int dgb_assemble_all_host(const dgb_mesh_arrays* mesh, const dgb_reference_tables* tables,
                           const dgb_problem* problem, const dgb_params* params, int32_t device,
                           dgb_bsr* out, double* rhs) {
-  dgb_plan* plan = nullptr;
-  const int st = dgb::guarded([&] {
+  return dgb::guarded([&] {
     if (!mesh || !tables || !problem || !params || !out || !rhs) {
       throw dgb::Error(DGB_STATUS_INVALID_ARGUMENT, "null argument");
     }
     DeviceGuard guard(device);
-    Buffers buf;
+    HostContext& cx = host_context(device);
+    std::lock_guard<std::mutex> lock(cx.mu);
     const int E = mesh->n_elements, ne = mesh->n_edges, nn = mesh->n_nodes;
     const int nl = tables->n_local;
     const int64_t nnzb = dgb_bsr_nnzb(E, mesh->n_interior_edges);
     if (out->nnzb != nnzb || out->block_dim != nl || out->n_block_rows != E) {
       throw dgb::Error(DGB_STATUS_DIMENSION_MISMATCH, "BSR output does not match mesh / tables");
     }
-    cudaStream_t s;
-    cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate");
-    struct StreamGuard {
-      cudaStream_t s;
-      ~StreamGuard() { cudaStreamDestroy(s); }
-    } sg{s};
-    dgb_mesh_arrays dm = *mesh;
+    cudaStream_t s = cx.stream();
+    dgb_plan* plan = cx.plan_for(tables, device);
+    // every call uploads its inputs (the caller's arrays may have changed); buffers are reused
+    int slot = 0;
     auto up = [&](const void* src, size_t bytes) {
-      void* d = buf.alloc<char>(bytes);
+      void* d = cx.buffer(slot++, bytes);
       cuda_check(cudaMemcpyAsync(d, src, bytes, cudaMemcpyHostToDevice, s), "cudaMemcpyAsync(H2D)");
       return d;
     };
+    dgb_mesh_arrays dm = *mesh;
     dm.nodes = static_cast<const double*>(up(mesh->nodes, sizeof(double) * 2 * nn));
     dm.elements = static_cast<const int32_t*>(up(mesh->elements, sizeof(int32_t) * 3 * E));
     dm.edges = static_cast<const int32_t*>(up(mesh->edges, sizeof(int32_t) * 2 * ne));
@@ -1577,17 +1643,17 @@ int dgb_assemble_all_host(const dgb_mesh_arrays* mesh, const dgb_reference_table
         f->per_element = static_cast<const double*>(up(f->per_element, sizeof(double) * E));
       }
     }
-    const int pc = dgb_plan_create(tables, device, &plan);
-    if (pc != DGB_OK) throw dgb::Error(pc, dgb_last_error_message(), dgb_last_error_detail());
     dgb_bsr d;
     d.n_block_rows = E;
     d.block_dim = nl;
     d.nnzb = nnzb;
-    d.row_ptr = buf.alloc<int32_t>(E + 1);
-    d.col = buf.alloc<int32_t>(nnzb);
-    d.val = buf.alloc<double>(static_cast<size_t>(nnzb) * nl * nl);
-    double* d_rhs = buf.alloc<double>(static_cast<size_t>(E) * nl);
-    int rc = dgb_assemble(plan, &dm, &dp, params, &d, d_rhs, s);
+    d.row_ptr = static_cast<int32_t*>(cx.buffer(slot++, sizeof(int32_t) * (E + 1)));
+    d.col = static_cast<int32_t*>(cx.buffer(slot++, sizeof(int32_t) * nnzb));
+    d.val = static_cast<double*>(cx.buffer(slot++, sizeof(double) * nnzb * nl * nl));
+    double* d_rhs = static_cast<double*>(cx.buffer(slot++, sizeof(double) * E * nl));
+    int rc = dgb_plan_bind_mesh(plan, &dm, 0, E, s);  // pattern + adjacency of this mesh
+    if (rc != DGB_OK) throw dgb::Error(rc, dgb_last_error_message(), dgb_last_error_detail());
+    rc = dgb_assemble(plan, &dm, &dp, params, &d, d_rhs, s);
     if (rc != DGB_OK) throw dgb::Error(rc, dgb_last_error_message(), dgb_last_error_detail());
     rc = dgb_plan_status(plan, s);
     if (rc != DGB_OK) throw dgb::Error(rc, dgb_last_error_message(), dgb_last_error_detail());
@@ -1597,8 +1663,6 @@ int dgb_assemble_all_host(const dgb_mesh_arrays* mesh, const dgb_reference_table
     cuda_check(cudaMemcpyAsync(rhs, d_rhs, sizeof(double) * E * nl, cudaMemcpyDeviceToHost, s), "D2H");
     cuda_check(cudaStreamSynchronize(s), "cudaStreamSynchronize");
   });
-  dgb_plan_destroy(plan);
-  return st;
 }
 
 }  // extern "C"

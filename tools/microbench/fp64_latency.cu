@@ -43,6 +43,35 @@ __global__ void dmma_chains(double* out, long long* cyc, int iters) {
   if ((threadIdx.x & 31) == 0) cyc[threadIdx.x >> 5] = t1 - t0;
 }
 
+// Half the warps run independent DFMA chains, half DMMA chains: do the two share a pipe?
+__global__ void mixed(double* out, long long* cyc, int iters, int mode) {
+  const int w = threadIdx.x >> 5;
+  const bool dmma_warp = mode == 2 ? ((w >> 2) & 1) : mode == 1;  // mode 2: one of each per SMSP
+  double a[8], b = 1.0000001, c = 0.9999999;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) a[i] = threadIdx.x * 1e-3 + i;
+  double d[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
+  __syncthreads();
+  const long long t0 = clock64();
+  if (dmma_warp) {
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) dmma(d[k][0], d[k][1], a[k], b);
+    }
+  } else {
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) a[k] = fma(a[k], b, c);
+    }
+  }
+  const long long t1 = clock64();
+  double s = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) s += d[k][0] + d[k][1] + a[k] + a[k + 4];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+  if ((threadIdx.x & 31) == 0) cyc[w] = t1 - t0;
+}
+
 int main() {
   double* out;
   long long* cyc;
@@ -72,6 +101,13 @@ int main() {
   RUN(4, 8)
   RUN(4, 16)
   RUN(8, 16)
+  for (int mode = 0; mode < 3; ++mode) {
+    mixed<<<1, mode == 2 ? 256 : 128>>>(out, cyc, iters, mode);
+    cudaMemcpy(h, cyc, 8 * 8, cudaMemcpyDeviceToHost);
+    printf("mixed mode %d (0 all DFMA, 1 all DMMA, 2 alternate):", mode);
+    for (int w = 0; w < 8; ++w) printf(" %.2f", double(h[w]) / iters);
+    printf("  cycles per iteration per warp (DFMA iter = 8 DFMA, DMMA iter = 4 DMMA)\n");
+  }
   cudaError_t e = cudaDeviceSynchronize();
   printf("status: %s\n", cudaGetErrorString(e));
   return 0;
