@@ -333,6 +333,46 @@ int dgb_assemble_all_host(const dgb_mesh_arrays* mesh, const dgb_reference_table
                           const dgb_problem* problem, const dgb_params* params, int32_t device,
                           dgb_bsr* out, double* rhs);
 
+/* ---- Nonlinear reaction ------------------------------------------
+ * The reaction r(u) of `alpha u - div(eps grad u) + b.grad u + r(u) = f`
+ * (ProblemSpec::nonlinear_reaction, problems.hpp:38-41, 62).  std::function callbacks cannot
+ * run on the device, so the reference's reactions are enumerated with their exact
+ * expressions:
+ *   ZERO    r = 0,          r' = 0            (test_nonlinear.cpp zero_reaction)
+ *   LINEAR  r = u,          r' = 1            (test_nonlinear.cpp "linear reaction")
+ *   SQUARE  r = u * u,      r' = 2.0 * u      (problems.cpp:125-127, paper-boundary-layer)
+ *   CUBIC   r = u * u * u,  r' = 3.0 * u * u  (test_nonlinear.cpp cubic_reaction)       */
+enum {
+  DGB_REACTION_ZERO = 0,
+  DGB_REACTION_LINEAR = 1,
+  DGB_REACTION_SQUARE = 2,
+  DGB_REACTION_CUBIC = 3
+};
+
+typedef struct dgb_reaction {
+  int32_t kind;
+  int32_t pad_;
+} dgb_reaction;
+
+/* Replaces dgfem::assemble_nonlinear(coef, mesh, ref, reaction) (nonlinear.cpp:11-107):
+ *   H_i   = sum_q det w_q r(u_h(x_q)) phi_i(x_q)            -> h[n_elements * nl]
+ *   HJ_ij = sum_q det w_q r'(u_h(x_q)) phi_j phi_i           -> hj, block-diagonal BSR
+ * with u_h = sum_j coef[e*nl + j] phi_j.  HJ has one nl x nl block per element: on return
+ * hj->row_ptr[e] = e and hj->col[e] = e (the reference's CSR expands 1:1 from it).
+ * DEVICE pointers (mesh arrays, coef, h, hj arrays), asynchronous on `stream`.
+ * hj->n_block_rows must equal n_elements, hj->nnzb == n_elements, hj->block_dim == nl
+ * (else DGB_STATUS_DIMENSION_MISMATCH, like the reference's coefficient-length check).   */
+int dgb_assemble_nonlinear(dgb_plan* plan, const dgb_mesh_arrays* mesh, const double* coef,
+                           int64_t n_coef, const dgb_reaction* reaction, double* h,
+                           dgb_bsr* hj, void* stream);
+
+/* The same with HOST buffers in and out (synchronous): uploads mesh and coef, downloads H and
+ * HJ.  n_coef must equal n_elements * nl (DGB_STATUS_DIMENSION_MISMATCH otherwise). */
+int dgb_assemble_nonlinear_host(const dgb_mesh_arrays* mesh, const dgb_reference_tables* tables,
+                                const double* coef, int64_t n_coef,
+                                const dgb_reaction* reaction, int32_t device, double* h,
+                                dgb_bsr* hj);
+
 #ifdef __cplusplus
 } /* extern "C" */
 #endif

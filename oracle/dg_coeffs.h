@@ -129,4 +129,15 @@ static inline void dgc_vector(const dgb_vector_field* b, double x, double y, dou
   }
 }
 
+/* Nonlinear reaction r(u), r'(u) with the reference's expressions (dgb_reaction kinds:
+ * problems.cpp:125-127, test_nonlinear.cpp square / cubic / zero / linear reactions). */
+static inline void dgc_reaction(int kind, double u, double* r, double* dr) {
+  switch (kind) {
+    case DGB_REACTION_LINEAR: *r = u; *dr = 1.0; return;
+    case DGB_REACTION_SQUARE: *r = u * u; *dr = 2.0 * u; return;
+    case DGB_REACTION_CUBIC: *r = u * u * u; *dr = 3.0 * u * u; return;
+    default: *r = 0.0; *dr = 0.0; return;
+  }
+}
+
 #endif /* DG_COEFFS_H */

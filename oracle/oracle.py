@@ -124,6 +124,8 @@ class RefLib:
             "dgref_system_free": (None, [vp]),
             "dgref_element_geometry": (C.c_int, [vp, C.c_int, vp]),
             "dgref_edge_geometry": (C.c_int, [vp, C.c_int, vp]),
+            "dgref_assemble_nonlinear": (C.c_int, [vp, vp, vp, C.c_longlong, C.c_int, C.c_int,
+                                                   vp, vp, vp, vp, P(C.c_double)]),
         }
         for name, (res, args) in sig.items():
             f = getattr(lib, name)
@@ -175,6 +177,23 @@ class RefLib:
 
     def assemble_convection(self, mesh, ref, problem, threads: int = 0) -> None:
         self._check(self.lib.dgref_assemble_convection(mesh.h, ref.h, C.byref(problem), threads))
+
+    def assemble_nonlinear(self, mesh: "RefMesh", ref: "RefElement", coef: np.ndarray, kind: int,
+                           threads: int = 0):
+        """dgfem::assemble_nonlinear: returns (h, (row_offsets, cols, vals), seconds)."""
+        coef = np.ascontiguousarray(coef, dtype=np.float64)
+        nl = ref.tables["n_local"]
+        n = coef.shape[0]
+        ne = n // nl if nl else 0
+        h = np.zeros(n)
+        ro = np.zeros(n + 1, np.int32)
+        cols = np.zeros(ne * nl * nl, np.int32)
+        vals = np.zeros(ne * nl * nl)
+        secs = (C.c_double * 1)()
+        self._check(self.lib.dgref_assemble_nonlinear(mesh.h, ref.h, _ptr(coef), n, kind, threads,
+                                                      _ptr(h), _ptr(ro), _ptr(cols), _ptr(vals),
+                                                      secs))
+        return h, (ro, cols, vals), secs[0]
 
 
 class RefMesh:
@@ -267,7 +286,31 @@ class OracleLib:
                                      C.c_int32, vp, vp, vp, vp, C.POINTER(C.c_longlong)]
         lib.dgo_spmv.restype = None
         lib.dgo_spmv.argtypes = [vp, vp, vp, C.c_int32, C.c_int32, vp, vp, C.c_int32]
+        lib.dgo_assemble_nonlinear.restype = C.c_int
+        lib.dgo_assemble_nonlinear.argtypes = [C.POINTER(MeshArrays), C.POINTER(ReferenceTables),
+                                               vp, C.c_int64, C.c_int32, vp, C.c_int32, C.c_int32,
+                                               vp, vp]
         self.lib = lib
+
+    def assemble_nonlinear(self, mesh: dict, tables: dict, coef: np.ndarray, kind: int,
+                           rows: np.ndarray | None = None, threads: int = 0):
+        """H and the HJ blocks of elements `rows` (default all): (h [n, nl], hj [n, nl, nl])."""
+        m = mesh_arrays_from_numpy(mesh)
+        t = tables_view_from_numpy(tables)
+        nl = tables["n_local"]
+        coef = np.ascontiguousarray(coef, dtype=np.float64)
+        if threads <= 0:
+            threads = os.cpu_count() or 1
+        if rows is not None:
+            rows = np.ascontiguousarray(rows, dtype=np.int32)
+        n = mesh["elements"].shape[0] if rows is None else rows.shape[0]
+        h = np.zeros((n, nl))
+        hj = np.zeros((n, nl, nl))
+        st = self.lib.dgo_assemble_nonlinear(C.byref(m), C.byref(t), _ptr(coef), coef.shape[0],
+                                             kind, _ptr(rows), n, threads, _ptr(h), _ptr(hj))
+        if st != 0:
+            raise ReferenceError_(st, capi.STATUS_NAMES[st], -1)
+        return h, hj
 
     def assemble(self, mesh: dict, tables: dict, problem: Problem, params: Params,
                  rows: np.ndarray | None = None, threads: int = 0):

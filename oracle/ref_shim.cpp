@@ -21,6 +21,7 @@
 #include "dgfem/errors.hpp"
 #include "dgfem/execution.hpp"
 #include "dgfem/mesh.hpp"
+#include "dgfem/nonlinear.hpp"
 #include "dgfem/problems.hpp"
 #include "dgfem/reference.hpp"
 #include "dgfem/sparse.hpp"
@@ -507,6 +508,33 @@ int dgref_edge_geometry(void* mesh_handle, int edge, double* out) {
     const double v[6] = {g.length,     g.normal[0], g.normal[1], g.tangent[0],
                          g.tangent[1], static_cast<double>(g.oriented_from)};
     std::memcpy(out, v, sizeof v);
+  });
+}
+
+
+// dgfem::assemble_nonlinear (nonlinear.cpp:11-107) with the reaction of dgb_reaction `kind`
+// (host twin dgc_reaction, the reference's own expressions).  h[n]; the CSR of HJ into
+// row_offsets[n+1], cols[nnz], vals[nnz] (nnz = n_elements * nl * nl).  seconds[0] = wall time.
+int dgref_assemble_nonlinear(void* mesh_handle, void* ref_handle, const double* coef, long long n,
+                             int kind, int threads, double* h, int32_t* row_offsets, int32_t* cols,
+                             double* vals, double* seconds) {
+  return guarded([&] {
+    auto* mh = static_cast<MeshHandle*>(mesh_handle);
+    auto* rh = static_cast<RefHandle*>(ref_handle);
+    const dgfem::ReactionTerm reaction{
+        dgfem::scalar_map([kind](double u) { double r, dr; dgc_reaction(kind, u, &r, &dr); return r; }),
+        dgfem::scalar_map([kind](double u) { double r, dr; dgc_reaction(kind, u, &r, &dr); return dr; })};
+    const std::vector<double> c(coef, coef + n);
+    const dgfem::Execution exec =
+        threads == 1 ? dgfem::Execution::serial() : dgfem::Execution::parallel(threads);
+    const auto t0 = std::chrono::steady_clock::now();
+    auto [hv, hj] = dgfem::assemble_nonlinear(c, mh->mesh, rh->ref, reaction, exec);
+    const auto t1 = std::chrono::steady_clock::now();
+    if (seconds) seconds[0] = std::chrono::duration<double>(t1 - t0).count();
+    if (h) std::memcpy(h, hv.data(), hv.size() * sizeof(double));
+    if (row_offsets) std::memcpy(row_offsets, hj.row_offsets.data(), (hj.n + 1) * sizeof(int32_t));
+    if (cols) std::memcpy(cols, hj.col_indices.data(), hj.nnz() * sizeof(int32_t));
+    if (vals) std::memcpy(vals, hj.values.data(), hj.nnz() * sizeof(double));
   });
 }
 

@@ -86,6 +86,13 @@ class Bsr(C.Structure):
     ]
 
 
+class Reaction(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("pad_", C.c_int32)]
+
+
+REACTION_ZERO, REACTION_LINEAR, REACTION_SQUARE, REACTION_CUBIC = 0, 1, 2, 3
+
+
 def _declare(lib: C.CDLL) -> C.CDLL:
     P = C.POINTER
     vp = C.c_void_p
@@ -124,6 +131,10 @@ def _declare(lib: C.CDLL) -> C.CDLL:
         "dgb_count_blocks_host": (C.c_int64, [P(MeshArrays), C.c_int32, C.c_int32]),
         "dgb_assemble_all_host": (C.c_int, [P(MeshArrays), P(ReferenceTables), P(Problem),
                                             P(Params), C.c_int32, P(Bsr), vp]),
+        "dgb_assemble_nonlinear": (C.c_int, [vp, P(MeshArrays), vp, C.c_int64, P(Reaction), vp,
+                                             P(Bsr), vp]),
+        "dgb_assemble_nonlinear_host": (C.c_int, [P(MeshArrays), P(ReferenceTables), vp,
+                                                  C.c_int64, P(Reaction), C.c_int32, vp, P(Bsr)]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(lib, name)
@@ -140,6 +151,7 @@ EXPORTED_SYMBOLS = [
     "dgb_assemble", "dgb_plan_status", "dgb_plan_set_kernel_events",
     "dgb_plan_bind_mesh", "dgb_plan_unbind_mesh", "dgb_plan_launch_count", "dgb_plan_set_option", "dgb_spmv", "dgb_assemble_all_host",
     "dgb_mesh_rectangle", "dgb_assemble_rows", "dgb_count_blocks_host",
+    "dgb_assemble_nonlinear", "dgb_assemble_nonlinear_host",
 ]
 OPTION_FORCE_GENERIC_KERNEL = 1
 OPTION_MIN_BLOCKS = 2

@@ -292,6 +292,7 @@ constexpr int kGeo = 13;  // doubles per element: B(4) G(4) det ox oy eps alpha
 }  // namespace dgb
 
 #include "assemble_v2.cuh"
+#include "nonlinear.cuh"
 
 namespace dgb {
 
@@ -901,6 +902,9 @@ struct dgb_plan {
   // DMMA B fragments of the diagonal terms, one table per kappa (W depends on kappa)
   std::vector<std::pair<double, double*>> bfrag_cache;
   int ablate = 0;  // profiling diagnostics (dgb_plan_set_option 1000)
+  // nonlinear reaction Jacobian: Phi_q,(i,j) = phi_qj phi_qi as DMMA B fragments [ks][nt][lane]
+  double* d_nlfrag = nullptr;
+  int nl_ks = 0;
 };
 
 namespace {
@@ -1277,6 +1281,45 @@ void compute_pattern(dgb_plan* plan, const dgb_mesh_arrays* mesh, int row_begin,
              "DeviceScan");
 }
 
+// Nonlinear reaction (H, HJ): B fragments of Phi_q,(i,j) = phi_qj * phi_qi, built on first use.
+void nonlinear_frag(dgb_plan* plan, cudaStream_t s) {
+  if (plan->d_nlfrag) return;
+  const int nl = plan->nl, nq = plan->nqv, n2 = nl * nl;
+  const int ks = (nq + 3) / 4, nt = (n2 + 7) / 8;
+  std::vector<double> hb(static_cast<size_t>(ks) * nt * 32, 0.0);
+  const double* phi = plan->h_tens.data() + plan->L.PHI;
+  for (size_t idx = 0; idx < hb.size(); ++idx) {
+    const int ln = static_cast<int>(idx & 31), tile = static_cast<int>(idx >> 5);
+    const int k = 4 * (tile / nt) + (ln & 3), n = 8 * (tile % nt) + (ln >> 2);
+    if (k < nq && n < n2) {
+      const int i = n / nl, j = n % nl;
+      hb[idx] = phi[k * nl + j] * phi[k * nl + i];  // the reference's rounded product (nonlinear.cpp:61)
+    }
+  }
+  cuda_check(cudaMalloc(&plan->d_nlfrag, hb.size() * sizeof(double)), "cudaMalloc(nlfrag)");
+  cuda_check(cudaMemcpyAsync(plan->d_nlfrag, hb.data(), hb.size() * sizeof(double),
+                             cudaMemcpyHostToDevice, s), "cudaMemcpyAsync(nlfrag)");
+  cuda_check(cudaStreamSynchronize(s), "cudaStreamSynchronize(nlfrag)");
+  plan->nl_ks = ks;
+}
+
+template <int NL>
+void launch_nonlinear(const dgb::nlr::NlParams& P, cudaStream_t s) {
+  constexpr int kThreads = 128;
+  const size_t smem = sizeof(double) * (dgb::nlr::kMaxQ * NL + dgb::nlr::kMaxQ +
+                                        (kThreads / 32) * (dgb::nlr::kMaxQ * dgb::nlr::kCT + 32 * NL));
+  auto kernel = dgb::nlr::nonlinear_kernel<NL>;
+  static bool configured = false;
+  if (!configured) {
+    cuda_check(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(smem)), "cudaFuncSetAttribute(nonlinear)");
+    configured = true;
+  }
+  const int grid = (P.n_elements + kThreads - 1) / kThreads;
+  kernel<<<grid, kThreads, smem, s>>>(P);
+  cuda_check(cudaGetLastError(), "nonlinear_kernel");
+}
+
 }  // namespace
 
 extern "C" {
@@ -1427,6 +1470,7 @@ void dgb_plan_destroy(dgb_plan* p) {
   cudaFree(p->d_pattern);
   cudaFree(p->d_adj);
   for (auto& c : p->bfrag_cache) cudaFree(c.second);
+  cudaFree(p->d_nlfrag);
   if (prev >= 0) cudaSetDevice(prev);
   delete p;
 }
@@ -1661,6 +1705,110 @@ int dgb_assemble_all_host(const dgb_mesh_arrays* mesh, const dgb_reference_table
     cuda_check(cudaMemcpyAsync(out->col, d.col, sizeof(int32_t) * nnzb, cudaMemcpyDeviceToHost, s), "D2H");
     cuda_check(cudaMemcpyAsync(out->val, d.val, sizeof(double) * nnzb * nl * nl, cudaMemcpyDeviceToHost, s), "D2H");
     cuda_check(cudaMemcpyAsync(rhs, d_rhs, sizeof(double) * E * nl, cudaMemcpyDeviceToHost, s), "D2H");
+    cuda_check(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+  });
+}
+
+
+int dgb_assemble_nonlinear(dgb_plan* plan, const dgb_mesh_arrays* mesh, const double* coef,
+                           int64_t n_coef, const dgb_reaction* reaction, double* h,
+                           dgb_bsr* hj, void* stream) {
+  return dgb::guarded([&] {
+    if (!plan || !mesh || !reaction || !h || !hj) {
+      throw dgb::Error(DGB_STATUS_INVALID_ARGUMENT, "null argument");
+    }
+    const int E = mesh->n_elements, nl = plan->nl;
+    // the reference's own check (nonlinear.cpp:17-19)
+    if (n_coef != static_cast<int64_t>(E) * nl) {
+      throw dgb::Error(DGB_STATUS_DIMENSION_MISMATCH, "coefficient vector size mismatch");
+    }
+    if (hj->n_block_rows != E || hj->nnzb != E || hj->block_dim != nl) {
+      throw dgb::Error(DGB_STATUS_DIMENSION_MISMATCH, "HJ output is not the block diagonal of the mesh");
+    }
+    if (reaction->kind < DGB_REACTION_ZERO || reaction->kind > DGB_REACTION_CUBIC) {
+      throw dgb::Error(DGB_STATUS_INVALID_ARGUMENT, "unknown reaction kind", reaction->kind);
+    }
+    if (plan->nqv > dgb::nlr::kMaxQ) {
+      throw dgb::Error(DGB_STATUS_INVALID_ARGUMENT, "too many volume points", plan->nqv);
+    }
+    DeviceGuard guard(plan->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (E == 0) {
+      if (hj->row_ptr) cuda_check(cudaMemsetAsync(hj->row_ptr, 0, sizeof(int32_t), s), "cudaMemsetAsync");
+      return;
+    }
+    if (!coef || !mesh->nodes || !mesh->elements || !hj->row_ptr || !hj->col || !hj->val) {
+      throw dgb::Error(DGB_STATUS_INVALID_ARGUMENT, "null array");
+    }
+    nonlinear_frag(plan, s);
+    dgb::nlr::NlParams P;
+    P.nodes = mesh->nodes;
+    P.elements = mesh->elements;
+    P.coef = coef;
+    P.phi = plan->d_tens + plan->L.PHI;
+    P.w = plan->d_tens + plan->L.VW;
+    P.bfrag = plan->d_nlfrag;
+    P.h = h;
+    P.val = hj->val;
+    P.row_ptr = hj->row_ptr;
+    P.col = hj->col;
+    P.n_elements = E;
+    P.nq = plan->nqv;
+    P.ks = plan->nl_ks;
+    P.kind = reaction->kind;
+    switch (nl) {
+      case 1: launch_nonlinear<1>(P, s); break;
+      case 3: launch_nonlinear<3>(P, s); break;
+      case 6: launch_nonlinear<6>(P, s); break;
+      case 10: launch_nonlinear<10>(P, s); break;
+      case 15: launch_nonlinear<15>(P, s); break;
+      default: throw dgb::Error(DGB_STATUS_UNSUPPORTED_DEGREE, "unsupported n_local", nl);
+    }
+    plan->last_launches = 1;
+  });
+}
+
+int dgb_assemble_nonlinear_host(const dgb_mesh_arrays* mesh, const dgb_reference_tables* tables,
+                                const double* coef, int64_t n_coef,
+                                const dgb_reaction* reaction, int32_t device, double* h,
+                                dgb_bsr* hj) {
+  return dgb::guarded([&] {
+    if (!mesh || !tables || !reaction || !h || !hj) {
+      throw dgb::Error(DGB_STATUS_INVALID_ARGUMENT, "null argument");
+    }
+    const int E = mesh->n_elements, nl = tables->n_local, nn = mesh->n_nodes;
+    if (n_coef != static_cast<int64_t>(E) * nl) {
+      throw dgb::Error(DGB_STATUS_DIMENSION_MISMATCH, "coefficient vector size mismatch");
+    }
+    if (hj->n_block_rows != E || hj->nnzb != E || hj->block_dim != nl) {
+      throw dgb::Error(DGB_STATUS_DIMENSION_MISMATCH, "HJ output is not the block diagonal of the mesh");
+    }
+    DeviceGuard guard(device);
+    HostContext& cx = host_context(device);
+    std::lock_guard<std::mutex> lock(cx.mu);
+    cudaStream_t s = cx.stream();
+    dgb_plan* plan = cx.plan_for(tables, device);
+    int slot = 16;  // buffers of its own (the assembly entry point uses the low slots)
+    auto up = [&](const void* src, size_t bytes) {
+      void* d = cx.buffer(slot++, bytes);
+      cuda_check(cudaMemcpyAsync(d, src, bytes, cudaMemcpyHostToDevice, s), "cudaMemcpyAsync(H2D)");
+      return d;
+    };
+    dgb_mesh_arrays dm = *mesh;
+    dm.nodes = static_cast<const double*>(up(mesh->nodes, sizeof(double) * 2 * nn));
+    dm.elements = static_cast<const int32_t*>(up(mesh->elements, sizeof(int32_t) * 3 * E));
+    const double* dcoef = static_cast<const double*>(up(coef, sizeof(double) * n_coef));
+    dgb_bsr d = *hj;
+    d.row_ptr = static_cast<int32_t*>(cx.buffer(slot++, sizeof(int32_t) * (E + 1)));
+    d.col = static_cast<int32_t*>(cx.buffer(slot++, sizeof(int32_t) * E));
+    d.val = static_cast<double*>(cx.buffer(slot++, sizeof(double) * E * nl * nl));
+    double* dh = static_cast<double*>(cx.buffer(slot++, sizeof(double) * E * nl));
+    const int rc = dgb_assemble_nonlinear(plan, &dm, dcoef, n_coef, reaction, dh, &d, s);
+    if (rc != DGB_OK) throw dgb::Error(rc, dgb_last_error_message(), dgb_last_error_detail());
+    cuda_check(cudaMemcpyAsync(h, dh, sizeof(double) * E * nl, cudaMemcpyDeviceToHost, s), "D2H");
+    cuda_check(cudaMemcpyAsync(hj->row_ptr, d.row_ptr, sizeof(int32_t) * (E + 1), cudaMemcpyDeviceToHost, s), "D2H");
+    cuda_check(cudaMemcpyAsync(hj->col, d.col, sizeof(int32_t) * E, cudaMemcpyDeviceToHost, s), "D2H");
+    cuda_check(cudaMemcpyAsync(hj->val, d.val, sizeof(double) * E * nl * nl, cudaMemcpyDeviceToHost, s), "D2H");
     cuda_check(cudaStreamSynchronize(s), "cudaStreamSynchronize");
   });
 }

@@ -306,6 +306,30 @@ class Plan:
             _check(self._lib.dgb_plan_status(self._h, C.c_void_p(handle)))
         return out
 
+    def assemble_nonlinear(self, dmesh: DeviceMesh, coef, reaction: int, h=None, hj=None,
+                           stream=None):
+        """dgb_assemble_nonlinear on device tensors: H [E, nl] and the block-diagonal HJ
+        (BsrSystem with rhs=None) for `coef` [E * nl] and the reaction kind (capi.REACTION_*)."""
+        import torch
+        dev = torch.device("cuda", self.device)
+        nl, E = self.n_local, dmesh.n_elements
+        if stream is None:
+            stream = torch.cuda.current_stream(self.device)
+        handle = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+        if h is None:
+            h = torch.empty((E, nl), dtype=torch.float64, device=dev)
+        if hj is None:
+            hj = BsrSystem(torch.empty(E + 1, dtype=torch.int32, device=dev),
+                           torch.empty(E, dtype=torch.int32, device=dev),
+                           torch.empty((E, nl, nl), dtype=torch.float64, device=dev), None, nl)
+        r = capi.Reaction()
+        r.kind = reaction
+        b = hj.struct()
+        _check(self._lib.dgb_assemble_nonlinear(self._h, C.byref(dmesh.view), coef.data_ptr(),
+                                                coef.numel(), C.byref(r), h.data_ptr(),
+                                                C.byref(b), C.c_void_p(handle)))
+        return h, hj
+
     def spmv(self, system: BsrSystem, x, y, stream=None):
         import torch
         if stream is None:
@@ -352,3 +376,25 @@ def assemble_all_host(mesh: Mesh, tables: ReferenceTables, problem: ProblemSpec,
     _check(lib.dgb_assemble_all_host(C.byref(mesh.view), C.byref(tables), C.byref(problem.c),
                                      C.byref(params), device, C.byref(b), rhs.ctypes.data))
     return row_ptr, col, val, rhs
+
+
+def assemble_nonlinear(coef, mesh: Mesh, ref: ReferenceElement, reaction: int, device: int = 0):
+    """`dgfem::assemble_nonlinear(coef, mesh, ref, reaction)` (nonlinear.cpp:11-107) through
+    the host-buffer entry point: numpy in, (h [E*nl], (row_ptr, col, val [E, nl, nl])) out --
+    HJ as its block diagonal (BSR, one block per element)."""
+    lib = capi.load()
+    coef = np.ascontiguousarray(coef, dtype=np.float64)
+    nl, E = ref.n_local, mesh.n_elements
+    h = np.zeros(E * nl)
+    row_ptr = np.zeros(E + 1, np.int32)
+    col = np.zeros(E, np.int32)
+    val = np.zeros((E, nl, nl))
+    b = Bsr()
+    b.n_block_rows, b.block_dim, b.nnzb = E, nl, E
+    b.row_ptr, b.col, b.val = row_ptr.ctypes.data, col.ctypes.data, val.ctypes.data
+    r = capi.Reaction()
+    r.kind = reaction
+    _check(lib.dgb_assemble_nonlinear_host(C.byref(mesh.view), C.byref(ref.view), coef.ctypes.data,
+                                           coef.shape[0], C.byref(r), device, h.ctypes.data,
+                                           C.byref(b)))
+    return h, (row_ptr, col, val)

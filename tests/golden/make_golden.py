@@ -15,6 +15,10 @@ Outputs (numpy .npz, a few MB in total):
   meshes.npz   build_mesh inputs and outputs, plus the reference's error codes/details
   systems.npz  assembled K (CSR) and F for small meshes: every BASELINE config's
                coefficients, the registry problems the reference tests use, all methods
+  nonlinear.npz  assemble_nonlinear's H and HJ (CSR), degrees 1..4, every reaction kind,
+               seeded coefficients; plus the coefficient-length error
+
+    python tests/golden/make_golden.py [tables meshes systems nonlinear]   (default: all)
 """
 from __future__ import annotations
 
@@ -170,13 +174,58 @@ def systems(ref: RefLib) -> dict:
     return out
 
 
+REACTIONS = {"zero": capi.REACTION_ZERO, "linear": capi.REACTION_LINEAR,
+             "square": capi.REACTION_SQUARE, "cubic": capi.REACTION_CUBIC}
+
+
+def nonlinear(ref: RefLib) -> dict:
+    """assemble_nonlinear (nonlinear.cpp:11-107) on small meshes; coefficients U[-1, 1] from
+    splitmix64 (problems.uniform01) with the seed stored next to each case."""
+    out = {}
+    meshes_ = [("square4", dgfem.unit_square_mesh(4, 0.15, 3, True, 4, 0).raw()),
+               ("two_element", dict(mesh_cases())["two_element"])]
+    for mname, raw in meshes_:
+        mesh = ref.build_mesh(raw["nodes"], raw["elements"], raw["dirichlet"], raw["neumann"])
+        n_el = raw["elements"].shape[0]
+        for k in (1, 2, 3, 4):
+            for qo in (0, 2 * k + 1):
+                r = ref.reference(k, qo)
+                nl = r.tables["n_local"]
+                for rname, kind in REACTIONS.items():
+                    seed = 1000 * k + 10 * qo + kind
+                    coef = 2.0 * problems.uniform01(seed, n_el * nl) - 1.0
+                    h, (ro, ci, va), _ = ref.assemble_nonlinear(mesh, r, coef, kind, threads=1)
+                    name = f"{mname}_k{k}_q{qo}_{rname}"
+                    out[f"{name}/coef"] = coef
+                    out[f"{name}/seed"] = np.array(seed)
+                    out[f"{name}/degree"] = np.array(k)
+                    out[f"{name}/quad_order"] = np.array(qo)
+                    out[f"{name}/kind"] = np.array(kind)
+                    out[f"{name}/h"] = h
+                    out[f"{name}/row_offsets"] = ro
+                    out[f"{name}/cols"] = ci
+                    out[f"{name}/vals"] = va
+                    for kk, v in raw.items():
+                        out[f"{name}/in_{kk}"] = np.asarray(v)
+    # coefficient length check (test_nonlinear.cpp:55-65)
+    raw = dict(meshes_)["square4"]
+    mesh = ref.build_mesh(raw["nodes"], raw["elements"], raw["dirichlet"], raw["neumann"])
+    try:
+        ref.assemble_nonlinear(mesh, ref.reference(1, 0), np.zeros(7), capi.REACTION_SQUARE)
+        status = 0
+    except ReferenceError_ as e:
+        status = e.status
+    out["length_error/status"] = np.array(status)
+    return out
+
+
 def main():
     ref = RefLib()
-    np.savez_compressed(os.path.join(HERE, "tables.npz"), **tables(ref))
-    np.savez_compressed(os.path.join(HERE, "meshes.npz"), **meshes(ref))
-    np.savez_compressed(os.path.join(HERE, "systems.npz"), **systems(ref))
-    for f in ("tables.npz", "meshes.npz", "systems.npz"):
-        print(f, os.path.getsize(os.path.join(HERE, f)), "bytes")
+    which = sys.argv[1:] or ["tables", "meshes", "systems", "nonlinear"]
+    makers = {"tables": tables, "meshes": meshes, "systems": systems, "nonlinear": nonlinear}
+    for w in which:
+        np.savez_compressed(os.path.join(HERE, f"{w}.npz"), **makers[w](ref))
+        print(f"{w}.npz", os.path.getsize(os.path.join(HERE, f"{w}.npz")), "bytes")
 
 
 if __name__ == "__main__":
