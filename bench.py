@@ -2,6 +2,7 @@
 """Benchmark of the B200 DG system assembly (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C]
+    python bench.py --op nonlinear [...]   # H(u), HJ(u) assembly
 
 Workload (default): BASELINE.json configs[1] = config 2 -- the 256x256 unit-square mesh
 (131,072 triangles), P2, assembled with each of SIPG, NIPG and IIPG (sigma = 18).  One step =
@@ -23,6 +24,8 @@ import sys
 import threading
 import time
 
+import numpy as np
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -30,6 +33,8 @@ PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
 HBM_FALLBACK_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
 PROFILE_SUMMARY = os.path.join(ROOT, "profiles", "ncu_summary.json")
 METRIC = "DG system assembly elements/sec (fp64, 1 B200) and achieved HBM GB/s vs roofline"
+METRIC_NL = ("nonlinear reaction assembly H(u), HJ(u) elements/sec (fp64, 1 B200) and achieved "
+             "HBM GB/s vs roofline")
 
 
 def parse_args():
@@ -39,6 +44,9 @@ def parse_args():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--op", choices=["assembly", "nonlinear"], default="assembly",
+                    help="assembly: the headline (assemble_all + stiffness); nonlinear: "
+                         "assemble_nonlinear on the config's mesh and degree, r(u) = u^2")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
@@ -434,10 +442,229 @@ def run_reference(args, world, rank):
     print(json.dumps(line), flush=True)
 
 
+# ----------------------------------------------------------------------------- nonlinear op
+def nonlinear_bytes(mesh, nl: int) -> int:
+    """Every input read once, every output written once: reads 16 n_nodes + 12 E (elements)
+    + 8 nl E (coefficients); writes 8 nl E (H) + 8 nl^2 E (HJ blocks) + 4 E (block columns)
+    + 4 (E + 1) (row pointer)."""
+    E, nn = mesh.n_elements, mesh.n_nodes
+    return 16 * nn + 12 * E + 8 * nl * E + 8 * nl * E + 8 * nl * nl * E + 4 * E + 4 * (E + 1)
+
+
+def nonlinear_cpu_sample(cfg_index: int, n_sample: int, seconds: float):
+    """The reference's assemble_nonlinear (oracle/_ref, OpenMP on all cores), else the C
+    restatement, repeated on a bounded sample mesh for about `seconds`."""
+    from oracle import oracle as orc
+    from paper_1502_02941_b200 import capi, dgfem, problems
+    cfg = problems.CONFIGS[cfg_index]
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    mesh = dgfem.unit_square_mesh(n_sample, cfg.jitter, problems.SEED_JITTER, cfg.permute,
+                                  problems.SEED_PERMUTE, cfg.neumann_sides)
+    ref = dgfem.ReferenceElement(cfg.degree, cfg.quad_order)
+    coef = 2.0 * problems.uniform01(SEED_NL_COEF, mesh.n_elements * ref.n_local) - 1.0
+    elements, t_total = 0, 0.0
+    try:
+        lib = orc.RefLib()
+        raw = mesh.raw()
+        rmesh = lib.build_mesh(raw["nodes"], raw["elements"], raw["dirichlet"], raw["neumann"])
+        rref = lib.reference(cfg.degree, cfg.quad_order)
+        kind = "reference"
+        while True:
+            _, _, secs = lib.assemble_nonlinear(rmesh, rref, coef, capi.REACTION_SQUARE, threads=cores)
+            t_total += secs
+            elements += mesh.n_elements
+            if t_total >= seconds:
+                break
+    except FileNotFoundError:
+        ol = orc.OracleLib()
+        kind = "port"
+        arrays, tables = mesh.arrays(), ref.tables()
+        while True:
+            t0 = time.perf_counter()
+            ol.assemble_nonlinear(arrays, tables, coef, capi.REACTION_SQUARE, threads=cores)
+            t_total += time.perf_counter() - t0
+            elements += mesh.n_elements
+            if t_total >= seconds:
+                break
+    desc = (f"P{cfg.degree} on a {n_sample}x{n_sample} unit-square mesh ({mesh.n_elements} "
+            f"elements), r(u) = u^2, assemble_nonlinear x{elements // mesh.n_elements} in "
+            f"{t_total:.1f} s")
+    return elements / t_total, kind, cores, desc, t_total
+
+
+SEED_NL_COEF = 0x5EED00F1
+
+
+def run_nonlinear(args, world, rank, local):
+    """assemble_nonlinear (nonlinear.cpp:11-107) on config `--config`'s mesh and degree with
+    the registry's r(u) = u^2 (paper-boundary-layer) and seeded U[-1, 1] coefficients.  Each
+    rank runs its own config-sized mesh (the op is element-local: weak scaling, no
+    collective)."""
+    import ctypes as C
+
+    import torch
+    from paper_1502_02941_b200 import capi, dgfem, problems
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    lib = capi.load()
+    cfg = problems.CONFIGS[args.config]
+    mesh = dgfem.config_mesh(cfg)
+    ref = dgfem.ReferenceElement(cfg.degree, cfg.quad_order)
+    nl, E = ref.n_local, mesh.n_elements
+    coef_np = 2.0 * problems.uniform01(SEED_NL_COEF, E * nl) - 1.0
+    plan = dgfem.Plan(ref.view, local)
+    dm = dgfem.DeviceMesh(mesh, local)
+    coef = torch.from_numpy(coef_np).cuda(local)
+    stream = torch.cuda.current_stream(local)
+    h, hj = plan.assemble_nonlinear(dm, coef, capi.REACTION_SQUARE, stream=stream)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=f"cuda:{local}")
+
+    def step():
+        plan.assemble_nonlinear(dm, coef, capi.REACTION_SQUARE, h, hj, stream=stream)
+
+    for _ in range(args.warmup):
+        flush.fill_(1.0)
+        step()
+    torch.cuda.synchronize()
+    K = args.steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        for k in range(K):
+            flush.fill_(float(k))
+            ev[k][0].record(stream)
+            step()
+            ev[k][1].record(stream)
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = sum(step_ms)
+    if dist:
+        t = torch.tensor([total_ms], device=f"cuda:{local}", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms = total_ms / K
+    value = world * E * K / (total_ms / 1e3)
+    nbytes = nonlinear_bytes(mesh, nl)
+    achieved = nbytes / (ms / 1e3) / 1e9
+    peak, peak_kind = peak_hbm()
+    traffic = None
+    try:
+        with open(PROFILE_SUMMARY) as f:
+            traffic = json.load(f).get(f"nonlinear_config{args.config}", {}).get("dram_bytes_per_launch")
+    except Exception:
+        pass
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_kind,
+                "kernel": f"nonlinear_kernel<{nl}>", "kernel_ms": round(ms, 4),
+                "bytes_per_launch": nbytes, "kernel_share_of_step": 1.0}
+
+    e2e = None
+    if not args.no_e2e:
+        pin = {k: torch.from_numpy(np.ascontiguousarray(a)).pin_memory() for k, a in mesh.arrays().items()}
+        mv = capi.MeshArrays()
+        mv.n_nodes, mv.n_elements, mv.n_edges = mesh.n_nodes, E, mesh.n_edges
+        mv.n_interior_edges = mesh.n_interior_edges
+        for k2, t2 in pin.items():
+            setattr(mv, k2, t2.data_ptr())
+        pc = torch.from_numpy(coef_np).pin_memory()
+        ph = torch.empty(E * nl, dtype=torch.float64).pin_memory()
+        prp = torch.empty(E + 1, dtype=torch.int32).pin_memory()
+        pcol = torch.empty(E, dtype=torch.int32).pin_memory()
+        pval = torch.empty(E * nl * nl, dtype=torch.float64).pin_memory()
+        b = capi.Bsr()
+        b.n_block_rows, b.block_dim, b.nnzb = E, nl, E
+        b.row_ptr, b.col, b.val = prp.data_ptr(), pcol.data_ptr(), pval.data_ptr()
+        r = capi.Reaction()
+        r.kind = capi.REACTION_SQUARE
+
+        def host_call():
+            dgfem._check(lib.dgb_assemble_nonlinear_host(C.byref(mv), C.byref(ref.view), pc.data_ptr(),
+                                                         E * nl, C.byref(r), local, ph.data_ptr(), C.byref(b)))
+        host_call()
+        steps = max(2, min(K, 10))
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            host_call()
+        secs = time.perf_counter() - t0
+        if dist:
+            t = torch.tensor([secs], device=f"cuda:{local}", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            secs = float(t.item())
+        h2d = 16 * mesh.n_nodes + 12 * E + 4 * 2 * mesh.n_edges + mesh.n_edges + 8 * E * nl
+        e2e = {"value": round(world * E * steps / secs, 1), "unit": "elements/s",
+               "h2d_bytes_per_step": 16 * mesh.n_nodes + 12 * E + 8 * E * nl,
+               "d2h_bytes_per_step": 8 * E * nl + 4 * (E + 1) + 4 * E + 8 * E * nl * nl,
+               "steps": steps, "api": "dgb_assemble_nonlinear_host"}
+        del h2d
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, kind, cores, desc, _ = nonlinear_cpu_sample(args.config, 256, args.cpu_seconds)
+        cpu = {"value": round(v, 1), "unit": "elements/s", "cores": cores, "kind": kind, "sample": desc}
+    if dist:
+        dist.destroy_process_group()
+    if rank != 0:
+        return
+    line = {
+        "metric": METRIC_NL, "value": round(value, 1), "unit": "elements/s", "n_gpus": world,
+        "steps": K, "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded U[-1,1] coefficients on the config mesh; no dataset involved)",
+        "config": {"workload": f"assemble_nonlinear, r(u) = u^2, config {args.config} mesh "
+                               f"({cfg.n}x{cfg.n}, {E} triangles), P{cfg.degree}, nq_vol {ref.nq_vol}",
+                   "elements_per_step": world * E, "n_local": nl,
+                   "l2": "flushed between timed steps by a 256 MiB write (outside the timed events)",
+                   "parallelism": f"{world} rank(s), one config mesh each" if world > 1 else "1 GPU"},
+        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+        "gpu_launches": K * lib.dgb_plan_launch_count(plan._h),
+        "clocks": clocks.summary(),
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_reference_nonlinear(args, world, rank):
+    if rank != 0:
+        return
+    per_step = max(0.5, min(10.0, 120.0 / max(1, args.steps + args.warmup)))
+    for _ in range(args.warmup):
+        nonlinear_cpu_sample(args.config, 256, 0.0)
+    vals, secs_total, kind, cores, desc = [], 0.0, None, None, None
+    for _ in range(args.steps):
+        v, kind, cores, desc, secs = nonlinear_cpu_sample(args.config, 256, per_step)
+        vals.append(v)
+        secs_total += secs
+    value = statistics.fmean(vals)
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC_NL, "value": round(value, 1), "unit": "elements/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1e3 * secs_total / args.steps, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded U[-1,1] coefficients)",
+        "config": {"workload": f"assemble_nonlinear (bounded CPU sample: {desc})",
+                   "parallelism": f"OpenMP, {cores} host threads"},
+        "cpu_baseline": {"value": round(value, 1), "unit": "elements/s", "cores": cores,
+                         "kind": kind, "sample": desc},
+        "e2e": {"value": round(value, 1), "unit": "elements/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
 def main():
     args = parse_args()
     world, rank, local = dist_setup(args)
-    if args.impl == "reference":
+    if args.op == "nonlinear":
+        if args.impl == "reference":
+            run_reference_nonlinear(args, world, rank)
+        else:
+            run_nonlinear(args, world, rank, local)
+    elif args.impl == "reference":
         run_reference(args, world, rank)
     else:
         run_ours(args, world, rank, local)

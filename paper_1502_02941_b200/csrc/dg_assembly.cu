@@ -1306,14 +1306,15 @@ void nonlinear_frag(dgb_plan* plan, cudaStream_t s) {
 template <int NL>
 void launch_nonlinear(const dgb::nlr::NlParams& P, cudaStream_t s) {
   constexpr int kThreads = 128;
-  const size_t smem = sizeof(double) * (dgb::nlr::kMaxQ * NL + dgb::nlr::kMaxQ +
-                                        (kThreads / 32) * (dgb::nlr::kMaxQ * dgb::nlr::kCT + 32 * NL));
+  const size_t smem = sizeof(double) * (((P.nq * NL + 1) & ~1) + ((P.nq + 1) & ~1) +
+                                        (kThreads / 32) * (4 * P.ks * dgb::nlr::kCT + 32 * NL));
   auto kernel = dgb::nlr::nonlinear_kernel<NL>;
-  static bool configured = false;
-  if (!configured) {
+  static size_t configured = 0;
+  if (smem > configured) {  // raise the dynamic shared-memory limit once per size class
     cuda_check(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(smem)), "cudaFuncSetAttribute(nonlinear)");
-    configured = true;
+                                    static_cast<int>(std::max<size_t>(smem, 48 * 1024))),
+               "cudaFuncSetAttribute(nonlinear)");
+    configured = std::max<size_t>(smem, 48 * 1024);
   }
   const int grid = (P.n_elements + kThreads - 1) / kThreads;
   kernel<<<grid, kThreads, smem, s>>>(P);

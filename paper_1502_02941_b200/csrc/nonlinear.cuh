@@ -55,11 +55,12 @@ template <int NL>
 __global__ void __launch_bounds__(128) nonlinear_kernel(const __grid_constant__ NlParams P) {
   constexpr int N2 = NL * NL, NT = (N2 + 7) / 8;
   extern __shared__ double sm[];
-  double* sphi = sm;                        // [nq][NL]
-  double* sw = sphi + kMaxQ * NL;           // [nq]
+  const int kpad = 4 * P.ks;
+  double* sphi = sm;                                  // [nq][NL]
+  double* sw = sphi + ((P.nq * NL + 1) & ~1);         // [nq]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double* S = sw + kMaxQ + warp * (kMaxQ * kCT + 32 * NL);  // [k][kCT]
-  double* sh = S + kMaxQ * kCT;                              // [32][NL] packed H
+  double* S = sw + ((P.nq + 1) & ~1) + warp * (kpad * kCT + 32 * NL);  // [k][kCT]
+  double* sh = S + kpad * kCT;                                         // [32][NL] packed H
   for (int i = threadIdx.x; i < P.nq * NL; i += blockDim.x) sphi[i] = P.phi[i];
   for (int i = threadIdx.x; i < P.nq; i += blockDim.x) sw[i] = P.w[i];
   __syncthreads();
@@ -87,7 +88,6 @@ __global__ void __launch_bounds__(128) nonlinear_kernel(const __grid_constant__ 
     c[j] = __ldg(P.coef + static_cast<long long>(ee) * NL + j);
     H[j] = 0.0;
   }
-  const int kpad = 4 * P.ks;
 #pragma unroll 1
   for (int q = 0; q < kpad; ++q) {
     if (q >= P.nq) {  // zero K padding of the A operand
