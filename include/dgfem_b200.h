@@ -373,6 +373,67 @@ int dgb_assemble_nonlinear_host(const dgb_mesh_arrays* mesh, const dgb_reference
                                 const dgb_reaction* reaction, int32_t device, double* h,
                                 dgb_bsr* hj);
 
+/* ---- Solve of the assembled system and the Newton driver ----------
+ * The reference solves with Eigen's SparseLU (direct_solve, sparse.cpp:154-217).  Here the
+ * BSR system is solved on the device by restarted GMRES(m) with a block-Jacobi
+ * preconditioner (the inverses of the nl x nl diagonal blocks), accepted under the
+ * reference's own accuracy contract:
+ *     ||A x - b||_2 <= 1e-10 (||A||_F ||x||_2 + ||b||_2)      (sparse.cpp:201-214)
+ * and the same errors: DimensionMismatch, SingularMatrix (a zero pivot in a diagonal block;
+ * detail = the scalar row), SolveAccuracy (the bound is not met within max_iterations).  */
+typedef struct dgb_solve_options {
+  double tolerance_scale;  /* stop at tolerance_scale * the contract bound (default 0.1)   */
+  int32_t max_iterations;  /* total Krylov iterations (default 20000)                     */
+  int32_t restart;         /* GMRES(m) restart length m (default 60, <= 200)              */
+} dgb_solve_options;
+
+typedef struct dgb_solve_info { /* SolveInfo (sparse.hpp:55-59) + the Krylov counters      */
+  double defect_norm2;
+  double defect_norm_inf;
+  double bound;
+  int32_t iterations;
+  int32_t restarts;
+} dgb_solve_info;
+
+/* Fills the defaults above. */
+void dgb_solve_options_default(dgb_solve_options* opt);
+
+/* Replaces direct_solve(a, rhs, &info) (sparse.cpp:154-217): solves A x = b for the BSR `a`
+ * from dgb_assemble (DEVICE pointers; sorted block columns with a diagonal block in every
+ * row).  x (device, n = n_block_rows * block_dim) holds the initial guess on entry (zeros
+ * are fine) and the solution on return.  Synchronises `stream`.  opt may be NULL. */
+int dgb_solve(const dgb_bsr* a, const double* b, double* x, const dgb_solve_options* opt,
+              dgb_solve_info* info, void* stream);
+
+typedef struct dgb_newton_config { /* NewtonConfig (nonlinear.hpp:16-26)                   */
+  int32_t max_iterations;          /* 50                                                   */
+  int32_t use_legacy_check;        /* 0: legacy_check unset                                */
+  double residual_tolerance;       /* 1e-10 on ||Res||_2                                   */
+  double step_tolerance;           /* 1e-12 on ||w||_2                                     */
+  double legacy_check;             /* the bound on ||J w + Res||_2 when use_legacy_check    */
+} dgb_newton_config;
+
+typedef struct dgb_newton_report { /* NewtonReport (nonlinear.hpp:28-33)                   */
+  int32_t iterations;
+  int32_t converged;
+  double final_residual;
+  double* residual_history;        /* HOST array, capacity max_iterations (may be NULL)    */
+  int32_t linear_iterations;       /* Krylov iterations over all Newton steps              */
+  int32_t pad_;
+} dgb_newton_report;
+
+void dgb_newton_config_default(dgb_newton_config* cfg);
+
+/* Replaces newton_solve(system, mesh, ref, reaction, config, initial_guess)
+ * (nonlinear.cpp:109-176) for K = stiffness() and F of dgb_assemble (DEVICE pointers) on the
+ * mesh the plan was built for: J w = -Res, u <- u + w, Res = K u + H(u) - F, J = K + HJ(u),
+ * with the inner solves of dgb_solve.  coef (device, n) holds the initial guess (zeros = the
+ * reference's empty guess) and returns the iterate.  Synchronises `stream`. */
+int dgb_newton_solve(dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_bsr* k,
+                     const double* f, const dgb_reaction* reaction,
+                     const dgb_newton_config* config, const dgb_solve_options* inner,
+                     double* coef, dgb_newton_report* report, void* stream);
+
 #ifdef __cplusplus
 } /* extern "C" */
 #endif

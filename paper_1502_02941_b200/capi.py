@@ -93,6 +93,28 @@ class Reaction(C.Structure):
 REACTION_ZERO, REACTION_LINEAR, REACTION_SQUARE, REACTION_CUBIC = 0, 1, 2, 3
 
 
+class SolveOptions(C.Structure):
+    _fields_ = [("tolerance_scale", C.c_double), ("max_iterations", C.c_int32),
+                ("restart", C.c_int32)]
+
+
+class SolveInfo(C.Structure):
+    _fields_ = [("defect_norm2", C.c_double), ("defect_norm_inf", C.c_double),
+                ("bound", C.c_double), ("iterations", C.c_int32), ("restarts", C.c_int32)]
+
+
+class NewtonConfig(C.Structure):
+    _fields_ = [("max_iterations", C.c_int32), ("use_legacy_check", C.c_int32),
+                ("residual_tolerance", C.c_double), ("step_tolerance", C.c_double),
+                ("legacy_check", C.c_double)]
+
+
+class NewtonReport(C.Structure):
+    _fields_ = [("iterations", C.c_int32), ("converged", C.c_int32),
+                ("final_residual", C.c_double), ("residual_history", C.c_void_p),
+                ("linear_iterations", C.c_int32), ("pad_", C.c_int32)]
+
+
 def _declare(lib: C.CDLL) -> C.CDLL:
     P = C.POINTER
     vp = C.c_void_p
@@ -135,6 +157,11 @@ def _declare(lib: C.CDLL) -> C.CDLL:
                                              P(Bsr), vp]),
         "dgb_assemble_nonlinear_host": (C.c_int, [P(MeshArrays), P(ReferenceTables), vp,
                                                   C.c_int64, P(Reaction), C.c_int32, vp, P(Bsr)]),
+        "dgb_solve_options_default": (None, [P(SolveOptions)]),
+        "dgb_newton_config_default": (None, [P(NewtonConfig)]),
+        "dgb_solve": (C.c_int, [P(Bsr), vp, vp, P(SolveOptions), P(SolveInfo), vp]),
+        "dgb_newton_solve": (C.c_int, [vp, P(MeshArrays), P(Bsr), vp, P(Reaction), P(NewtonConfig),
+                                       P(SolveOptions), vp, P(NewtonReport), vp]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(lib, name)
@@ -152,6 +179,7 @@ EXPORTED_SYMBOLS = [
     "dgb_plan_bind_mesh", "dgb_plan_unbind_mesh", "dgb_plan_launch_count", "dgb_plan_set_option", "dgb_spmv", "dgb_assemble_all_host",
     "dgb_mesh_rectangle", "dgb_assemble_rows", "dgb_count_blocks_host",
     "dgb_assemble_nonlinear", "dgb_assemble_nonlinear_host",
+    "dgb_solve_options_default", "dgb_newton_config_default", "dgb_solve", "dgb_newton_solve",
 ]
 OPTION_FORCE_GENERIC_KERNEL = 1
 OPTION_MIN_BLOCKS = 2

@@ -398,3 +398,82 @@ def assemble_nonlinear(coef, mesh: Mesh, ref: ReferenceElement, reaction: int, d
                                            coef.shape[0], C.byref(r), device, h.ctypes.data,
                                            C.byref(b)))
     return h, (row_ptr, col, val)
+
+
+def _stream_handle(device: int, stream=None) -> int:
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream(device)
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def solve_options(tolerance_scale: float | None = None, max_iterations: int | None = None,
+                  restart: int | None = None) -> "capi.SolveOptions":
+    o = capi.SolveOptions()
+    capi.load().dgb_solve_options_default(C.byref(o))
+    if tolerance_scale is not None:
+        o.tolerance_scale = tolerance_scale
+    if max_iterations is not None:
+        o.max_iterations = max_iterations
+    if restart is not None:
+        o.restart = restart
+    return o
+
+
+def solve(system: BsrSystem, b, x=None, options=None, device: int = 0, stream=None):
+    """`direct_solve(stiffness(), b, &info)` (sparse.cpp:154-217) on the device: block-Jacobi
+    GMRES(m) under the reference's accuracy contract.  b, x: device tensors [n] (x = initial
+    guess, zeros by default).  Returns (x, info dict); raises Error(SingularMatrix /
+    SolveAccuracy / DimensionMismatch) like the reference."""
+    import torch
+    lib = capi.load()
+    n = (system.row_ptr.shape[0] - 1) * system.block_dim
+    if b.numel() != n:
+        raise Error(capi.STATUS_NAMES.index("DimensionMismatch"), "right-hand side size mismatch", -1)
+    if x is None:
+        x = torch.zeros(n, dtype=torch.float64, device=b.device)
+    info = capi.SolveInfo()
+    bs = system.struct()
+    _check(lib.dgb_solve(C.byref(bs), b.data_ptr(), x.data_ptr(),
+                         C.byref(options) if options is not None else None, C.byref(info),
+                         C.c_void_p(_stream_handle(device, stream))))
+    return x, {"defect_norm2": info.defect_norm2, "defect_norm_inf": info.defect_norm_inf,
+               "bound": info.bound, "iterations": info.iterations, "restarts": info.restarts}
+
+
+def newton_config(max_iterations: int = 50, residual_tolerance: float = 1e-10,
+                  step_tolerance: float = 1e-12, legacy_check: float | None = None):
+    c = capi.NewtonConfig()
+    c.max_iterations, c.residual_tolerance, c.step_tolerance = max_iterations, residual_tolerance, step_tolerance
+    c.use_legacy_check = int(legacy_check is not None)
+    c.legacy_check = legacy_check if legacy_check is not None else 0.0
+    return c
+
+
+def newton_solve(plan: Plan, dmesh: DeviceMesh, system: BsrSystem, reaction: int, config=None,
+                 initial_guess=None, options=None, stream=None):
+    """`newton_solve(system, mesh, ref, reaction, config, initial_guess)`
+    (nonlinear.cpp:109-176) on the device.  Returns (coef tensor, report dict)."""
+    import torch
+    lib = capi.load()
+    n = dmesh.n_elements * plan.n_local
+    cfg = config if config is not None else newton_config()
+    if initial_guess is None:
+        coef = torch.zeros(n, dtype=torch.float64, device=system.val.device)
+    else:
+        coef = initial_guess.clone()
+    hist = np.zeros(max(cfg.max_iterations, 1))
+    rep = capi.NewtonReport()
+    rep.residual_history = hist.ctypes.data
+    r = capi.Reaction()
+    r.kind = reaction
+    bs = system.struct()
+    _check(lib.dgb_newton_solve(plan._h, C.byref(dmesh.view), C.byref(bs),
+                                system.rhs.data_ptr(), C.byref(r), C.byref(cfg),
+                                C.byref(options) if options is not None else None,
+                                coef.data_ptr(), C.byref(rep),
+                                C.c_void_p(_stream_handle(plan.device, stream))))
+    return coef, {"iterations": rep.iterations, "converged": bool(rep.converged),
+                  "final_residual": rep.final_residual,
+                  "residual_history": hist[:rep.iterations].tolist(),
+                  "linear_iterations": rep.linear_iterations}

@@ -1,0 +1,142 @@
+"""GPU: dgb_solve (block-Jacobi GMRES under direct_solve's accuracy contract, sparse.cpp:154-217)
+and dgb_newton_solve (nonlinear.cpp:109-176) against the numpy/SuperLU restatement
+(oracle/newton.py) and the reference's own tests of this layer.  SURVEY.md §8(f) rank 2."""
+import numpy as np
+import pytest
+
+from oracle import newton as onewton
+from oracle.oracle import OracleLib, bsr_to_csr
+from paper_1502_02941_b200 import capi, dgfem, problems
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def orc():
+    return OracleLib()
+
+
+def device_system(mesh, degree, spec, params, quad_order=0):
+    ref = dgfem.ReferenceElement(degree, quad_order)
+    plan = dgfem.Plan(ref.view)
+    dm, dp = dgfem.DeviceMesh(mesh), dgfem.DeviceProblem(spec)
+    out = plan.assemble(dm, dp, params, plan.allocate(dm))
+    return ref, plan, dm, out
+
+
+def host_csr(out):
+    rp, col, val = out.row_ptr.cpu().numpy(), out.col.cpu().numpy(), out.val.cpu().numpy()
+    return bsr_to_csr(rp, col, val), out.rhs.cpu().numpy().reshape(-1)
+
+
+@pytest.mark.parametrize("case", ["config1", "config2_small", "smooth-sine_k3", "layer_k2"])
+def test_solve_matches_direct_solution(case):
+    if case == "config1":
+        cfg = problems.CONFIGS[1]
+        mesh = dgfem.config_mesh(cfg)
+        spec = problems.config_problem(1)
+        params = dgfem.config_parameters(cfg, capi.SIPG)
+        degree, qo = cfg.degree, cfg.quad_order
+    elif case == "config2_small":
+        cfg = problems.CONFIGS[2]
+        mesh = dgfem.unit_square_mesh(24)
+        spec = problems.config_problem(2)
+        params = dgfem.config_parameters(cfg, capi.NIPG)
+        degree, qo = cfg.degree, cfg.quad_order
+    elif case == "smooth-sine_k3":
+        spec = problems.registry_get("smooth-sine")
+        mesh = dgfem.unit_square_mesh(8, 0.2, 3, True, 4)
+        params = dgfem.set_parameters(capi.IIPG, 3)
+        degree, qo = 3, 0
+    else:
+        spec = problems.registry_get("paper-boundary-layer-linear")
+        mesh = dgfem.unit_square_mesh(12)
+        params = dgfem.set_parameters(capi.SIPG, 2)
+        degree, qo = 2, 0
+    ref, plan, dm, out = device_system(mesh, degree, spec, params, qo)
+    # the reference's acceptance contract with the default (production) tolerance
+    x, info = dgfem.solve(out, out.rhs.reshape(-1))
+    assert info["defect_norm2"] <= info["bound"]
+    # tightened: converges to the direct solution
+    x2, info2 = dgfem.solve(out, out.rhs.reshape(-1), options=dgfem.solve_options(tolerance_scale=1e-4))
+    (ro, ci, va), F = host_csr(out)
+    xr, _ = onewton.direct_solve(ro, ci, va, F)
+    err = np.abs(x2.cpu().numpy() - xr).max() / max(1.0, np.abs(xr).max())
+    assert err <= 1e-8, err
+    assert info2["iterations"] >= info["iterations"]
+
+
+def test_solve_is_deterministic():
+    cfg = problems.CONFIGS[1]
+    mesh = dgfem.config_mesh(cfg)
+    ref, plan, dm, out = device_system(mesh, 1, problems.config_problem(1),
+                                       dgfem.config_parameters(cfg, capi.SIPG), cfg.quad_order)
+    a, _ = dgfem.solve(out, out.rhs.reshape(-1))
+    b, _ = dgfem.solve(out, out.rhs.reshape(-1))
+    assert bool((a == b).all())
+
+
+def test_singular_block_raises():
+    import torch
+    cfg = problems.CONFIGS[1]
+    mesh = dgfem.unit_square_mesh(4)
+    ref, plan, dm, out = device_system(mesh, 1, problems.config_problem(1),
+                                       dgfem.config_parameters(cfg, capi.SIPG))
+    rp, col = out.row_ptr.cpu().numpy(), out.col.cpu().numpy()
+    e = 5
+    diag = [b for b in range(rp[e], rp[e + 1]) if col[b] == e][0]
+    out.val[diag].zero_()
+    torch.cuda.synchronize()
+    with pytest.raises(dgfem.Error) as ex:
+        dgfem.solve(out, out.rhs.reshape(-1))
+    assert ex.value.code == "SingularMatrix"
+    assert ex.value.detail == e * ref.n_local
+
+
+def test_rhs_length_mismatch():
+    import torch
+    mesh = dgfem.unit_square_mesh(4)
+    ref, plan, dm, out = device_system(mesh, 1, problems.config_problem(1),
+                                       dgfem.config_parameters(problems.CONFIGS[1], capi.SIPG))
+    with pytest.raises(dgfem.Error) as ex:
+        dgfem.solve(out, torch.zeros(7, dtype=torch.float64, device="cuda"))
+    assert ex.value.code == "DimensionMismatch"
+
+
+def newton_case(orc, name, degree, n, kind, scale=1.0):
+    spec = problems.registry_get(name)
+    mesh = dgfem.unit_square_mesh(n, 0.0, 0, False, 0, spec.neumann_sides)
+    ref, plan, dm, out = device_system(mesh, degree, spec, dgfem.set_parameters(capi.SIPG, degree))
+    if scale != 1.0:
+        out.rhs.mul_(scale)
+    coef, rep = dgfem.newton_solve(plan, dm, out, kind,
+                                   options=dgfem.solve_options(tolerance_scale=1e-4))
+    K, F = host_csr(out)
+    c_ref, rep_ref = onewton.newton_solve(K, F, mesh.arrays(), ref.tables(), kind, orc)
+    return coef.cpu().numpy(), rep, c_ref, rep_ref
+
+
+def test_newton_linear_problem_one_step(orc):
+    """test_nonlinear.cpp:164-182."""
+    c, rep, c_ref, rep_ref = newton_case(orc, "smooth-sine", 1, 4, capi.REACTION_ZERO)
+    assert rep["iterations"] == 1 and rep["converged"] and rep["final_residual"] <= 1e-10
+    assert np.all(np.abs(c - c_ref) <= 1e-10 * np.maximum(1.0, np.abs(c_ref)))
+
+
+def test_newton_layer_problem_matches_restatement(orc):
+    """test_nonlinear.cpp:184-199 with the linear variant's data and r(u) = u^2."""
+    c, rep, c_ref, rep_ref = newton_case(orc, "paper-boundary-layer-linear", 1, 8,
+                                         capi.REACTION_SQUARE)
+    assert rep["converged"] and rep["iterations"] <= 50 and rep["final_residual"] <= 1e-10
+    assert rep["iterations"] == rep_ref["iterations"]
+    assert np.abs(c - c_ref).max() <= 1e-8 * max(1.0, np.abs(c_ref).max())
+
+
+def test_newton_cubic_matches_restatement(orc):
+    c, rep, c_ref, rep_ref = newton_case(orc, "smooth-sine", 2, 6, capi.REACTION_CUBIC, 10.0)
+    assert rep["converged"]
+    assert rep["iterations"] == rep_ref["iterations"]
+    h, hr = np.array(rep["residual_history"]), np.array(rep_ref["residual_history"])
+    # relative agreement down to the rounding floor of the residual (1e-12 of the first one)
+    assert np.all(np.abs(h - hr) <= 1e-6 * hr + 1e-12 * hr[0])
+    assert np.abs(c - c_ref).max() <= 1e-8 * max(1.0, np.abs(c_ref).max())
