@@ -44,9 +44,10 @@ def parse_args():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", type=int, default=2)
-    ap.add_argument("--op", choices=["assembly", "nonlinear"], default="assembly",
+    ap.add_argument("--op", choices=["assembly", "nonlinear", "solve"], default="assembly",
                     help="assembly: the headline (assemble_all + stiffness); nonlinear: "
-                         "assemble_nonlinear on the config's mesh and degree, r(u) = u^2")
+                         "assemble_nonlinear on the config's mesh and degree, r(u) = u^2; "
+                         "solve: K x = F of the config's SIPG system (block-Jacobi GMRES)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
@@ -656,9 +657,138 @@ def run_reference_nonlinear(args, world, rank):
     }), flush=True)
 
 
+# ----------------------------------------------------------------------------- solve op
+METRIC_SOLVE = "linear solve of the assembled DG system K x = F: unknowns/sec (fp64, 1 B200)"
+
+
+def solve_bytes(E: int, nl: int, nnzb: int, iterations: int, restart: int) -> int:
+    """Modeled bytes of a block-Jacobi GMRES(m) solve, every operand read / written once per
+    use: per Arnoldi step with k previous basis vectors -- SpMV (values, indices, x, y),
+    block-Jacobi apply (inverse blocks, in, out), CGS2 (two passes of k+1 dots and a
+    (k+1)-term update) and the normalisation."""
+    n = E * nl
+    spmv = 8 * nl * nl * nnzb + 4 * nnzb + 4 * (E + 1) + 16 * n
+    prec = 8 * nl * nl * E + 16 * n
+    total = 0
+    for j in range(iterations):
+        k = j % restart
+        cgs = 2 * ((k + 2) * 8 * n + (k + 1) * 8 * n + 16 * n)
+        total += spmv + prec + cgs + 3 * 8 * n
+    return total
+
+
+def solve_cpu_sample(cfg_index: int, n_sample: int, seconds: float):
+    """The reference's direct solve restated (oracle/newton.py: SuperLU standing in for Eigen's
+    SparseLU, single-threaded) on a bounded sample of the config's system."""
+    from oracle import newton as onewton
+    from oracle.oracle import OracleLib, bsr_to_csr
+    from paper_1502_02941_b200 import capi, dgfem, problems
+    cfg = problems.CONFIGS[cfg_index]
+    mesh = dgfem.unit_square_mesh(n_sample, cfg.jitter, problems.SEED_JITTER, cfg.permute,
+                                  problems.SEED_PERMUTE, cfg.neumann_sides)
+    spec = problems.config_problem(cfg_index, mesh.n_elements)
+    tables = dgfem.ReferenceElement(cfg.degree, cfg.quad_order).tables()
+    rp, col, val, rhs = OracleLib().assemble(mesh.arrays(), tables, spec.c,
+                                             dgfem.config_parameters(cfg, capi.SIPG))
+    ro, ci, va = bsr_to_csr(rp, col, val)
+    F = rhs.reshape(-1)
+    unknowns, t_total = 0, 0.0
+    while True:
+        t0 = time.perf_counter()
+        onewton.direct_solve(ro, ci, va, F)
+        t_total += time.perf_counter() - t0
+        unknowns += F.size
+        if t_total >= seconds:
+            break
+    desc = (f"SuperLU (stand-in for Eigen SparseLU, absent here) on the config {cfg_index} SIPG "
+            f"system of a {n_sample}x{n_sample} mesh ({F.size} unknowns), "
+            f"{unknowns // F.size} solves in {t_total:.1f} s")
+    return unknowns / t_total, "port", 1, desc, t_total
+
+
+def run_solve(args, world, rank, local):
+    import torch
+    from paper_1502_02941_b200 import capi, dgfem, problems
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    lib = capi.load()
+    cfg = problems.CONFIGS[args.config]
+    mesh = dgfem.config_mesh(cfg)
+    spec = problems.config_problem(args.config, mesh.n_elements)
+    ref = dgfem.ReferenceElement(cfg.degree, cfg.quad_order)
+    plan = dgfem.Plan(ref.view, local)
+    dm, dp = dgfem.DeviceMesh(mesh, local), dgfem.DeviceProblem(spec, local)
+    out = plan.assemble(dm, dp, dgfem.config_parameters(cfg, capi.SIPG), plan.allocate(dm))
+    b = out.rhs.reshape(-1)
+    n = b.numel()
+    opts = dgfem.solve_options()
+    for _ in range(args.warmup):
+        dgfem.solve(out, b, options=opts, device=local)
+    torch.cuda.synchronize()
+    K = args.steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    stream = torch.cuda.current_stream(local)
+    infos = []
+    if dist:
+        dist.barrier()
+    with ClockSampler(local) as clocks:
+        for k in range(K):
+            ev[k][0].record(stream)
+            _, info = dgfem.solve(out, b, options=opts, device=local)   # synchronises
+            ev[k][1].record(stream)
+            infos.append(info)
+        torch.cuda.synchronize()
+    total_ms = sum(a.elapsed_time(bb) for a, bb in ev)
+    if dist:
+        t = torch.tensor([total_ms], device=f"cuda:{local}", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms = total_ms / K
+    value = world * n * K / (total_ms / 1e3)
+    its = infos[-1]["iterations"]
+    nbytes = solve_bytes(mesh.n_elements, ref.n_local, out.col.shape[0], its, opts.restart)
+    peak, peak_kind = peak_hbm()
+    achieved = nbytes / (ms / 1e3) / 1e9
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, kind, cores, desc, _ = solve_cpu_sample(args.config, {1: 32, 2: 48, 3: 16, 4: 128, 5: 16}[args.config],
+                                                   args.cpu_seconds)
+        cpu = {"value": round(v, 1), "unit": "unknowns/s", "cores": cores, "kind": kind, "sample": desc}
+    if dist:
+        dist.destroy_process_group()
+    if rank != 0:
+        return
+    print(json.dumps({
+        "metric": METRIC_SOLVE, "value": round(value, 1), "unit": "unknowns/s", "n_gpus": world,
+        "steps": K, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (the config's seeded SIPG system; no dataset involved)",
+        "config": {"workload": f"dgb_solve of config {args.config}'s SIPG system ({n} unknowns, "
+                               f"P{cfg.degree}), block-Jacobi GMRES({opts.restart}), accepted under "
+                               "direct_solve's bound 1e-10 (||A||_F ||x|| + ||b||)",
+                   "iterations": its, "restarts": infos[-1]["restarts"],
+                   "defect_norm2": infos[-1]["defect_norm2"], "bound": infos[-1]["bound"],
+                   "parallelism": "1 GPU" if world == 1 else f"{world} independent replicas"},
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": None, "peak_source": peak_kind,
+                     "kernel": "whole solve (modeled bytes: SpMV + block-Jacobi + CGS2 per step)",
+                     "kernel_ms": round(ms, 3), "bytes_per_launch": nbytes},
+        "cpu_baseline": cpu,
+        "e2e": None,
+        "gpu_launches": None,
+        "clocks": clocks.summary(),
+    }), flush=True)
+
+
 def main():
     args = parse_args()
     world, rank, local = dist_setup(args)
+    if args.op == "solve":
+        run_solve(args, world, rank, local)
+        return
     if args.op == "nonlinear":
         if args.impl == "reference":
             run_reference_nonlinear(args, world, rank)
