@@ -434,6 +434,35 @@ int dgb_newton_solve(dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_bsr*
                      const dgb_newton_config* config, const dgb_solve_options* inner,
                      double* coef, dgb_newton_report* report, void* stream);
 
+/* ---- Postprocessing --------------------------------------------- */
+
+/* The quadrature order l2_error integrates with for ReferenceElement(degree, quad_order):
+ * max(2k + 3, volume_rule().degree + 1) (postprocess.cpp:22-23; rule degrees as
+ * triangle_rule, quadrature.cpp:46-154).  Create the plan for dgb_l2_error from
+ * dgb_reference_create(degree, dgb_l2_quad_order(degree, quad_order)). */
+int32_t dgb_l2_quad_order(int32_t degree, int32_t quad_order);
+
+/* Replaces l2_error(coef, mesh, ref, exact) (postprocess.cpp:14-50): out[0] = ||u_h - u||_L2,
+ * out[1] = max_element_diameter(mesh) (mesh.cpp:259-265).  `plan` carries the sharper rule
+ * (dgb_l2_quad_order); exact = the exact solution's value as a scalar field.  DEVICE mesh
+ * and coef, HOST out[2]; synchronises `stream`.  n_coef != n_elements * nl ->
+ * DGB_STATUS_DIMENSION_MISMATCH. */
+int dgb_l2_error(dgb_plan* plan, const dgb_mesh_arrays* mesh, const double* coef, int64_t n_coef,
+                 const dgb_scalar_field* exact, double* out, void* stream);
+
+/* Replaces project(mesh, ref, f) (postprocess.cpp:56-81): coef[e*nl + j] =
+ * sum_q w_q f(x_q) phi_qj with the plan's volume rule.  DEVICE pointers, asynchronous. */
+int dgb_project(dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_scalar_field* f,
+                double* coef, void* stream);
+
+/* Replaces eval_solution(coef, ref, element, xhat, yhat) (postprocess.cpp:83-93) for a batch
+ * of n points: values[i] = u_h(element[i]; xhat[i], yhat[i]).  DEVICE pointers; synchronises
+ * `stream`.  An element outside [0, n_elements) -> DGB_STATUS_INVALID_INDEX, detail = the
+ * first offending point. */
+int dgb_eval_solution(const double* coef, int32_t degree, int32_t n_elements, int64_t n,
+                      const int32_t* elements, const double* xhat, const double* yhat,
+                      double* values, void* stream);
+
 #ifdef __cplusplus
 } /* extern "C" */
 #endif

@@ -126,6 +126,9 @@ class RefLib:
             "dgref_edge_geometry": (C.c_int, [vp, C.c_int, vp]),
             "dgref_assemble_nonlinear": (C.c_int, [vp, vp, vp, C.c_longlong, C.c_int, C.c_int,
                                                    vp, vp, vp, vp, P(C.c_double)]),
+            "dgref_l2_error": (C.c_int, [vp, vp, vp, C.c_longlong, vp, vp]),
+            "dgref_project": (C.c_int, [vp, vp, vp, vp]),
+            "dgref_eval_solution": (C.c_int, [vp, C.c_longlong, vp, C.c_longlong, vp, vp, vp, vp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(lib, name)
@@ -177,6 +180,28 @@ class RefLib:
 
     def assemble_convection(self, mesh, ref, problem, threads: int = 0) -> None:
         self._check(self.lib.dgref_assemble_convection(mesh.h, ref.h, C.byref(problem), threads))
+
+    def l2_error(self, mesh: "RefMesh", ref: "RefElement", coef: np.ndarray, exact) -> tuple:
+        coef = np.ascontiguousarray(coef, dtype=np.float64)
+        out = np.zeros(2)
+        self._check(self.lib.dgref_l2_error(mesh.h, ref.h, _ptr(coef), coef.shape[0],
+                                            C.byref(exact), _ptr(out)))
+        return float(out[0]), float(out[1])
+
+    def project(self, mesh: "RefMesh", ref: "RefElement", f, n_elements: int) -> np.ndarray:
+        out = np.zeros(n_elements * ref.tables["n_local"])
+        self._check(self.lib.dgref_project(mesh.h, ref.h, C.byref(f), _ptr(out)))
+        return out
+
+    def eval_solution(self, coef, ref: "RefElement", elements, xh, yh) -> np.ndarray:
+        coef = np.ascontiguousarray(coef, dtype=np.float64)
+        elements = np.ascontiguousarray(elements, dtype=np.int32)
+        xh = np.ascontiguousarray(xh, dtype=np.float64)
+        yh = np.ascontiguousarray(yh, dtype=np.float64)
+        out = np.zeros(elements.shape[0])
+        self._check(self.lib.dgref_eval_solution(_ptr(coef), coef.shape[0], ref.h, elements.shape[0],
+                                                 _ptr(elements), _ptr(xh), _ptr(yh), _ptr(out)))
+        return out
 
     def assemble_nonlinear(self, mesh: "RefMesh", ref: "RefElement", coef: np.ndarray, kind: int,
                            threads: int = 0):
@@ -290,7 +315,43 @@ class OracleLib:
         lib.dgo_assemble_nonlinear.argtypes = [C.POINTER(MeshArrays), C.POINTER(ReferenceTables),
                                                vp, C.c_int64, C.c_int32, vp, C.c_int32, C.c_int32,
                                                vp, vp]
+        lib.dgo_l2_error.restype = C.c_int
+        lib.dgo_l2_error.argtypes = [C.POINTER(MeshArrays), C.POINTER(ReferenceTables), vp, C.c_int64,
+                                     vp, vp]
+        lib.dgo_project.restype = C.c_int
+        lib.dgo_project.argtypes = [C.POINTER(MeshArrays), C.POINTER(ReferenceTables), vp, vp]
+        lib.dgo_eval_solution.restype = C.c_int
+        lib.dgo_eval_solution.argtypes = [vp, C.c_int32, C.c_int64, vp, vp, vp, vp]
         self.lib = lib
+
+    def l2_error(self, mesh: dict, sharp_tables: dict, coef, exact) -> tuple:
+        """postprocess.cpp:14-50 with the sharper rule's tables (see dgb_l2_quad_order)."""
+        m = mesh_arrays_from_numpy(mesh)
+        t = tables_view_from_numpy(sharp_tables)
+        coef = np.ascontiguousarray(coef, dtype=np.float64)
+        out = np.zeros(2)
+        st = self.lib.dgo_l2_error(C.byref(m), C.byref(t), _ptr(coef), coef.shape[0],
+                                   C.addressof(exact), _ptr(out))
+        if st != 0:
+            raise ReferenceError_(st, capi.STATUS_NAMES[st], -1)
+        return float(out[0]), float(out[1])
+
+    def project(self, mesh: dict, tables: dict, f) -> np.ndarray:
+        m = mesh_arrays_from_numpy(mesh)
+        t = tables_view_from_numpy(tables)
+        out = np.zeros(mesh["elements"].shape[0] * tables["n_local"])
+        self.lib.dgo_project(C.byref(m), C.byref(t), C.addressof(f), _ptr(out))
+        return out
+
+    def eval_solution(self, coef, degree: int, elements, xh, yh) -> np.ndarray:
+        coef = np.ascontiguousarray(coef, dtype=np.float64)
+        elements = np.ascontiguousarray(elements, dtype=np.int32)
+        xh = np.ascontiguousarray(xh, dtype=np.float64)
+        yh = np.ascontiguousarray(yh, dtype=np.float64)
+        out = np.zeros(elements.shape[0])
+        self.lib.dgo_eval_solution(_ptr(coef), degree, elements.shape[0], _ptr(elements),
+                                   _ptr(xh), _ptr(yh), _ptr(out))
+        return out
 
     def assemble_nonlinear(self, mesh: dict, tables: dict, coef: np.ndarray, kind: int,
                            rows: np.ndarray | None = None, threads: int = 0):

@@ -22,6 +22,7 @@
 #include "dgfem/execution.hpp"
 #include "dgfem/mesh.hpp"
 #include "dgfem/nonlinear.hpp"
+#include "dgfem/postprocess.hpp"
 #include "dgfem/problems.hpp"
 #include "dgfem/reference.hpp"
 #include "dgfem/sparse.hpp"
@@ -535,6 +536,46 @@ int dgref_assemble_nonlinear(void* mesh_handle, void* ref_handle, const double* 
     if (row_offsets) std::memcpy(row_offsets, hj.row_offsets.data(), (hj.n + 1) * sizeof(int32_t));
     if (cols) std::memcpy(cols, hj.col_indices.data(), hj.nnz() * sizeof(int32_t));
     if (vals) std::memcpy(vals, hj.values.data(), hj.nnz() * sizeof(double));
+  });
+}
+
+
+// dgfem::l2_error (postprocess.cpp:14-50): out[0] = L2 error, out[1] = max element diameter.
+int dgref_l2_error(void* mesh_handle, void* ref_handle, const double* coef, long long n,
+                   const dgb_scalar_field* exact, double* out) {
+  return guarded([&] {
+    auto* mh = static_cast<MeshHandle*>(mesh_handle);
+    auto* rh = static_cast<RefHandle*>(ref_handle);
+    std::shared_ptr<Locator> loc;
+    dgfem::ExactSolution ex;
+    ex.value = scalar_field_from(*exact, mh->mesh, loc);
+    ex.du_dx = ex.value;
+    ex.du_dy = ex.value;
+    const std::vector<double> c(coef, coef + n);
+    const auto [err, h] = dgfem::l2_error(c, mh->mesh, rh->ref, ex);
+    out[0] = err;
+    out[1] = h;
+  });
+}
+
+// dgfem::project (postprocess.cpp:56-81) into out[n_elements * nl].
+int dgref_project(void* mesh_handle, void* ref_handle, const dgb_scalar_field* f, double* out) {
+  return guarded([&] {
+    auto* mh = static_cast<MeshHandle*>(mesh_handle);
+    auto* rh = static_cast<RefHandle*>(ref_handle);
+    std::shared_ptr<Locator> loc;
+    const std::vector<double> c = dgfem::project(mh->mesh, rh->ref, scalar_field_from(*f, mh->mesh, loc));
+    std::memcpy(out, c.data(), c.size() * sizeof(double));
+  });
+}
+
+// dgfem::eval_solution (postprocess.cpp:83-93) at n points.
+int dgref_eval_solution(const double* coef, long long n_coef, void* ref_handle, long long n,
+                        const int32_t* elements, const double* xh, const double* yh, double* out) {
+  return guarded([&] {
+    auto* rh = static_cast<RefHandle*>(ref_handle);
+    const std::vector<double> c(coef, coef + n_coef);
+    for (long long i = 0; i < n; ++i) out[i] = dgfem::eval_solution(c, rh->ref, elements[i], xh[i], yh[i]);
   });
 }
 

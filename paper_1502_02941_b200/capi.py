@@ -157,6 +157,10 @@ def _declare(lib: C.CDLL) -> C.CDLL:
                                              P(Bsr), vp]),
         "dgb_assemble_nonlinear_host": (C.c_int, [P(MeshArrays), P(ReferenceTables), vp,
                                                   C.c_int64, P(Reaction), C.c_int32, vp, P(Bsr)]),
+        "dgb_l2_quad_order": (C.c_int32, [C.c_int32, C.c_int32]),
+        "dgb_l2_error": (C.c_int, [vp, P(MeshArrays), vp, C.c_int64, P(ScalarField), vp, vp]),
+        "dgb_project": (C.c_int, [vp, P(MeshArrays), P(ScalarField), vp, vp]),
+        "dgb_eval_solution": (C.c_int, [vp, C.c_int32, C.c_int32, C.c_int64, vp, vp, vp, vp, vp]),
         "dgb_solve_options_default": (None, [P(SolveOptions)]),
         "dgb_newton_config_default": (None, [P(NewtonConfig)]),
         "dgb_solve": (C.c_int, [P(Bsr), vp, vp, P(SolveOptions), P(SolveInfo), vp]),
@@ -180,6 +184,7 @@ EXPORTED_SYMBOLS = [
     "dgb_mesh_rectangle", "dgb_assemble_rows", "dgb_count_blocks_host",
     "dgb_assemble_nonlinear", "dgb_assemble_nonlinear_host",
     "dgb_solve_options_default", "dgb_newton_config_default", "dgb_solve", "dgb_newton_solve",
+    "dgb_l2_quad_order", "dgb_l2_error", "dgb_project", "dgb_eval_solution",
 ]
 OPTION_FORCE_GENERIC_KERNEL = 1
 OPTION_MIN_BLOCKS = 2

@@ -293,6 +293,7 @@ constexpr int kGeo = 13;  // doubles per element: B(4) G(4) det ox oy eps alpha
 
 #include "assemble_v2.cuh"
 #include "nonlinear.cuh"
+#include "postprocess.cuh"
 
 namespace dgb {
 
@@ -1811,6 +1812,132 @@ int dgb_assemble_nonlinear_host(const dgb_mesh_arrays* mesh, const dgb_reference
     cuda_check(cudaMemcpyAsync(hj->col, d.col, sizeof(int32_t) * E, cudaMemcpyDeviceToHost, s), "D2H");
     cuda_check(cudaMemcpyAsync(hj->val, d.val, sizeof(double) * E * nl * nl, cudaMemcpyDeviceToHost, s), "D2H");
     cuda_check(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+  });
+}
+
+
+int32_t dgb_l2_quad_order(int32_t degree, int32_t quad_order) {
+  auto rule_degree = [](int q) {  // triangle_rule's delivered degree (quadrature.cpp:46-154)
+    if (q <= 1) return 1;
+    if (q == 3) return 4;
+    if (q == 7) return 8;
+    return q;
+  };
+  const int vol = quad_order > 0 ? quad_order : 2 * degree + 2;
+  return std::max(2 * degree + 3, rule_degree(vol) + 1);
+}
+
+int dgb_l2_error(dgb_plan* plan, const dgb_mesh_arrays* mesh, const double* coef, int64_t n_coef,
+                 const dgb_scalar_field* exact, double* out, void* stream) {
+  return dgb::guarded([&] {
+    if (!plan || !mesh || !exact || !out) throw dgb::Error(DGB_STATUS_INVALID_ARGUMENT, "null argument");
+    const int E = mesh->n_elements, nl = plan->nl;
+    if (n_coef != static_cast<int64_t>(E) * nl) {
+      throw dgb::Error(DGB_STATUS_DIMENSION_MISMATCH, "coefficient vector size mismatch");
+    }
+    validate_field(*exact, false, "exact");
+    if (exact->kind == DGB_FIELD_PER_ELEMENT) {
+      throw dgb::Error(DGB_STATUS_INVALID_ARGUMENT, "exact: a point field is required");
+    }
+    DeviceGuard guard(plan->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    out[0] = out[1] = 0.0;
+    if (E == 0) return;
+    dgb::post::PostParams P{};
+    P.nodes = mesh->nodes;
+    P.elements = mesh->elements;
+    P.coef = coef;
+    P.phi = plan->d_tens + plan->L.PHI;
+    P.vx = plan->d_tens + plan->L.VX;
+    P.vy = plan->d_tens + plan->L.VY;
+    P.vw = plan->d_tens + plan->L.VW;
+    P.field = *exact;
+    P.n_elements = E;
+    P.nq = plan->nqv;
+    const int nb = (E + dgb::post::kThreads - 1) / dgb::post::kThreads;
+    Buffers buf;
+    double* partial = buf.alloc<double>(2 * static_cast<size_t>(nb) + 2);
+    P.out = partial;
+    switch (nl) {
+      case 3: dgb::post::l2_error_kernel<3><<<nb, dgb::post::kThreads, 0, s>>>(P); break;
+      case 6: dgb::post::l2_error_kernel<6><<<nb, dgb::post::kThreads, 0, s>>>(P); break;
+      case 10: dgb::post::l2_error_kernel<10><<<nb, dgb::post::kThreads, 0, s>>>(P); break;
+      case 15: dgb::post::l2_error_kernel<15><<<nb, dgb::post::kThreads, 0, s>>>(P); break;
+      default: throw dgb::Error(DGB_STATUS_UNSUPPORTED_DEGREE, "unsupported n_local", nl);
+    }
+    dgb::post::l2_finish_kernel<<<1, dgb::post::kThreads, 0, s>>>(partial, nb, partial + 2 * nb);
+    cuda_check(cudaGetLastError(), "l2_error_kernel");
+    double h[2];
+    cuda_check(cudaMemcpyAsync(h, partial + 2 * nb, sizeof h, cudaMemcpyDeviceToHost, s), "D2H(l2)");
+    cuda_check(cudaStreamSynchronize(s), "cudaStreamSynchronize(l2)");
+    out[0] = std::sqrt(h[0]);
+    out[1] = h[1];
+  });
+}
+
+int dgb_project(dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_scalar_field* f,
+                double* coef, void* stream) {
+  return dgb::guarded([&] {
+    if (!plan || !mesh || !f || !coef) throw dgb::Error(DGB_STATUS_INVALID_ARGUMENT, "null argument");
+    validate_field(*f, false, "field");
+    if (f->kind == DGB_FIELD_PER_ELEMENT) {
+      throw dgb::Error(DGB_STATUS_INVALID_ARGUMENT, "field: a point field is required");
+    }
+    DeviceGuard guard(plan->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int E = mesh->n_elements;
+    if (E == 0) return;
+    dgb::post::PostParams P{};
+    P.nodes = mesh->nodes;
+    P.elements = mesh->elements;
+    P.phi = plan->d_tens + plan->L.PHI;
+    P.vx = plan->d_tens + plan->L.VX;
+    P.vy = plan->d_tens + plan->L.VY;
+    P.vw = plan->d_tens + plan->L.VW;
+    P.field = *f;
+    P.out = coef;
+    P.n_elements = E;
+    P.nq = plan->nqv;
+    const int nb = (E + dgb::post::kThreads - 1) / dgb::post::kThreads;
+    switch (plan->nl) {
+      case 3: dgb::post::project_kernel<3><<<nb, dgb::post::kThreads, 0, s>>>(P); break;
+      case 6: dgb::post::project_kernel<6><<<nb, dgb::post::kThreads, 0, s>>>(P); break;
+      case 10: dgb::post::project_kernel<10><<<nb, dgb::post::kThreads, 0, s>>>(P); break;
+      case 15: dgb::post::project_kernel<15><<<nb, dgb::post::kThreads, 0, s>>>(P); break;
+      default: throw dgb::Error(DGB_STATUS_UNSUPPORTED_DEGREE, "unsupported n_local", plan->nl);
+    }
+    cuda_check(cudaGetLastError(), "project_kernel");
+  });
+}
+
+int dgb_eval_solution(const double* coef, int32_t degree, int32_t n_elements, int64_t n,
+                      const int32_t* elements, const double* xhat, const double* yhat,
+                      double* values, void* stream) {
+  return dgb::guarded([&] {
+    if (degree < 1 || degree > 4) {
+      throw dgb::Error(DGB_STATUS_UNSUPPORTED_DEGREE, "polynomial degree must be between 1 and 4", degree);
+    }
+    if (n < 0) throw dgb::Error(DGB_STATUS_INVALID_ARGUMENT, "negative point count");
+    if (n == 0) return;
+    if (!coef || !elements || !xhat || !yhat || !values) {
+      throw dgb::Error(DGB_STATUS_INVALID_ARGUMENT, "null argument");
+    }
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    Buffers buf;
+    unsigned long long* bad = buf.alloc<unsigned long long>(1);
+    cuda_check(cudaMemsetAsync(bad, 0xFF, sizeof(unsigned long long), s), "memset");
+    const unsigned nb = static_cast<unsigned>((n + dgb::post::kThreads - 1) / dgb::post::kThreads);
+    switch (degree) {
+      case 1: dgb::post::eval_kernel<1><<<nb, dgb::post::kThreads, 0, s>>>(coef, n_elements, n, elements, xhat, yhat, values, bad); break;
+      case 2: dgb::post::eval_kernel<2><<<nb, dgb::post::kThreads, 0, s>>>(coef, n_elements, n, elements, xhat, yhat, values, bad); break;
+      case 3: dgb::post::eval_kernel<3><<<nb, dgb::post::kThreads, 0, s>>>(coef, n_elements, n, elements, xhat, yhat, values, bad); break;
+      default: dgb::post::eval_kernel<4><<<nb, dgb::post::kThreads, 0, s>>>(coef, n_elements, n, elements, xhat, yhat, values, bad); break;
+    }
+    cuda_check(cudaGetLastError(), "eval_kernel");
+    unsigned long long hb = 0;
+    cuda_check(cudaMemcpyAsync(&hb, bad, sizeof hb, cudaMemcpyDeviceToHost, s), "D2H(eval)");
+    cuda_check(cudaStreamSynchronize(s), "cudaStreamSynchronize(eval)");
+    if (hb != ~0ull) throw dgb::Error(DGB_STATUS_INVALID_INDEX, "element index out of range", static_cast<long long>(hb));
   });
 }
 

@@ -146,6 +146,7 @@ class ReferenceElement:
         h = C.c_void_p()
         _check(self._lib.dgb_reference_create(degree, quad_order, C.byref(h)))
         self._h = h
+        self.quad_order = quad_order
         v = ReferenceTables()
         _check(self._lib.dgb_reference_view(h, C.byref(v)))
         self.view = v
@@ -477,3 +478,42 @@ def newton_solve(plan: Plan, dmesh: DeviceMesh, system: BsrSystem, reaction: int
                   "final_residual": rep.final_residual,
                   "residual_history": hist[:rep.iterations].tolist(),
                   "linear_iterations": rep.linear_iterations}
+
+
+# ------------------------------------------------------------------------------ postprocess
+def l2_error(coef, dmesh: DeviceMesh, ref: ReferenceElement, exact, device: int = 0, stream=None):
+    """`l2_error(coef, mesh, ref, exact)` (postprocess.cpp:14-50) on the device: coef a device
+    tensor [E * nl], exact a ScalarField descriptor (capi.ScalarField, e.g. problems.function).
+    Returns (error, h_max)."""
+    lib = capi.load()
+    sharp = ReferenceElement(ref.degree, lib.dgb_l2_quad_order(ref.degree, ref.quad_order))
+    plan = Plan(sharp.view, device)
+    out = (C.c_double * 2)()
+    _check(lib.dgb_l2_error(plan._h, C.byref(dmesh.view), coef.data_ptr(), coef.numel(),
+                            C.byref(exact), out, C.c_void_p(_stream_handle(device, stream))))
+    return out[0], out[1]
+
+
+def project(dmesh: DeviceMesh, ref: ReferenceElement, f, device: int = 0, stream=None):
+    """`project(mesh, ref, f)` (postprocess.cpp:56-81): device tensor [E * nl]."""
+    import torch
+    lib = capi.load()
+    plan = Plan(ref.view, device)
+    coef = torch.empty(dmesh.n_elements * ref.n_local, dtype=torch.float64,
+                       device=torch.device("cuda", device))
+    _check(lib.dgb_project(plan._h, C.byref(dmesh.view), C.byref(f), coef.data_ptr(),
+                           C.c_void_p(_stream_handle(device, stream))))
+    return coef
+
+
+def eval_solution(coef, ref: ReferenceElement, elements, xhat, yhat, device: int = 0, stream=None):
+    """`eval_solution(coef, ref, element, xhat, yhat)` (postprocess.cpp:83-93) for a batch of
+    points (device tensors); returns a device tensor of values."""
+    import torch
+    lib = capi.load()
+    n = elements.numel()
+    out = torch.empty(n, dtype=torch.float64, device=coef.device)
+    _check(lib.dgb_eval_solution(coef.data_ptr(), ref.degree, coef.numel() // ref.n_local, n,
+                                 elements.data_ptr(), xhat.data_ptr(), yhat.data_ptr(),
+                                 out.data_ptr(), C.c_void_p(_stream_handle(device, stream))))
+    return out

@@ -17,6 +17,7 @@ Outputs (numpy .npz, a few MB in total):
                coefficients, the registry problems the reference tests use, all methods
   nonlinear.npz  assemble_nonlinear's H and HJ (CSR), degrees 1..4, every reaction kind,
                seeded coefficients; plus the coefficient-length error
+  postprocess.npz  l2_error, project and eval_solution, degrees 1..4
 
     python tests/golden/make_golden.py [tables meshes systems nonlinear]   (default: all)
 """
@@ -219,10 +220,37 @@ def nonlinear(ref: RefLib) -> dict:
     return out
 
 
+def postprocess(ref: RefLib) -> dict:
+    """l2_error / project / eval_solution (postprocess.cpp:14-93) of the reference on a jittered
+    permuted 6x6 mesh, degrees 1..4, seeded coefficients and points."""
+    out = {}
+    m = dgfem.unit_square_mesh(6, 0.2, 8, True, 9)
+    raw = m.raw()
+    rmesh = ref.build_mesh(raw["nodes"], raw["elements"], raw["dirichlet"], raw["neumann"])
+    for kk, v in raw.items():
+        out[f"in_{kk}"] = np.asarray(v)
+    exact = problems.function(capi.FN_SIN_SIN, (1.0,))
+    f = problems.function(capi.FN_GAUSSIAN, (50.0, 0.5, 0.5))
+    for k in (1, 2, 3, 4):
+        rref = ref.reference(k, 0)
+        nl = rref.tables["n_local"]
+        coef = 2.0 * problems.uniform01(31 + k, m.n_elements * nl) - 1.0
+        rng = np.random.default_rng(k)
+        el = rng.integers(0, m.n_elements, 64).astype(np.int32)
+        xh, yh = rng.random(64) * 0.5, rng.random(64) * 0.5
+        out[f"k{k}/coef"] = coef
+        out[f"k{k}/l2"] = np.array(ref.l2_error(rmesh, rref, coef, exact))
+        out[f"k{k}/project"] = ref.project(rmesh, rref, f, m.n_elements)
+        out[f"k{k}/el"], out[f"k{k}/xh"], out[f"k{k}/yh"] = el, xh, yh
+        out[f"k{k}/eval"] = ref.eval_solution(coef, rref, el, xh, yh)
+    return out
+
+
 def main():
     ref = RefLib()
-    which = sys.argv[1:] or ["tables", "meshes", "systems", "nonlinear"]
-    makers = {"tables": tables, "meshes": meshes, "systems": systems, "nonlinear": nonlinear}
+    which = sys.argv[1:] or ["tables", "meshes", "systems", "nonlinear", "postprocess"]
+    makers = {"tables": tables, "meshes": meshes, "systems": systems, "nonlinear": nonlinear,
+              "postprocess": postprocess}
     for w in which:
         np.savez_compressed(os.path.join(HERE, f"{w}.npz"), **makers[w](ref))
         print(f"{w}.npz", os.path.getsize(os.path.join(HERE, f"{w}.npz")), "bytes")
