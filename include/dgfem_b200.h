@@ -463,6 +463,32 @@ int dgb_eval_solution(const double* coef, int32_t degree, int32_t n_elements, in
                       const int32_t* elements, const double* xhat, const double* yhat,
                       double* values, void* stream);
 
+/* ---- Mesh topology on the device -------------------------------- */
+typedef struct dgb_device_mesh dgb_device_mesh;
+
+/* Replaces build_mesh(nodes, elements, dirichlet, neumann) (mesh.cpp:51-151) on `device`:
+ * the same validation (InvalidTopology / DegenerateElement / NonManifold /
+ * InvalidBoundarySpec with the reference's details), CCW reorientation, lexicographic edge
+ * numbering, edge_elements, element_edges and edge kinds -- bit-identical arrays, resident in
+ * HBM (view them with dgb_device_mesh_view and pass the view to dgb_assemble).  Inputs may be
+ * HOST or DEVICE pointers (copied; cudaMemcpyDefault).  Synchronises `stream`. */
+int dgb_device_mesh_build(const double* nodes_xy, int32_t n_nodes, const int32_t* elements,
+                          int32_t n_elements, const int32_t* dirichlet_pairs, int32_t n_dirichlet,
+                          const int32_t* neumann_pairs, int32_t n_neumann, int32_t device,
+                          dgb_device_mesh** out, void* stream);
+
+/* Replaces uniform_refine(mesh) (mesh.cpp:153-187): midpoint refinement (4 children per
+ * element, boundary edges split in edge order), then the device build_mesh above. */
+int dgb_device_mesh_refine(const dgb_device_mesh* in, dgb_device_mesh** out, void* stream);
+
+/* DEVICE-pointer view (valid until dgb_device_mesh_free). */
+int dgb_device_mesh_view(const dgb_device_mesh* mesh, dgb_mesh_arrays* out);
+/* Copies the arrays into HOST buffers sized by the view's counts (any pointer may be NULL). */
+int dgb_device_mesh_copy_to_host(const dgb_device_mesh* mesh, double* nodes, int32_t* elements,
+                                 int32_t* edges, uint8_t* edge_kind, int32_t* edge_elements,
+                                 int32_t* element_edges);
+void dgb_device_mesh_free(dgb_device_mesh* mesh);
+
 #ifdef __cplusplus
 } /* extern "C" */
 #endif

@@ -30,6 +30,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include "common.hpp"
+#include "device_math.cuh"
 
 namespace dgb {
 
@@ -95,28 +96,8 @@ struct KParams {
 };
 
 // ------------------------------------------------------------------------------------------
-// device helpers
+// device helpers (FMUL / FADD / FSUB / FDIV and hypot_dd: device_math.cuh)
 // ------------------------------------------------------------------------------------------
-#define FMUL __dmul_rn
-#define FADD __dadd_rn
-#define FSUB __dsub_rn
-#define FDIV __ddiv_rn
-
-// sqrt(x^2 + y^2) with a double-double Newton correction (within ~0.5 ulp; glibc's hypot
-// itself is not correctly rounded).
-__device__ __forceinline__ double hypot_dd(double x, double y) {
-  x = fabs(x);
-  y = fabs(y);
-  const double x2 = FMUL(x, x), y2 = FMUL(y, y);
-  const double ex = fma(x, x, -x2), ey = fma(y, y, -y2);
-  const double s = FADD(x2, y2);
-  const double bb = FSUB(s, x2);
-  const double es = FADD(FSUB(x2, FSUB(s, bb)), FSUB(y2, bb));
-  const double lo = es + ex + ey;
-  const double r = __dsqrt_rn(s);
-  const double d = fma(r, r, -s) - lo;
-  return r - d / (2.0 * r);
-}
 
 __device__ __forceinline__ void family(int fn, const double* p, double x, double y, double& u,
                                        double& ux, double& uy, double& lap) {

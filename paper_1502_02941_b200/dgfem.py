@@ -517,3 +517,67 @@ def eval_solution(coef, ref: ReferenceElement, elements, xhat, yhat, device: int
                                  elements.data_ptr(), xhat.data_ptr(), yhat.data_ptr(),
                                  out.data_ptr(), C.c_void_p(_stream_handle(device, stream))))
     return out
+
+
+# ------------------------------------------------------------------------------ device mesh build
+class DeviceBuiltMesh:
+    """A mesh built in HBM by dgb_device_mesh_build / dgb_device_mesh_refine (build_mesh and
+    uniform_refine, mesh.cpp:51-187).  Usable wherever a DeviceMesh is (`.view`)."""
+
+    def __init__(self, handle, device: int = 0):
+        self._lib = capi.load()
+        self._h = handle
+        self.device = device
+        v = MeshArrays()
+        _check(self._lib.dgb_device_mesh_view(handle, C.byref(v)))
+        self.view = v
+        self.n_nodes, self.n_elements, self.n_edges = v.n_nodes, v.n_elements, v.n_edges
+        self.n_interior_edges = v.n_interior_edges
+
+    def refine(self, stream=None) -> "DeviceBuiltMesh":
+        h = C.c_void_p()
+        _check(self._lib.dgb_device_mesh_refine(self._h, C.byref(h),
+                                                C.c_void_p(_stream_handle(self.device, stream))))
+        return DeviceBuiltMesh(h, self.device)
+
+    def arrays(self) -> dict:
+        """Host copies of the mesh arrays (the layout of Mesh.arrays())."""
+        v = self.view
+        out = {"nodes": np.zeros((v.n_nodes, 2)), "elements": np.zeros((v.n_elements, 3), np.int32),
+               "edges": np.zeros((v.n_edges, 2), np.int32), "edge_kind": np.zeros(v.n_edges, np.uint8),
+               "edge_elements": np.zeros((v.n_edges, 2), np.int32),
+               "element_edges": np.zeros((v.n_elements, 3), np.int32)}
+        _check(self._lib.dgb_device_mesh_copy_to_host(
+            self._h, *(out[k].ctypes.data for k in ("nodes", "elements", "edges", "edge_kind",
+                                                     "edge_elements", "element_edges"))))
+        return out
+
+    def __del__(self):
+        try:
+            self._lib.dgb_device_mesh_free(self._h)
+        except Exception:
+            pass
+
+
+def device_build_mesh(nodes, elements, dirichlet, neumann, device: int = 0,
+                      stream=None) -> DeviceBuiltMesh:
+    """build_mesh(nodes, elements, dirichlet, neumann) (mesh.cpp:51-151) on the device; host
+    numpy or device torch inputs.  Raises Error like the reference."""
+    lib = capi.load()
+
+    def ptr(a, dtype):
+        if hasattr(a, "data_ptr"):
+            return a.data_ptr(), a
+        arr = np.ascontiguousarray(a, dtype=dtype)
+        return arr.ctypes.data, arr
+    pn, kn = ptr(nodes, np.float64)
+    pe, ke = ptr(elements, np.int32)
+    pd, kd = ptr(dirichlet, np.int32)
+    pm, km = ptr(neumann, np.int32)
+    count = (lambda a, w: (a.numel() if hasattr(a, "numel") else np.asarray(a).size) // w)
+    h = C.c_void_p()
+    _check(lib.dgb_device_mesh_build(pn, count(nodes, 2), pe, count(elements, 3), pd,
+                                     count(dirichlet, 2), pm, count(neumann, 2), device, C.byref(h),
+                                     C.c_void_p(_stream_handle(device, stream))))
+    del kn, ke, kd, km
+    return DeviceBuiltMesh(h, device)

@@ -18,6 +18,7 @@ Outputs (numpy .npz, a few MB in total):
   nonlinear.npz  assemble_nonlinear's H and HJ (CSR), degrees 1..4, every reaction kind,
                seeded coefficients; plus the coefficient-length error
   postprocess.npz  l2_error, project and eval_solution, degrees 1..4
+  refine.npz   unit_square_mesh + uniform_refine, levels 0 and 4
 
     python tests/golden/make_golden.py [tables meshes systems nonlinear]   (default: all)
 """
@@ -246,11 +247,23 @@ def postprocess(ref: RefLib) -> dict:
     return out
 
 
+def refine(ref: RefLib) -> dict:
+    """unit_square_mesh (mesh.cpp:189-211) and uniform_refine (mesh.cpp:153-187) of the
+    reference: level 0 and level 4 arrays, all-Dirichlet and with Neumann sides 2|8."""
+    out = {}
+    for sides in (0, 2 | 8):
+        for level in (0, 4):
+            m = ref.unit_square_refined(level, sides)
+            for k, v in m.arrays.items():
+                out[f"s{sides}_l{level}/{k}"] = v
+    return out
+
+
 def main():
     ref = RefLib()
-    which = sys.argv[1:] or ["tables", "meshes", "systems", "nonlinear", "postprocess"]
+    which = sys.argv[1:] or ["tables", "meshes", "systems", "nonlinear", "postprocess", "refine"]
     makers = {"tables": tables, "meshes": meshes, "systems": systems, "nonlinear": nonlinear,
-              "postprocess": postprocess}
+              "postprocess": postprocess, "refine": refine}
     for w in which:
         np.savez_compressed(os.path.join(HERE, f"{w}.npz"), **makers[w](ref))
         print(f"{w}.npz", os.path.getsize(os.path.join(HERE, f"{w}.npz")), "bytes")
