@@ -44,10 +44,12 @@ def parse_args():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", type=int, default=2)
-    ap.add_argument("--op", choices=["assembly", "nonlinear", "solve"], default="assembly",
+    ap.add_argument("--op", choices=["assembly", "nonlinear", "solve", "mesh"], default="assembly",
                     help="assembly: the headline (assemble_all + stiffness); nonlinear: "
                          "assemble_nonlinear on the config's mesh and degree, r(u) = u^2; "
-                         "solve: K x = F of the config's SIPG system (block-Jacobi GMRES)")
+                         "solve: K x = F of the config's SIPG system (block-Jacobi GMRES); "
+                         "mesh: build_mesh + uniform_refine to level --levels on the device")
+    ap.add_argument("--levels", type=int, default=10, help="--op mesh: refinement levels")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
@@ -783,9 +785,81 @@ def run_solve(args, world, rank, local):
     }), flush=True)
 
 
+# ----------------------------------------------------------------------------- mesh op
+METRIC_MESH = ("mesh topology build (build_mesh + uniform_refine chain to the C4 size): "
+               "elements/sec (1 B200)")
+
+
+def run_mesh(args, world, rank, local):
+    """uniform_refine from the reference's unit_square_mesh (8 triangles) to --levels (10: 8.4M
+    triangles, the reference's C4 mesh), every level through the device build_mesh.  `value` =
+    elements of the final level / the time of the whole chain.  cpu_baseline = the reference's
+    own uniform_refine chain (oracle/_ref) to a bounded level, rescaled to elements/s."""
+    import torch
+    from paper_1502_02941_b200 import capi, dgfem
+    torch.cuda.set_device(local)
+    base = {"nodes": np.array([[0.0, 0.0], [0.5, 0.0], [1.0, 0.0], [0.0, 0.5], [0.5, 0.5], [1.0, 0.5],
+                               [0.0, 1.0], [0.5, 1.0], [1.0, 1.0]]),
+            "elements": np.array([[3, 0, 4], [0, 1, 4], [4, 1, 5], [1, 2, 5], [6, 3, 7], [3, 4, 7],
+                                  [7, 4, 8], [4, 5, 8]], np.int32),
+            "dirichlet": np.array([[0, 1], [1, 2], [0, 3], [2, 5], [3, 6], [5, 8], [6, 7], [7, 8]], np.int32),
+            "neumann": np.zeros((0, 2), np.int32)}   # unit_square_mesh() (mesh.cpp:189-211)
+
+    def chain():
+        m = dgfem.device_build_mesh(base["nodes"], base["elements"], base["dirichlet"], base["neumann"], local)
+        for _ in range(args.levels):
+            m = m.refine()
+        return m
+    for _ in range(args.warmup):
+        chain()
+    torch.cuda.synchronize()
+    K = args.steps
+    times = []
+    with ClockSampler(local) as clocks:
+        for _ in range(K):
+            t0 = time.perf_counter()      # the chain synchronises at every level (host counts)
+            m = chain()
+            torch.cuda.synchronize()
+            times.append(time.perf_counter() - t0)
+    sec = sum(times) / K
+    E = m.n_elements
+    value = E / sec
+    cpu = None
+    if not args.no_cpu_baseline:
+        try:
+            from oracle import oracle as orc
+            lib = orc.RefLib()
+            lvl = min(args.levels, 8)
+            t0 = time.perf_counter()
+            lib.unit_square_refined(lvl, 0)
+            t = time.perf_counter() - t0
+            e_cpu = 8 * 4 ** lvl
+            cpu = {"value": round(e_cpu / t, 1), "unit": "elements/s", "cores": 1, "kind": "reference",
+                   "sample": f"the reference's unit_square_mesh + uniform_refine x{lvl} ({e_cpu} "
+                             f"elements) in {t:.2f} s (includes the ref_shim flatten copy)"}
+        except FileNotFoundError:
+            cpu = None
+    print(json.dumps({
+        "metric": METRIC_MESH, "value": round(value, 1), "unit": "elements/s", "n_gpus": 1,
+        "steps": K, "warmup": args.warmup, "ms_per_step": round(1e3 * sec, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+        "data": "synthetic (the reference's unit_square_mesh, refined)",
+        "config": {"workload": f"device build_mesh of unit_square_mesh() + {args.levels} x "
+                               f"uniform_refine (each level rebuilt by the device build_mesh): "
+                               f"{E} triangles, {m.n_edges} edges",
+                   "timing": "host wall clock around the chain (it synchronises per level)"},
+        "roofline": None, "cpu_baseline": cpu, "e2e": None, "gpu_launches": None,
+        "clocks": clocks.summary(),
+    }), flush=True)
+
+
 def main():
     args = parse_args()
     world, rank, local = dist_setup(args)
+    if args.op == "mesh":
+        if rank == 0:
+            run_mesh(args, world, rank, local)
+        return
     if args.op == "solve":
         run_solve(args, world, rank, local)
         return
