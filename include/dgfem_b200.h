@@ -317,6 +317,15 @@ int dgb_plan_bind_mesh(dgb_plan* plan, const dgb_mesh_arrays* mesh, int32_t row_
                        int32_t row_end, void* stream);
 int dgb_plan_unbind_mesh(dgb_plan* plan);
 
+/* Several assemblies of block rows [row_begin, row_end) of the same mesh and problem with
+ * different parameter sets (SIPG / NIPG / IIPG, penalty sweeps): outs[i], rhs[i] receive the
+ * system of params[i], exactly as n calls of dgb_assemble_rows would.  With the rows bound
+ * (dgb_plan_bind_mesh), the P2 tensor-core kernel and n <= 4 this is ONE launch (grid.y = n:
+ * no per-launch tail or launch gap between the assemblies); otherwise n calls.  DEVICE. */
+int dgb_assemble_batch(dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_problem* problem,
+                       const dgb_params* params, int32_t n, int32_t row_begin, int32_t row_end,
+                       dgb_bsr* outs, double* const* rhs, void* stream);
+
 /* Device operations (kernels, CUB scan kernels) the plan's last dgb_assemble* call launched:
  * 1 with a bound pattern, 4 without (bench.py's gpu_launches). */
 int32_t dgb_plan_launch_count(const dgb_plan* plan);

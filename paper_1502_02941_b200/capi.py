@@ -163,6 +163,8 @@ def _declare(lib: C.CDLL) -> C.CDLL:
         "dgb_device_mesh_view": (C.c_int, [vp, P(MeshArrays)]),
         "dgb_device_mesh_free": (None, [vp]),
         "dgb_device_mesh_copy_to_host": (C.c_int, [vp, vp, vp, vp, vp, vp, vp]),
+        "dgb_assemble_batch": (C.c_int, [vp, P(MeshArrays), P(Problem), P(Params), C.c_int32,
+                                         C.c_int32, C.c_int32, P(Bsr), P(vp), vp]),
         "dgb_l2_quad_order": (C.c_int32, [C.c_int32, C.c_int32]),
         "dgb_l2_error": (C.c_int, [vp, P(MeshArrays), vp, C.c_int64, P(ScalarField), vp, vp]),
         "dgb_project": (C.c_int, [vp, P(MeshArrays), P(ScalarField), vp, vp]),
@@ -192,7 +194,7 @@ EXPORTED_SYMBOLS = [
     "dgb_solve_options_default", "dgb_newton_config_default", "dgb_solve", "dgb_newton_solve",
     "dgb_l2_quad_order", "dgb_l2_error", "dgb_project", "dgb_eval_solution",
     "dgb_device_mesh_build", "dgb_device_mesh_refine", "dgb_device_mesh_view",
-    "dgb_device_mesh_free", "dgb_device_mesh_copy_to_host",
+    "dgb_device_mesh_free", "dgb_device_mesh_copy_to_host", "dgb_assemble_batch",
 ]
 OPTION_FORCE_GENERIC_KERNEL = 1
 OPTION_MIN_BLOCKS = 2

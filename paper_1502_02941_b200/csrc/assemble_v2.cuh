@@ -56,6 +56,19 @@ struct Tab {
 // The tensor-core kernel (P2, constant velocity) takes the compact parameter block.
 constexpr bool full_tensors(int NL, int BK) { return !(NL == 6 && BK == 0); }
 
+// One assembly of a launch: its penalty parameters and its outputs.  A launch assembles
+// n_batch parameter sets of the same mesh and problem (grid.y = n_batch; the tensor-core
+// kernel only, whose kappa-dependent terms live in the per-set B operand `bfrag`).
+constexpr int kMaxBatch = 4;
+struct MethodOut {
+  int32_t* row_ptr;              // output row pointer of the launch's rows
+  int32_t* col;
+  double* val;
+  double* rhs;
+  const double* bfrag;           // DMMA B fragments (diagonal: kappa-folded W) [ks][nt][lane]
+  double kappa, sigma_i, sigma_b;
+};
+
 template <int NL, int NQV, int NQE, bool TRIG, bool FULL>
 struct Params2 {
   const double* nodes;
@@ -63,14 +76,9 @@ struct Params2 {
   const uint8_t* edge_kind;
   const int32_t* edge_elements;
   const int32_t* element_edges;
-  int32_t* row_ptr;              // output row pointer of the launch's rows
   const int32_t* row_ptr_src;    // bound pattern (dgb_plan_bind_mesh) copied to row_ptr, or null
   const int4* adj_nb;            // bound adjacency: neighbour per local edge, .w = kinds | lf << 2
   const int4* adj_op;            // bound adjacency: neighbour's vertex opposite the shared edge
-  const double* bfrag;           // DMMA B fragments of the diagonal terms [ks][nt][lane]
-  int32_t* col;
-  double* val;
-  double* rhs;
   unsigned long long* err_edge;  // epoch << 32 | ~edge, max-reduced (lowest edge wins)
   unsigned long long epoch;
   int32_t n_elements;
@@ -78,7 +86,8 @@ struct Params2 {
   int32_t drop_neumann;
   int32_t evict_first;           // L2 evict-first hint on the output stream
   int32_t ablate;                // profiling diagnostics only (wrong results): see dg_assembly.cu
-  double kappa, sigma_i, sigma_b;
+  int32_t n_batch;
+  MethodOut bt[kMaxBatch];
   dgb_problem prob;
   Tab<NL, NQV, NQE, TRIG, FULL> t;
 };
@@ -322,6 +331,14 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
   __syncthreads();
   if (P.ablate & 16) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // this CTA's parameter set (grid.y) and its outputs
+  const int mset = blockIdx.y;
+  const double kappa = P.bt[mset].kappa, sigma_i = P.bt[mset].sigma_i, sigma_b = P.bt[mset].sigma_b;
+  int32_t* const o_row_ptr = P.bt[mset].row_ptr;
+  int32_t* const o_col = P.bt[mset].col;
+  double* const o_val = P.bt[mset].val;
+  double* const o_rhs = P.bt[mset].rhs;
+  const double* const o_bfrag = P.bt[mset].bfrag;
   double* stw = smem + SM::kTr + warp * SM::kWarp;  // staging [32][SS]
   double* st = stw + lane * SS;  // (even N2) this lane's block
   double* sk = stw + SM::kStage;                     // stash [NF][3][32]
@@ -359,7 +376,7 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
   const double G10 = -B01 * rdet, G11 = B00 * rdet;
   const double eps = scalar_element(P.prob.diffusion, ee);
   if (P.ablate & 32) {
-    if (active) P.rhs[ee - P.row_begin] = det;
+    if (active) o_rhs[ee - P.row_begin] = det;
     return;
   }
 
@@ -442,9 +459,9 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
       w1 = base * ge1;
       y0 = -base * (gf.G00 * nx + gf.G10 * ny);
       y1 = -base * (gf.G01 * nx + gf.G11 * ny);
-      z0 = -P.kappa * base * ge0;
-      z1 = -P.kappa * base * ge1;
-      const double sh = P.sigma_i * rh;
+      z0 = -kappa * base * ge0;
+      z1 = -kappa * base * ge1;
+      const double sh = sigma_i * rh;
       if constexpr (BK == 0) {
         // constant b: every point has the same flux, so the point weights factor out
         const double fl = FADD(FMUL(bf.p[0], nx), FMUL(bf.p[1], ny));
@@ -498,7 +515,7 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
         const double base = h * eps;  // avg = 1
         w0 = base * ge0;
         w1 = base * ge1;
-        const double sh = P.sigma_b * rh;
+        const double sh = sigma_b * rh;
         if constexpr (BK == 0) {
           cp = sh * (h * eps) - ((inflow && fls[0] < 0.0) ? FMUL(h, fls[0]) : 0.0);
         }
@@ -508,7 +525,7 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
           const double win = (inflow && fls[p] < 0.0) ? -FMUL(w, fls[p]) : 0.0;
           const double wgd = w * gb[p];
           cG[p] = wgd * (sh * eps) + win * gb[p];  // emit_dirichlet_rhs + inflow data term
-          cH[p] = wgd * (P.kappa * eps);
+          cH[p] = wgd * (kappa * eps);
           if constexpr (BK != 0) K(F_U + p, l) = FMUL(sh, FMUL(w, eps)) + win;
         }
       }
@@ -552,18 +569,18 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
   if (P.row_ptr_src) {  // pattern computed once per mesh: copy this element's entry
     rp = __ldg(P.row_ptr_src + (ee - P.row_begin));
     if (active) {
-      P.row_ptr[ee - P.row_begin + 1] = __ldg(P.row_ptr_src + (ee - P.row_begin + 1));
-      if (ee == P.row_begin) P.row_ptr[0] = 0;
+      o_row_ptr[ee - P.row_begin + 1] = __ldg(P.row_ptr_src + (ee - P.row_begin + 1));
+      if (ee == P.row_begin) o_row_ptr[0] = 0;
     }
   } else {
-    rp = P.row_ptr[ee - P.row_begin];
+    rp = o_row_ptr[ee - P.row_begin];
   }
   const int diag_slot = slot_of[0];
-  if (active) P.col[rp + diag_slot] = ee;
+  if (active) o_col[rp + diag_slot] = ee;
 #pragma unroll
   for (int l = 0; l < 3; ++l) {
     if (fcol[l] >= 0) {
-      if (active) P.col[rp + slot_of[1 + l]] = fcol[l];
+      if (active) o_col[rp + slot_of[1 + l]] = fcol[l];
       mk[l * 32 + lane] |= slot_of[1 + l] << 4;
     }
   }
@@ -589,7 +606,7 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
     __syncwarp();
     const int e_first = blockIdx.x * blockDim.x + warp * 32;  // relative to row_begin
     const int n_here = min(32, P.row_end - P.row_begin - e_first);
-    double* dst = P.rhs + static_cast<long long>(e_first) * NL;
+    double* dst = o_rhs + static_cast<long long>(e_first) * NL;
     const int bulk = (n_here * NL) & ~1;  // 16-byte multiple (warp slices start 16-B aligned)
     if (lane == 0 && bulk > 0) {
       fence_smem_to_async();
@@ -634,9 +651,9 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
       const int g = lane >> 2, t = lane & 3;
       if (!(P.ablate & 8)) {
         mma_block_store<SM::kKS, SM::kNT, N2>(
-            [&](int m, int ks) { return sk[(4 * ks + t) * SM::kCT + 8 * m + g]; }, P.bfrag,
+            [&](int m, int ks) { return sk[(4 * ks + t) * SM::kCT + 8 * m + g]; }, o_bfrag,
             (active && !(P.ablate & 1)) ? static_cast<long long>(rp + diag_slot) * N2 : -1LL,
-            P.val, lane, pol);
+            o_val, lane, pol);
       }
     } else {
     constexpr int RC = NL <= 6 ? NL : (NL <= 10 ? 2 : 1);  // rows per register chunk
@@ -731,7 +748,7 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
     }  // register path
     if constexpr (!SM::kRowMode && !SM::kMma) {
       write_block<N2>(stw, st, active ? static_cast<long long>(rp + diag_slot) * N2 : -1LL,
-                      P.val, lane, P.evict_first);
+                      o_val, lane, P.evict_first);
     }
   }
 
@@ -785,7 +802,7 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
       for (int v = 0; v < 3; ++v) {
         const int tb = v == 0 ? 0 : (v == 1 ? t1 : t2), te = v == 0 ? t1 : (v == 1 ? t2 : ntiles);
         if (tb == te) continue;
-        const double* fr = P.bfrag + SM::kFragTile + (l * 3 + v) * SM::kOffTile + lane;
+        const double* fr = o_bfrag + SM::kFragTile + (l * 3 + v) * SM::kOffTile + lane;
         double bv[2][SM::kNT];
 #pragma unroll
         for (int nt = 0; nt < SM::kNT; ++nt) {
@@ -803,7 +820,7 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
             dmma_8x8x4(d0, d1, c0, bv[0][nt]);
             dmma_8x8x4(d0, d1, c1, bv[1][nt]);
             const int n0 = 8 * nt + 2 * t;
-            if ((N2 % 8 == 0 || n0 < N2) && cb >= 0 && !(P.ablate & 1)) store_pair(P.val + cb + n0, d0, d1, pol);
+            if ((N2 % 8 == 0 || n0 < N2) && cb >= 0 && !(P.ablate & 1)) store_pair(o_val + cb + n0, d0, d1, pol);
           }
         }
       }
@@ -857,7 +874,7 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
       }
     }
     if constexpr (!SM::kRowMode) {
-      write_block<N2>(stw, st, store ? static_cast<long long>(rp + slot) * N2 : -1LL, P.val, lane,
+      write_block<N2>(stw, st, store ? static_cast<long long>(rp + slot) * N2 : -1LL, o_val, lane,
                       P.evict_first);
     }
   }
@@ -865,7 +882,7 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
     // one bulk copy of the warp's whole row range; the unaligned head / tail doubles by hand
     __syncwarp();
     const int n = (rp_last - rp_first) * N2;
-    double* dst = P.val + static_cast<long long>(rp_first) * N2;
+    double* dst = o_val + static_cast<long long>(rp_first) * N2;
     const int head = rp_first & 1;
     const int body = (n - head) & ~1;
     if (lane == 0 && body > 0) {

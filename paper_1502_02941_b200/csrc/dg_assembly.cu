@@ -953,7 +953,7 @@ void validate_field(const dgb_scalar_field& f, bool element_constant, const char
 // folded per launch) and launches the element-per-thread kernel.
 template <int NL, int NQV, int NQE, int BK, int THREADS, int MINB>
 void launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_problem* problem,
-               const dgb_params* params, dgb_bsr* out, double* rhs, cudaStream_t s,
+               const dgb_params* params, dgb_bsr* out, double* const* rhs, int nb, cudaStream_t s,
                int out_row_begin, int out_row_end, const int32_t* row_ptr_src) {
   constexpr bool TRIG = BK == 2;
   constexpr bool FULL = dgb::v2::full_tensors(NL, BK);
@@ -970,10 +970,19 @@ void launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_prob
   P.edge_kind = mesh->edge_kind;
   P.edge_elements = mesh->edge_elements;
   P.element_edges = mesh->element_edges;
-  P.row_ptr = out->row_ptr;
-  P.col = out->col;
-  P.val = out->val;
-  P.rhs = rhs;
+  if (nb < 1 || nb > dgb::v2::kMaxBatch || (nb > 1 && FULL)) {
+    throw dgb::Error(DGB_STATUS_INVALID_ARGUMENT, "unsupported batch size for this kernel", nb);
+  }
+  P.n_batch = nb;
+  for (int i = 0; i < nb; ++i) {
+    P.bt[i].row_ptr = out[i].row_ptr;
+    P.bt[i].col = out[i].col;
+    P.bt[i].val = out[i].val;
+    P.bt[i].rhs = rhs[i];
+    P.bt[i].kappa = params[i].kappa;
+    P.bt[i].sigma_i = params[i].sigma_interior;
+    P.bt[i].sigma_b = params[i].sigma_boundary;
+  }
   P.row_ptr_src = row_ptr_src;
   if (row_ptr_src) {
     P.adj_nb = plan->d_adj;
@@ -987,9 +996,6 @@ void launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_prob
   P.drop_neumann = params->neumann_inflow == DGB_INFLOW_DROP;
   P.evict_first = (plan->l2_policy & 2) != 0;
   P.ablate = plan->ablate;
-  P.kappa = params->kappa;
-  P.sigma_i = params->sigma_interior;
-  P.sigma_b = params->sigma_boundary;
   P.prob = *problem;
   const double* h = plan->h_tens.data();
   const dgb::Layout& V = plan->L;
@@ -1003,7 +1009,7 @@ void launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_prob
     for (int i = 0; i < NL; ++i) {
       for (int j = 0; j < NL; ++j) {
         x[L::W + la * N2 + i * NL + j] =
-            params->kappa * h[V.Q + la * N2 + j * NL + i] - h[V.Q + la * N2 + i * NL + j];
+            params[0].kappa * h[V.Q + la * N2 + j * NL + i] - h[V.Q + la * N2 + i * NL + j];
       }
     }
   }
@@ -1036,9 +1042,11 @@ void launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_prob
     // (the factored neighbour block of the CUDA-core path, expanded).  Built once per
     // (plan, kappa) on the host.
     dgb_plan* mp = const_cast<dgb_plan*>(plan);
+    for (int bi_ = 0; bi_ < nb; ++bi_) {
+    const double kap = params[bi_].kappa;
     double* frag = nullptr;
     for (auto& c : mp->bfrag_cache) {
-      if (c.first == params->kappa) frag = c.second;
+      if (c.first == kap) frag = c.second;
     }
     if (!frag) {  // first assembly with this kappa: build and upload (stream-ordered) once
       auto ephi = [&](int l, int p, int i) { return x[L::EPHI + (l * NQE + p) * NL + i]; };
@@ -1057,9 +1065,14 @@ void launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_prob
           if (k < 3) off = L::S + k * N2;
           else if (k == 3) off = L::M;
           else if (k < 6) off = L::T + (k - 4) * N2;
-          else if (k < 12) off = L::W + (k - 6) * N2;
+          else if (k < 12) off = -1;  // W = kappa Q^T - Q for this set's kappa
           else off = L::P + (k - 12) * N2;
-          hb[i] = x[off + n];
+          if (off >= 0) {
+            hb[i] = x[off + n];
+          } else {
+            const int la = k - 6, bi = n / NL, bj = n % NL;
+            hb[i] = kap * h[V.Q + la * N2 + bj * NL + bi] - h[V.Q + la * N2 + bi * NL + bj];
+          }
         } else {
           const int l = (which - 1) / 3, lf = (which - 1) % 3, term = k, bi = n / NL, bj = n % NL;
           double acc = 0.0;
@@ -1080,9 +1093,10 @@ void launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_prob
       cuda_check(cudaMemcpyAsync(frag, hb.data(), hb.size() * sizeof(double),
                                  cudaMemcpyHostToDevice, s), "cudaMemcpyAsync(bfrag)");
       cuda_check(cudaStreamSynchronize(s), "cudaStreamSynchronize(bfrag)");
-      mp->bfrag_cache.emplace_back(params->kappa, frag);
+      mp->bfrag_cache.emplace_back(kap, frag);
     }
-    P.bfrag = frag;
+    P.bt[bi_].bfrag = frag;
+    }
   }
   auto kernel = dgb::v2::assemble_kernel<NL, NQV, NQE, BK, THREADS, MINB>;
   static bool configured = false;
@@ -1096,7 +1110,7 @@ void launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_prob
   // Keep the node coordinates (gathered by every element and its neighbours, in random order
   // for permuted meshes) persisting in L2 while the output streams through with evict-first.
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
+  cfg.gridDim = dim3(grid, nb);
   cfg.blockDim = dim3(THREADS);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
@@ -1123,7 +1137,7 @@ void launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_prob
 // CTA sizes / register budgets chosen by measurement (profiles/NOTES.md); returns false when
 // no specialisation exists (the generic kernel runs instead).
 bool try_launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_problem* problem,
-                   const dgb_params* params, dgb_bsr* out, double* rhs, cudaStream_t s,
+                   const dgb_params* params, dgb_bsr* out, double* const* rhs, int nb, cudaStream_t s,
                    int rb, int re, const int32_t* src) {
   if (plan->force_generic) return false;
   const int bk = problem->advection.kind;
@@ -1131,7 +1145,7 @@ bool try_launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_
   const int mb = plan->minblocks;
 #define DGB_V2(NL_, NQV_, NQE_, BK_, T_, MB_)                                               \
   if (key == NL_ * 10000 + NQV_ * 100 + NQE_ && bk == BK_) {                              \
-    launch_v2<NL_, NQV_, NQE_, BK_, T_, MB_>(plan, mesh, problem, params, out, rhs, s, rb, re, src); \
+    launch_v2<NL_, NQV_, NQE_, BK_, T_, MB_>(plan, mesh, problem, params, out, rhs, nb, s, rb, re, src); \
     return true;                                                                           \
   }
   if (mb == 3) {  // tuning variants of the headline kernels: smaller CTAs (shorter tail)
@@ -1458,6 +1472,70 @@ void dgb_plan_destroy(dgb_plan* p) {
   delete p;
 }
 
+int dgb_assemble_batch(dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_problem* problem,
+                       const dgb_params* params, int32_t n, int32_t row_begin, int32_t row_end,
+                       dgb_bsr* outs, double* const* rhs, void* stream) {
+  if (!plan || !mesh || !problem || !params || !outs || !rhs || n < 0) {
+    return dgb::record_error(DGB_STATUS_INVALID_ARGUMENT, "null argument", -1);
+  }
+  if (row_begin < 0 || row_end > mesh->n_elements || row_begin > row_end) {
+    return dgb::record_error(DGB_STATUS_INVALID_INDEX, "block row range outside the mesh", row_begin);
+  }
+  const int E = row_end - row_begin;
+  bool same_drop = true;
+  for (int i = 1; i < n; ++i) same_drop &= params[i].neumann_inflow == params[0].neumann_inflow;
+  const bool bound = plan->d_pattern && plan->bound_ee == mesh->element_edges &&
+                     plan->bound_elements == mesh->elements &&
+                     plan->bound_edge_elements == mesh->edge_elements &&
+                     plan->bound_kind == mesh->edge_kind && plan->bound_n == mesh->n_elements &&
+                     plan->bound_begin == row_begin && plan->bound_end == row_end;
+  // one launch for all parameter sets: the tensor-core P2 kernel on a bound mesh
+  const bool one_launch = n > 1 && n <= dgb::v2::kMaxBatch && bound && same_drop && E > 0 &&
+                          plan->nl == 6 && problem->advection.kind == DGB_VEC_CONSTANT &&
+                          !plan->force_generic;
+  if (one_launch) {
+    // validate exactly as a single assembly would (and reject mismatched outputs)
+    for (int i = 0; i < n; ++i) {
+      if (!outs[i].row_ptr || !outs[i].col || !outs[i].val || !rhs[i] ||
+          outs[i].block_dim != plan->nl || outs[i].n_block_rows != E) {
+        return dgb::record_error(DGB_STATUS_DIMENSION_MISMATCH, "BSR output does not match rows / plan", i);
+      }
+    }
+    const int st = dgb::guarded([&] {
+      validate_field(problem->diffusion, true, "diffusion");
+      validate_field(problem->linear_reaction, true, "linear_reaction");
+      validate_field(problem->source, false, "source");
+      validate_field(problem->dirichlet, false, "dirichlet");
+      validate_field(problem->neumann, false, "neumann");
+      if (problem->dirichlet.kind == DGB_FIELD_PER_ELEMENT ||
+          problem->neumann.kind == DGB_FIELD_PER_ELEMENT) {
+        throw dgb::Error(DGB_STATUS_INVALID_ARGUMENT, "boundary data cannot be PER_ELEMENT");
+      }
+      DeviceGuard guard(plan->device);
+      cudaStream_t s = static_cast<cudaStream_t>(stream);
+      plan->last_status = DGB_OK;
+      ++plan->epoch;
+      plan->last_launches = 1;
+      if (plan->ev_start) cuda_check(cudaEventRecord(plan->ev_start, s), "cudaEventRecord");
+      if (!try_launch_v2(plan, mesh, problem, params, outs, rhs, n, s, row_begin, row_end,
+                         plan->d_pattern)) {
+        throw dgb::Error(DGB_STATUS_UNSUPPORTED_DEGREE, "no batched kernel for this plan");
+      }
+      if (plan->ev_stop) cuda_check(cudaEventRecord(plan->ev_stop, s), "cudaEventRecord");
+    });
+    if (st != DGB_STATUS_UNSUPPORTED_DEGREE) return st;  // else: the per-set path below
+  }
+  int launches = 0;
+  for (int i = 0; i < n; ++i) {
+    const int st = dgb_assemble_rows(plan, mesh, problem, params + i, row_begin, row_end, outs + i,
+                                     rhs[i], stream);
+    if (st != DGB_OK) return st;
+    launches += plan->last_launches;
+  }
+  plan->last_launches = launches;
+  return DGB_OK;
+}
+
 int dgb_assemble_rows(dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_problem* problem,
                       const dgb_params* params, int32_t row_begin, int32_t row_end, dgb_bsr* out,
                       double* rhs, void* stream) {
@@ -1506,7 +1584,8 @@ int dgb_assemble_rows(dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_pro
       plan->last_launches += 3;
     }
     if (plan->ev_start) cuda_check(cudaEventRecord(plan->ev_start, s), "cudaEventRecord");
-    if (!try_launch_v2(plan, mesh, problem, params, out, rhs, s, row_begin, row_end, src)) {
+    double* rhs1[1] = {rhs};
+    if (!try_launch_v2(plan, mesh, problem, params, out, rhs1, 1, s, row_begin, row_end, src)) {
       if (src) {
         cuda_check(cudaMemcpyAsync(out->row_ptr, src, sizeof(int32_t) * (E + 1),
                                    cudaMemcpyDeviceToDevice, s), "cudaMemcpyAsync(pattern)");

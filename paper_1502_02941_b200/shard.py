@@ -94,3 +94,24 @@ class ShardAssembler:
         if check:
             dgfem._check(lib.dgb_plan_status(self.plan._h, C.c_void_p(h)))
         return self.out
+
+
+def assemble_batch(assemblers, params_list, stream=None, check: bool = True):
+    """dgb_assemble_batch over ShardAssemblers sharing one plan, device mesh and row range
+    (one launch for all parameter sets when the rows are bound)."""
+    import torch
+    from . import dgfem
+    lib = capi.load()
+    a0 = assemblers[0]
+    if stream is None:
+        stream = torch.cuda.current_stream(a0.plan.device)
+    h = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+    n = len(assemblers)
+    outs = (capi.Bsr * n)(*[a.out.struct() for a in assemblers])
+    rhs = (C.c_void_p * n)(*[a.out.rhs.data_ptr() for a in assemblers])
+    prm = (capi.Params * n)(*params_list)
+    dgfem._check(lib.dgb_assemble_batch(a0.plan._h, C.byref(a0.dmesh.view), C.byref(a0.dprob.c),
+                                        prm, n, a0.begin, a0.end, outs, rhs, C.c_void_p(h)))
+    if check:
+        dgfem._check(lib.dgb_plan_status(a0.plan._h, C.c_void_p(h)))
+    return [a.out for a in assemblers]

@@ -261,3 +261,25 @@ def test_bound_pattern_single_kernel_matches_unbound():
     capi.load().dgb_plan_unbind_mesh(plan._h)
     plan.assemble(dm, dp, params, b)
     assert capi.load().dgb_plan_launch_count(plan._h) == 4
+
+
+@pytest.mark.parametrize("cfg_index", [2, 4])
+def test_batch_equals_separate_assemblies(cfg_index):
+    """dgb_assemble_batch (SIPG, NIPG, IIPG in one launch for P2 on a bound mesh; a loop
+    otherwise) writes exactly what three dgb_assemble_rows calls write."""
+    cfg = problems.CONFIGS[cfg_index]
+    mesh = dgfem.unit_square_mesh(48, cfg.jitter, problems.SEED_JITTER, cfg.permute,
+                                  problems.SEED_PERMUTE, cfg.neumann_sides)
+    ref = dgfem.ReferenceElement(cfg.degree, cfg.quad_order)
+    spec = problems.config_problem(cfg_index, mesh.n_elements)
+    methods = [capi.SIPG, capi.NIPG, capi.IIPG]
+    params = [dgfem.config_parameters(cfg, m) for m in methods]
+    a = [shard.ShardAssembler(mesh, ref, spec, 0, 0, mesh.n_elements, bind=True)]
+    a += [shard.ShardAssembler(mesh, ref, spec, 0, 0, mesh.n_elements, share=a[0]) for _ in methods[1:]]
+    shard.assemble_batch(a, params)
+    got = [to_np(x.out) for x in a]
+    for p, g in zip(params, got):
+        single = shard.ShardAssembler(mesh, ref, spec, 0, 0, mesh.n_elements, share=a[0])
+        want = to_np(single.assemble(p))
+        for x, y in zip(g, want):
+            assert np.array_equal(x, y)
