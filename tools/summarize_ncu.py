@@ -38,6 +38,15 @@ def ncu_csv(rep: str, *args) -> list[list[str]]:
     return list(csv.reader(io.StringIO(r.stdout)))
 
 
+def assemblies_per_launch(cfg: int) -> int:
+    """The bench line's roofline.assemblies_per_launch (dgb_assemble_batch), else 1."""
+    try:
+        with open(os.path.join(OUT, f"bench_c{cfg}.json")) as f:
+            return int(json.load(f)["roofline"].get("assemblies_per_launch", 1) or 1)
+    except Exception:
+        return 1
+
+
 def summarize(rep: str, cfg: int) -> dict:
     rows = ncu_csv(rep, "--page", "details")
     h = rows[0]
@@ -68,7 +77,9 @@ def summarize(rep: str, cfg: int) -> dict:
         "details": det,
         "dram_bytes_read": rd, "dram_bytes_write": wr,
         "dram_bytes_per_launch": (rd + wr) if rd is not None and wr is not None else None,
-        "warp_instructions_per_element": inst / ELEMENTS[cfg] if inst else None,
+        "assemblies_per_launch": assemblies_per_launch(cfg),
+        "warp_instructions_per_element": (inst / (ELEMENTS[cfg] * assemblies_per_launch(cfg))
+                                          if inst else None),
         "fp64_pipe_active_pct": num("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
         "stall_share_pct": {k: round(100 * v / tot, 1) for k, v in top},
         "note": "ncu --set full --clock-control none (cold caches, serialised replay): use "
