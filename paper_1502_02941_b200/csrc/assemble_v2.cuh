@@ -361,13 +361,24 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
   const int ee = active ? e : P.row_end - 1;  // inactive lanes mirror a valid element
   const dgb_vector_field& bf = P.prob.advection;
 
-  // ---- phase A0: own geometry ----------------------------------------------------------------
+  // ---- phase A0: own geometry; every gather issued up front (two dependent levels) -------------
   int v[3];
 #pragma unroll
   for (int k = 0; k < 3; ++k) v[k] = __ldg(P.elements + 3 * ee + k);
+  int4 anb = make_int4(0, 0, 0, 0), aop = make_int4(0, 0, 0, 0);
+  if (P.adj_nb) {  // bound adjacency record: two coalesced 16-byte loads per element
+    anb = __ldg(P.adj_nb + (ee - P.row_begin));
+    aop = __ldg(P.adj_op + (ee - P.row_begin));
+  }
   double2 pv[3];
 #pragma unroll
   for (int k = 0; k < 3; ++k) pv[k] = __ldg(reinterpret_cast<const double2*>(P.nodes) + v[k]);
+  double2 po[3];  // bound path: the neighbours' vertices opposite the shared edges
+  if (P.adj_nb) {
+    po[0] = __ldg(reinterpret_cast<const double2*>(P.nodes) + max(aop.x, 0));
+    po[1] = __ldg(reinterpret_cast<const double2*>(P.nodes) + max(aop.y, 0));
+    po[2] = __ldg(reinterpret_cast<const double2*>(P.nodes) + max(aop.z, 0));
+  }
   const double B00 = FSUB(pv[1].x, pv[0].x), B01 = FSUB(pv[2].x, pv[0].x);
   const double B10 = FSUB(pv[1].y, pv[0].y), B11 = FSUB(pv[2].y, pv[0].y);
   const double det = FSUB(FMUL(B00, B11), FMUL(B01, B10));
@@ -407,11 +418,6 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
 
   // ---- phase A2: per local edge -> stashed coefficient record, boundary RHS --------------------
   int fcol[3] = {-1, -1, -1};  // neighbour across local edge l (interior edges only)
-  int4 anb = make_int4(0, 0, 0, 0), aop = make_int4(0, 0, 0, 0);
-  if (P.adj_nb) {  // bound adjacency record: two coalesced 16-byte loads per element
-    anb = __ldg(P.adj_nb + (ee - P.row_begin));
-    aop = __ldg(P.adj_op + (ee - P.row_begin));
-  }
 #pragma unroll
   for (int l = 0; l < 3; ++l) {
     const int a = v[(l + 1) % 3], b = v[(l + 2) % 3];
@@ -447,7 +453,18 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
     }
     double w0 = 0.0, w1 = 0.0, cp = 0.0, y0 = 0.0, y1 = 0.0, z0 = 0.0, z1 = 0.0, cx = 0.0;
     if (kind == DGB_EDGE_INTERIOR) {
-      const Geo gf = element_geo_fast(P.nodes, vf);
+      Geo gf;
+      if (P.adj_nb) {  // coordinates in registers: q[lf] = opposite, q[lf+1] = b, q[lf+2] = a
+        const double2 qo = l == 0 ? po[0] : (l == 1 ? po[1] : po[2]);
+        const double2 qa = l == 0 ? pv[1] : (l == 1 ? pv[2] : pv[0]);
+        const double2 qb = l == 0 ? pv[2] : (l == 1 ? pv[0] : pv[1]);
+        const double2 q0 = lf == 0 ? qo : (lf == 1 ? qa : qb);
+        const double2 q1 = lf == 1 ? qo : (lf == 2 ? qa : qb);
+        const double2 q2 = lf == 2 ? qo : (lf == 0 ? qa : qb);
+        gf = element_geo_coords(q0, q1, q2);
+      } else {
+        gf = element_geo_fast(P.nodes, vf);
+      }
       double eps_e = eps;
       if (P.prob.diffusion.kind == DGB_FIELD_PER_ELEMENT) {
         const double ef = __ldg(P.prob.diffusion.per_element + f);

@@ -243,6 +243,24 @@ __device__ __forceinline__ Geo element_geo(const double* __restrict__ nodes,
 
 // element_geometry with one reciprocal instead of four divisions (values only; no term-selecting
 // decision depends on G).
+// element_geo_fast from coordinates already in registers (same arithmetic).
+__device__ __forceinline__ Geo element_geo_coords(double2 p0, double2 p1, double2 p2) {
+  Geo g;
+  g.B00 = p1.x - p0.x;
+  g.B01 = p2.x - p0.x;
+  g.B10 = p1.y - p0.y;
+  g.B11 = p2.y - p0.y;
+  g.det = FSUB(FMUL(g.B00, g.B11), FMUL(g.B01, g.B10));
+  const double rd = 1.0 / g.det;
+  g.G00 = g.B11 * rd;
+  g.G01 = -g.B10 * rd;
+  g.G10 = -g.B01 * rd;
+  g.G11 = g.B00 * rd;
+  g.ox = p0.x;
+  g.oy = p0.y;
+  return g;
+}
+
 __device__ __forceinline__ Geo element_geo_fast(const double* __restrict__ nodes,
                                                 const int32_t* v) {
   Geo g;
