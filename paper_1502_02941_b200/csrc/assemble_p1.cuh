@@ -1,0 +1,358 @@
+// assemble_p1.cuh -- the block-row kernel for P1 with constant velocity (configs 1 and 4),
+// included by dg_assembly.cu after assemble_v2.cuh.
+//
+// Same decomposition and the same arithmetic, in the same order, as the general
+// element-per-thread kernel (assemble_v2.cuh), restructured for occupancy: every block
+// slot is known before the edge loop (the neighbour ids come first), so each edge's
+// neighbour block is computed and staged the moment its coefficients exist, and its face
+// terms go straight into the diagonal block held in registers.  No per-edge coefficient
+// stash is needed (6 KB of shared memory per warp on the general path), which lifts the P1
+// kernel from 12 to 16 resident warps per SM.  The staged rows leave as one bulk copy per
+// warp (the warp's row range is contiguous in the BSR).
+#pragma once
+
+namespace dgb {
+namespace v2 {
+
+template <int NQV, int NQE>
+struct SmemP1 {
+  static constexpr int NL = 3, N2 = 9;
+  static constexpr int kStage = (32 * 4 * N2 + 2 + 1) & ~1;  // the warp's row range
+  static constexpr int kRhs = (32 * NL + 1) & ~1;
+  static constexpr int kWarp = kStage + kRhs;
+  static constexpr int kTr = (3 * NQE * 3 * NL + 1) & ~1;
+};
+
+template <int NQV, int NQE, int THREADS, int MINB, bool BOUND>
+__global__ void __launch_bounds__(THREADS, MINB) assemble_p1_kernel(
+    const __grid_constant__ Params2<3, NQV, NQE, false, true> P) {
+  constexpr int NL = 3, N2 = 9;
+  using L = Lay<NL, NQV, NQE, false, true>;
+  using SM = SmemP1<NQV, NQE>;
+  extern __shared__ double smem[];
+  double* tr = smem;  // [3][NQE][3][NL]: phi, w d0 phi, w d1 phi of each local edge's points
+  for (int i = threadIdx.x; i < 3 * NQE * 3 * NL; i += blockDim.x) {
+    const int j = i % NL, c = (i / NL) % 3, p = (i / (3 * NL)) % NQE, l = i / (3 * NL * NQE);
+    tr[i] = c == 0 ? P.t.x[L::EPHI + (l * NQE + p) * NL + j]
+                   : P.t.x[L::EDW + ((l * NQE + p) * 2 + c - 1) * NL + j];
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int mset = blockIdx.y;
+  const double kappa = P.bt[mset].kappa, sigma_i = P.bt[mset].sigma_i, sigma_b = P.bt[mset].sigma_b;
+  int32_t* const o_row_ptr = P.bt[mset].row_ptr;
+  int32_t* const o_col = P.bt[mset].col;
+  double* const o_val = P.bt[mset].val;
+  double* const o_rhs = P.bt[mset].rhs;
+  double* stw = smem + SM::kTr + warp * SM::kWarp;
+  double* srhs = stw + SM::kStage;
+
+  const int e = P.row_begin + blockIdx.x * blockDim.x + threadIdx.x;
+  const bool active = e < P.row_end;
+  const int ee = active ? e : P.row_end - 1;
+  const dgb_vector_field& bf = P.prob.advection;
+  constexpr bool bound = BOUND;  // bound adjacency record (dgb_plan_bind_mesh) or not
+
+  // ---- gathers up front ------------------------------------------------------------------------
+  int v[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) v[k] = __ldg(P.elements + 3 * ee + k);
+  int4 anb = make_int4(0, 0, 0, 0), aop = make_int4(0, 0, 0, 0);
+  int rp = 0, rp_next = 0;
+  if constexpr (bound) {
+    anb = __ldg(P.adj_nb + (ee - P.row_begin));
+    aop = __ldg(P.adj_op + (ee - P.row_begin));
+  }
+  if (P.row_ptr_src) {
+    rp = __ldg(P.row_ptr_src + (ee - P.row_begin));
+    rp_next = __ldg(P.row_ptr_src + (ee - P.row_begin + 1));
+  }
+  double2 pv[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) pv[k] = __ldg(reinterpret_cast<const double2*>(P.nodes) + v[k]);
+  double2 po[3];
+  if constexpr (bound) {
+    po[0] = __ldg(reinterpret_cast<const double2*>(P.nodes) + max(aop.x, 0));
+    po[1] = __ldg(reinterpret_cast<const double2*>(P.nodes) + max(aop.y, 0));
+    po[2] = __ldg(reinterpret_cast<const double2*>(P.nodes) + max(aop.z, 0));
+  }
+  // neighbours first: kind, neighbour, its local edge (and, unbound, its vertices)
+  int kindv[3], lfv[3], fv[3], edgev[3], vfv[3][3];
+#pragma unroll
+  for (int l = 0; l < 3; ++l) {
+    const int a = v[(l + 1) % 3], b = v[(l + 2) % 3];
+    edgev[l] = -1;
+    lfv[l] = 0;
+    fv[l] = -1;
+    if constexpr (bound) {
+      kindv[l] = (anb.w >> (4 * l)) & 3;
+      lfv[l] = (anb.w >> (4 * l + 2)) & 3;
+      fv[l] = l == 0 ? anb.x : (l == 1 ? anb.y : anb.z);
+    } else {
+      edgev[l] = __ldg(P.element_edges + 3 * ee + l);
+      kindv[l] = __ldg(P.edge_kind + edgev[l]);
+      if (kindv[l] == DGB_EDGE_INTERIOR) {
+        const int2 lr = __ldg(reinterpret_cast<const int2*>(P.edge_elements) + edgev[l]);
+        fv[l] = lr.x == ee ? lr.y : lr.x;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) vfv[l][k] = __ldg(P.elements + 3 * fv[l] + k);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) if (vfv[l][k] != a && vfv[l][k] != b) lfv[l] = k;
+      }
+    }
+    if (kindv[l] != DGB_EDGE_INTERIOR) fv[l] = -1;
+  }
+  // sorted block columns -> slots (rank among the row's distinct columns)
+  int slot_of[4], nb = 1;
+  {
+    const int cx[4] = {ee, fv[0], fv[1], fv[2]};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      int r = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) r += (j != i && cx[j] >= 0 && cx[j] < cx[i]) ? 1 : 0;
+      slot_of[i] = r;
+    }
+#pragma unroll
+    for (int l = 0; l < 3; ++l) nb += fv[l] >= 0 ? 1 : 0;
+  }
+  if (P.row_ptr_src) {
+    if (active) {
+      o_row_ptr[ee - P.row_begin + 1] = rp_next;
+      if (ee == P.row_begin) o_row_ptr[0] = 0;
+    }
+  } else {
+    rp = o_row_ptr[ee - P.row_begin];
+  }
+  if (active) {
+    o_col[rp + slot_of[0]] = ee;
+#pragma unroll
+    for (int l = 0; l < 3; ++l) if (fv[l] >= 0) o_col[rp + slot_of[1 + l]] = fv[l];
+  }
+  const int rp_first = __shfl_sync(0xffffffffu, rp, 0);
+  const int rp_last = __reduce_max_sync(0xffffffffu, active ? rp + nb : 0);
+  double* srow = stw + (rp_first & 1);  // same 16-byte phase as val + rp_first * N2
+  double* const myrow = srow + (rp - rp_first) * N2;
+
+  // ---- own geometry, coefficients of the volume terms ------------------------------------------
+  const double B00 = FSUB(pv[1].x, pv[0].x), B01 = FSUB(pv[2].x, pv[0].x);
+  const double B10 = FSUB(pv[1].y, pv[0].y), B11 = FSUB(pv[2].y, pv[0].y);
+  const double det = FSUB(FMUL(B00, B11), FMUL(B01, B10));
+  const double rdet = 1.0 / det;
+  const double G00 = B11 * rdet, G01 = -B10 * rdet;
+  const double G10 = -B01 * rdet, G11 = B00 * rdet;
+  const double eps = scalar_element(P.prob.diffusion, ee);
+
+  // RHS volume term
+  double F[NL];
+#pragma unroll
+  for (int i = 0; i < NL; ++i) F[i] = 0.0;
+  {
+    const dgb_scalar_field& fs = P.prob.source;
+#pragma unroll 1
+    for (int q = 0; q < NQV; ++q) {
+      const double px = FADD(FADD(pv[0].x, FMUL(B00, P.t.x[L::VX + q])), FMUL(B01, P.t.x[L::VY + q]));
+      const double py = FADD(FADD(pv[0].y, FMUL(B10, P.t.x[L::VX + q])), FMUL(B11, P.t.x[L::VY + q]));
+      const double f = fs.kind == DGB_FIELD_PER_ELEMENT ? __ldg(fs.per_element + ee)
+                                                        : scalar_point_inline(fs, px, py);
+      const double c = (det * P.t.x[L::VW + q]) * f;
+#pragma unroll
+      for (int i = 0; i < NL; ++i) F[i] = fma(c, P.t.x[L::PHI + q * NL + i], F[i]);
+    }
+  }
+
+  // diagonal block: volume terms (registers)
+  double acc[N2];
+  {
+    const double alpha = scalar_element(P.prob.linear_reaction, ee);
+    const double de = det * eps;
+    const double cD0 = de * (G00 * G00 + G10 * G10);
+    const double cD1 = de * (G00 * G01 + G10 * G11);
+    const double cD2 = de * (G01 * G01 + G11 * G11);
+    const double cR = det * alpha;
+    const double cC0 = det * (G00 * bf.p[0] + G10 * bf.p[1]);
+    const double cC1 = det * (G01 * bf.p[0] + G11 * bf.p[1]);
+#pragma unroll
+    for (int k = 0; k < N2; ++k) {
+      double x = cD0 * P.t.x[L::S + k];
+      x = fma(cD1, P.t.x[L::S + N2 + k], x);
+      x = fma(cD2, P.t.x[L::S + 2 * N2 + k], x);
+      x = fma(cR, P.t.x[L::M + k], x);
+      x = fma(cC0, P.t.x[L::T + k], x);
+      x = fma(cC1, P.t.x[L::T + N2 + k], x);
+      acc[k] = x;
+    }
+  }
+
+  // ---- edges: face terms into the diagonal, neighbour blocks staged at once --------------------
+#pragma unroll
+  for (int l = 0; l < 3; ++l) {
+    const int a = v[(l + 1) % 3], b = v[(l + 2) % 3];
+    const int o = a < b ? 0 : 1;  // make_side orientation (assembly.cpp:125-126)
+    const double2 A = o == 0 ? pv[(l + 1) % 3] : pv[(l + 2) % 3];
+    const double2 Bn = o == 0 ? pv[(l + 2) % 3] : pv[(l + 1) % 3];
+    const double dx = FSUB(Bn.x, A.x), dy = FSUB(Bn.y, A.y);
+    const double h = hypot_dd(dx, dy);  // edge_geometry (mesh.cpp:232-257)
+    const double rh = 1.0 / h;
+    const double tx = dx * rh, ty = dy * rh;
+    const double nx = o == 0 ? ty : -ty, ny = o == 0 ? -tx : tx;
+    const double ge0 = G00 * nx + G10 * ny, ge1 = G01 * nx + G11 * ny;
+    const int kind = kindv[l], lf = lfv[l], f = fv[l];
+    double w0 = 0.0, w1 = 0.0, cp = 0.0;
+    if (kind == DGB_EDGE_INTERIOR) {
+      Geo gf;
+      if constexpr (bound) {
+        const double2 qo = po[l];
+        const double2 qa = pv[(l + 1) % 3];
+        const double2 qb = pv[(l + 2) % 3];
+        const double2 q0 = lf == 0 ? qo : (lf == 1 ? qa : qb);
+        const double2 q1 = lf == 1 ? qo : (lf == 2 ? qa : qb);
+        const double2 q2 = lf == 2 ? qo : (lf == 0 ? qa : qb);
+        gf = element_geo_coords(q0, q1, q2);
+      } else {
+        gf = element_geo_fast(P.nodes, vfv[l]);
+      }
+      double eps_e = eps;
+      if (P.prob.diffusion.kind == DGB_FIELD_PER_ELEMENT) {
+        const double ef = __ldg(P.prob.diffusion.per_element + f);
+        eps_e = ee < f ? 0.5 * (eps + ef) : 0.5 * (ef + eps);
+      }
+      const double base = 0.5 * h * eps_e;
+      w0 = base * ge0;
+      w1 = base * ge1;
+      const double cY0 = -base * (gf.G00 * nx + gf.G10 * ny);
+      const double cY1 = -base * (gf.G01 * nx + gf.G11 * ny);
+      const double cZ0 = -kappa * base * ge0;
+      const double cZ1 = -kappa * base * ge1;
+      const double sh = sigma_i * rh;
+      const double fl = FADD(FMUL(bf.p[0], nx), FMUL(bf.p[1], ny));
+      const double up = fl < 0.0 ? FMUL(h, fl) : 0.0;
+      cp = sh * (h * eps_e) - up;
+      const double cx = up - sh * (h * eps_e);
+      // K_ef = sum_p phi^l_p (x) b1_p + a2_p (x) phi^lf_(n-1-p)
+      const double* trm = tr + lf * (NQE * 3 * NL);
+      double pm[NQE][NL], b1[NQE][NL];
+#pragma unroll
+      for (int p = 0; p < NQE; ++p) {
+        const double cV = cx * P.t.x[L::EW + p];
+        const double* row = trm + (NQE - 1 - p) * 3 * NL;
+#pragma unroll
+        for (int j = 0; j < NL; ++j) {
+          const double fr = row[j], g0 = row[NL + j], g1 = row[2 * NL + j];
+          pm[p][j] = fr;
+          b1[p][j] = fma(cV, fr, fma(cY0, g0, cY1 * g1));
+        }
+      }
+      double* blk = myrow + slot_of[1 + l] * N2;
+#pragma unroll
+      for (int i = 0; i < NL; ++i) {
+        double r[NL];
+#pragma unroll
+        for (int j = 0; j < NL; ++j) r[j] = 0.0;
+#pragma unroll
+        for (int p = 0; p < NQE; ++p) {
+          const double a2 = fma(cZ0, P.t.x[L::EDW + ((l * NQE + p) * 2) * NL + i],
+                                cZ1 * P.t.x[L::EDW + ((l * NQE + p) * 2 + 1) * NL + i]);
+          const double ph = P.t.x[L::EPHI + (l * NQE + p) * NL + i];
+#pragma unroll
+          for (int j = 0; j < NL; ++j) r[j] = fma(ph, b1[p][j], fma(a2, pm[p][j], r[j]));
+        }
+#pragma unroll
+        for (int j = 0; j < NL; ++j) if (active) blk[i * NL + j] = r[j];
+      }
+    } else {
+      // boundary edge: diffusion (Dirichlet), inflow upwind, and the boundary RHS terms
+      double fls[NQE], gb[NQE];
+      bool inflow = false;
+#pragma unroll
+      for (int p = 0; p < NQE; ++p) {
+        const double tq = o == 0 ? P.t.x[L::ET + p] : 1.0 - P.t.x[L::ET + p];
+        const double px = FADD(A.x, FMUL(tq, dx));
+        const double py = FADD(A.y, FMUL(tq, dy));
+        fls[p] = FADD(FMUL(bf.p[0], nx), FMUL(bf.p[1], ny));
+        if (fls[p] < -1e-12 * fmax(1.0, hypot_dd(bf.p[0], bf.p[1]))) inflow = true;
+        gb[p] = scalar_point(kind == DGB_EDGE_NEUMANN ? P.prob.neumann : P.prob.dirichlet, px, py);
+      }
+      double cG[NQE], cH[NQE];
+      if (kind == DGB_EDGE_NEUMANN) {
+        const int edge = bound ? __ldg(P.element_edges + 3 * ee + l) : edgev[l];
+        if (inflow && !P.drop_neumann && active) {
+          atomicMax(P.err_edge, (P.epoch << 32) | (0xFFFFFFFFull - static_cast<unsigned>(edge)));
+        }
+#pragma unroll
+        for (int p = 0; p < NQE; ++p) {
+          cG[p] = FMUL(FMUL(P.t.x[L::EW + p], h), gb[p]);
+          cH[p] = 0.0;
+        }
+      } else {
+        const double base = h * eps;
+        w0 = base * ge0;
+        w1 = base * ge1;
+        const double sh = sigma_b * rh;
+        cp = sh * (h * eps) - ((inflow && fls[0] < 0.0) ? FMUL(h, fls[0]) : 0.0);
+#pragma unroll
+        for (int p = 0; p < NQE; ++p) {
+          const double w = FMUL(P.t.x[L::EW + p], h);
+          const double win = (inflow && fls[p] < 0.0) ? -FMUL(w, fls[p]) : 0.0;
+          const double wgd = w * gb[p];
+          cG[p] = wgd * (sh * eps) + win * gb[p];
+          cH[p] = wgd * (kappa * eps);
+        }
+      }
+#pragma unroll
+      for (int p = 0; p < NQE; ++p) {
+        const double h0 = cH[p] * ge0, h1 = cH[p] * ge1;
+#pragma unroll
+        for (int i = 0; i < NL; ++i) {
+          F[i] = fma(cG[p], P.t.x[L::EPHI + (l * NQE + p) * NL + i],
+                     fma(h0, P.t.x[L::EDPHI + ((l * NQE + p) * 2) * NL + i],
+                         fma(h1, P.t.x[L::EDPHI + ((l * NQE + p) * 2 + 1) * NL + i], F[i])));
+        }
+      }
+    }
+    // face terms of the diagonal block (the general kernel's order: W then P, per edge)
+#pragma unroll
+    for (int k = 0; k < N2; ++k) {
+      acc[k] = fma(w0, P.t.x[L::W + 2 * l * N2 + k], fma(w1, P.t.x[L::W + (2 * l + 1) * N2 + k], acc[k]));
+      acc[k] = fma(cp, P.t.x[L::P + l * N2 + k], acc[k]);
+    }
+  }
+  if (active) {
+#pragma unroll
+    for (int k = 0; k < N2; ++k) myrow[slot_of[0] * N2 + k] = acc[k];
+  }
+
+  // ---- RHS: the warp's contiguous slice in one bulk copy ------------------------------------------
+  {
+#pragma unroll
+    for (int i = 0; i < NL; ++i) srhs[lane * NL + i] = F[i];
+    __syncwarp();
+    const int e_first = blockIdx.x * blockDim.x + warp * 32;
+    const int n_here = min(32, P.row_end - P.row_begin - e_first);
+    double* dst = o_rhs + static_cast<long long>(e_first) * NL;
+    const int bulk = (n_here * NL) & ~1;
+    if (lane == 0 && bulk > 0) {
+      fence_smem_to_async();
+      bulk_store(dst, srhs, bulk * sizeof(double), P.evict_first);
+    }
+    for (int idx = bulk + lane; idx < n_here * NL; idx += 32) dst[idx] = srhs[idx];
+  }
+  // ---- the warp's row range: one bulk copy, unaligned head / tail by hand ----------------------------
+  __syncwarp();
+  {
+    const int n = (rp_last - rp_first) * N2;
+    double* dst = o_val + static_cast<long long>(rp_first) * N2;
+    const int head = rp_first & 1;
+    const int body = (n - head) & ~1;
+    if (lane == 0 && body > 0) {
+      fence_smem_to_async();
+      bulk_store(dst + head, srow + head, body * sizeof(double), P.evict_first);
+    }
+    if (lane == 1 && head) dst[0] = srow[0];
+    if (lane == 2 && head + body < n) dst[n - 1] = srow[n - 1];
+  }
+  if (lane == 0) bulk_wait_all();
+}
+
+}  // namespace v2
+}  // namespace dgb

@@ -291,6 +291,7 @@ constexpr int kGeo = 13;  // doubles per element: B(4) G(4) det ox oy eps alpha
 }  // namespace dgb
 
 #include "assemble_v2.cuh"
+#include "assemble_p1.cuh"
 #include "nonlinear.cuh"
 #include "postprocess.cuh"
 
@@ -1117,12 +1118,32 @@ void launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_prob
     }
   }
   auto kernel = dgb::v2::assemble_kernel<NL, NQV, NQE, BK, THREADS, MINB>;
-  static bool configured = false;
-  if (!configured) {
-    cuda_check(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(smem)),
+  size_t smem_bytes = smem;
+  if constexpr (NL == 3 && BK == 0) {
+    // P1, constant velocity: the stash-free kernel (assemble_p1.cuh); option MIN_BLOCKS = 11
+    // selects the general kernel for comparison
+    if (plan->minblocks != 11) {
+      using SP = dgb::v2::SmemP1<NQV, NQE>;
+      kernel = row_ptr_src ? dgb::v2::assemble_p1_kernel<NQV, NQE, THREADS, MINB, true>
+                           : dgb::v2::assemble_p1_kernel<NQV, NQE, THREADS, MINB, false>;
+      smem_bytes = sizeof(double) * (SP::kTr + (THREADS / 32) * SP::kWarp);
+    }
+  }
+  static size_t configured = 0;
+  if (std::max(smem_bytes, smem) > configured) {  // every kernel this instantiation may launch
+    const int bytes = static_cast<int>(std::max(smem_bytes, smem));
+    cuda_check(cudaFuncSetAttribute(dgb::v2::assemble_kernel<NL, NQV, NQE, BK, THREADS, MINB>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, bytes),
                "cudaFuncSetAttribute(v2)");
-    configured = true;
+    if constexpr (NL == 3 && BK == 0) {
+      cuda_check(cudaFuncSetAttribute(dgb::v2::assemble_p1_kernel<NQV, NQE, THREADS, MINB, true>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, bytes),
+                 "cudaFuncSetAttribute(p1)");
+      cuda_check(cudaFuncSetAttribute(dgb::v2::assemble_p1_kernel<NQV, NQE, THREADS, MINB, false>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, bytes),
+                 "cudaFuncSetAttribute(p1)");
+    }
+    configured = std::max(smem_bytes, smem);
   }
   const int grid = (out_row_end - out_row_begin + THREADS - 1) / THREADS;
   // Keep the node coordinates (gathered by every element and its neighbours, in random order
@@ -1130,7 +1151,7 @@ void launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_prob
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid, nb);
   cfg.blockDim = dim3(THREADS);
-  cfg.dynamicSmemBytes = smem;
+  cfg.dynamicSmemBytes = smem_bytes;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   int nattr = 0;
