@@ -12,6 +12,6 @@ CMD="python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline"
 $CMD > gpurun_out/plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv \
     --log-file gpurun_out/launches_c2.csv $CMD > gpurun_out/ncu1.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:assemble_kernel -s 3 -c 1 \
+ncu --set full --clock-control none --import-source on -k regex:assemble_ -s 3 -c 1 \
     -o gpurun_out/prof_c2 $CMD > gpurun_out/ncu2.log 2>&1
 for f in gpurun_out/*.err gpurun_out/ncu*.log; do echo "== $f"; tail -n 3 "$f"; done

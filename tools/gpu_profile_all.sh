@@ -15,7 +15,7 @@ for c in 2 3 4; do
     ncu --metrics gpu__time_duration.sum --clock-control none --csv \
         --log-file gpurun_out/launches_c2.csv $CMD > gpurun_out/ncu_launch.log 2>&1
   fi
-  ncu --set full --clock-control none --import-source on -k regex:assemble_kernel -s 1 -c 1 \
+  ncu --set full --clock-control none --import-source on -k regex:assemble_ -s 1 -c 1 \
       -o gpurun_out/prof_c$c $CMD > gpurun_out/ncu_c$c.log 2>&1
 done
 ls -la gpurun_out
