@@ -223,7 +223,7 @@ def run_ours(args, world, rank, local):
     spec = problems.config_problem(args.config, mesh.n_elements)
     params = [dgfem.config_parameters(cfg, m) for m in cfg.methods]
     begin, end = shard.row_range(mesh.n_elements, rank, world)
-    l2 = args.l2_policy if args.l2_policy >= 0 else (1 if cfg.permute else 2)  # measured
+    l2 = args.l2_policy if args.l2_policy >= 0 else 2  # measured: evict-first output (profiles/NOTES.md)
     shards = [shard.ShardAssembler(mesh, ref, spec, local, begin, end, bind=False)]
     shards[0].plan.set_option(capi.OPTION_L2_POLICY, l2)
     if not args.no_bind:
