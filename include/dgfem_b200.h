@@ -393,7 +393,7 @@ int dgb_assemble_nonlinear_host(const dgb_mesh_arrays* mesh, const dgb_reference
 typedef struct dgb_solve_options {
   double tolerance_scale;  /* stop at tolerance_scale * the contract bound (default 0.1)   */
   int32_t max_iterations;  /* total Krylov iterations (default 20000)                     */
-  int32_t restart;         /* GMRES(m) restart length m (default 60, <= 200)              */
+  int32_t restart;         /* GMRES(m) restart length m (default 30, <= 200)              */
 } dgb_solve_options;
 
 typedef struct dgb_solve_info { /* SolveInfo (sparse.hpp:55-59) + the Krylov counters      */

@@ -251,23 +251,120 @@ __global__ void newton_residual_kernel(double* __restrict__ res, const double* _
   if (i < n) res[i] += h[i] - f[i];
 }
 
+// h[j] += d[j], j < k (the second CGS pass into the Hessenberg column)
+__global__ void add_small_kernel(double* __restrict__ h, const double* __restrict__ d, int k) {
+  const int j = threadIdx.x;
+  if (j < k) h[j] += d[j];
+}
+
+// h_{k+1,k} = ||w||, v_{k+1} = w / ||w|| (zero on a happy breakdown); nrm2 = w . w on the device
+__global__ void normalize_kernel(double* __restrict__ v, const double* __restrict__ w,
+                                 const double* __restrict__ nrm2, double* __restrict__ hsub,
+                                 long long n) {
+  const double hn = sqrt(*nrm2);
+  const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i == 0) *hsub = hn;
+  if (i < n) v[i] = hn > 0.0 ? w[i] * (1.0 / hn) : 0.0;
+}
+
+// Givens rotations of Hessenberg column k (column-major, leading dimension ld) and the
+// right-hand side g; one thread.  res = |g[k+1]| (the GMRES residual estimate).
+__global__ void givens_kernel(double* __restrict__ H, int ld, double* __restrict__ cs,
+                              double* __restrict__ sn, double* __restrict__ g, int k,
+                              double* __restrict__ res) {
+  double* hk = H + static_cast<long long>(k) * ld;
+  for (int j = 0; j < k; ++j) {
+    const double t = cs[j] * hk[j] + sn[j] * hk[j + 1];
+    hk[j + 1] = -sn[j] * hk[j] + cs[j] * hk[j + 1];
+    hk[j] = t;
+  }
+  const double rr = hypot(hk[k], hk[k + 1]);
+  cs[k] = rr > 0 ? hk[k] / rr : 1.0;
+  sn[k] = rr > 0 ? hk[k + 1] / rr : 0.0;
+  hk[k] = rr;
+  hk[k + 1] = 0.0;
+  g[k + 1] = -sn[k] * g[k];
+  g[k] = cs[k] * g[k];
+  *res = fabs(g[k + 1]);
+}
+
+__global__ void set_scalar_kernel(double* p, double v) { *p = v; }
+
 unsigned grid_for(long long n) { return static_cast<unsigned>((n + kThreads - 1) / kThreads); }
 
 // ------------------------------------------------------------------------------ host side
+// Stream-ordered allocations from the device's default memory pool, kept cached across solves
+// (the pool's release threshold is raised once), so a repeated solve allocates nothing new.
+cudaStream_t& alloc_stream() {
+  static thread_local cudaStream_t st = nullptr;
+  return st;
+}
+
+void keep_pool_cached() {
+  static bool done = false;
+  if (done) return;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    unsigned long long keep = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  done = true;
+}
+
 struct DevBuf {
   void* p = nullptr;
+  cudaStream_t s = nullptr;
   DevBuf() = default;
-  explicit DevBuf(size_t bytes) { cuda_check(cudaMalloc(&p, std::max<size_t>(bytes, 16)), "cudaMalloc(solve)"); }
+  explicit DevBuf(size_t bytes) : s(alloc_stream()) {
+    keep_pool_cached();
+    cuda_check(cudaMallocAsync(&p, std::max<size_t>(bytes, 16), s), "cudaMallocAsync(solve)");
+  }
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
-  ~DevBuf() { if (p) cudaFree(p); }
+  ~DevBuf() { if (p) cudaFreeAsync(p, s); }
   template <typename T> T* as() const { return static_cast<T*>(p); }
 };
 
+// Pinned host scratch (one per thread, grown on demand): no cudaMallocHost per solve.  A nested
+// user (a Newton reducer alive during its inner solves) gets a private buffer.
+struct PinnedPool {
+  double* buf = nullptr;
+  size_t cap = 0;
+  int users = 0;
+};
+PinnedPool& pinned_pool() {
+  static thread_local PinnedPool pp;
+  return pp;
+}
 struct PinnedBuf {
   double* p = nullptr;
-  explicit PinnedBuf(size_t n) { cuda_check(cudaMallocHost(&p, std::max<size_t>(n, 1) * sizeof(double)), "cudaMallocHost"); }
-  ~PinnedBuf() { if (p) cudaFreeHost(p); }
+  bool own = false;
+  explicit PinnedBuf(size_t n) {
+    PinnedPool& pp = pinned_pool();
+    n = std::max<size_t>(n, 1);
+    if (pp.users == 0) {
+      if (pp.cap < n) {
+        if (pp.buf) cudaFreeHost(pp.buf);
+        pp.buf = nullptr;
+        pp.cap = 0;
+        cuda_check(cudaMallocHost(&pp.buf, n * sizeof(double)), "cudaMallocHost");
+        pp.cap = n;
+      }
+      p = pp.buf;
+    } else {
+      cuda_check(cudaMallocHost(&p, n * sizeof(double)), "cudaMallocHost");
+      own = true;
+    }
+    ++pp.users;
+  }
+  PinnedBuf(const PinnedBuf&) = delete;
+  PinnedBuf& operator=(const PinnedBuf&) = delete;
+  ~PinnedBuf() {
+    if (own) cudaFreeHost(p);
+    --pinned_pool().users;
+  }
 };
 
 // The operator pieces one solve needs, for block size NL.
@@ -329,6 +426,12 @@ struct Reducer {
     return host.p;
   }
   double dot(const double* a, const double* b, long long n) { return dots(a, 0, 1, b, n)[0]; }
+  // the same, left on the device: out[j] = V_j . w (no host round trip)
+  void dots_device(const double* V, long long ldv, int k, const double* w, long long n, double* out) {
+    multidot_partial_kernel<<<dim3(kRedBlocks, k), kThreads, 0, s>>>(V, ldv, w, n, partial.as<double>());
+    sum_partials_kernel<<<k, kThreads, 0, s>>>(partial.as<double>(), kRedBlocks, out);
+    cuda_check(cudaGetLastError(), "multidot");
+  }
   double absmax(const double* x, long long n) {
     absmax_partial_kernel<<<kRedBlocks, kThreads, 0, s>>>(x, n, partial.as<double>());
     cuda_check(cudaGetLastError(), "absmax");
@@ -363,6 +466,7 @@ void gmres_solve(const dgb_bsr* a, const double* b, double* x, const dgb_solve_o
                  dgb_solve_info* info, cudaStream_t s) {
   const int nl = a->block_dim, E = a->n_block_rows;
   const long long n = static_cast<long long>(E) * nl;
+  alloc_stream() = s;
   BsrOps A{a, nl, n, s};
   Reducer R(s);
   dgb_solve_info inf{};
@@ -374,6 +478,10 @@ void gmres_solve(const dgb_bsr* a, const double* b, double* x, const dgb_solve_o
   DevBuf dinv(sizeof(double) * n * nl), fail(sizeof(unsigned long long));
   DevBuf V(sizeof(double) * n * (m + 1)), z(sizeof(double) * n), w(sizeof(double) * n),
       r(sizeof(double) * n), hdev(sizeof(double) * (m + 1));
+  DevBuf Hd(sizeof(double) * (m + 1) * m), gd(sizeof(double) * (m + 1)), csd(sizeof(double) * m),
+      snd(sizeof(double) * m), nrm(sizeof(double)), resd(sizeof(double));
+  PinnedBuf est(1);
+  constexpr int kCheck = 4;
   cuda_check(cudaMemsetAsync(fail.p, 0xFF, sizeof(unsigned long long), s), "memset(fail)");
   A.diag_inverse(dinv.as<double>(), fail.as<unsigned long long>());
   unsigned long long bad = 0;
@@ -395,53 +503,46 @@ void gmres_solve(const dgb_bsr* a, const double* b, double* x, const dgb_solve_o
   };
   double beta = residual();
   double x_norm = std::sqrt(R.dot(x, x, n));
-  std::vector<double> H(static_cast<size_t>(m + 1) * m), cs(m), sn(m), g(m + 1), y(m);
+  std::vector<double> H(static_cast<size_t>(m + 1) * m), g(m + 1), y(m);
   int its = 0, restarts = 0;
   while (true) {
     const double bound = 1e-10 * (a_fro * x_norm + b_norm);
     const double target = o.tolerance_scale * bound;
     if (beta <= target || its >= o.max_iterations) break;
     scale_kernel<<<grid_for(n), kThreads, 0, s>>>(Vp, r.as<double>(), 1.0 / beta, n);
-    std::fill(g.begin(), g.end(), 0.0);
-    g[0] = beta;
+    // Arnoldi on the device: Hessenberg columns, rotations and g live in HBM; the host reads
+    // the residual estimate every kCheck steps (extra steps past convergence only lower it)
+    cuda_check(cudaMemsetAsync(gd.p, 0, sizeof(double) * (m + 1), s), "memset(g)");
+    set_scalar_kernel<<<1, 1, 0, s>>>(gd.as<double>(), beta);
     int k = 0;
-    for (; k < m && its < o.max_iterations; ++k) {
+    bool done = false;
+    for (; k < m && its < o.max_iterations && !done; ++k) {
       ++its;
       double* vk = Vp + static_cast<long long>(k) * n;
       double* vn = Vp + static_cast<long long>(k + 1) * n;
+      double* hk = Hd.as<double>() + static_cast<long long>(k) * (m + 1);
       A.precond(dinv.as<double>(), vk, z.as<double>());
       A.spmv(z.as<double>(), w.as<double>());
-      double* hk = &H[static_cast<size_t>(k) * (m + 1)];
-      for (int pass = 0; pass < 2; ++pass) {  // CGS2
-        const double* h = R.dots(Vp, n, k + 1, w.as<double>(), n);
-        cuda_check(cudaMemcpyAsync(hdev.p, h, sizeof(double) * (k + 1), cudaMemcpyHostToDevice, s), "H2D(h)");
-        subtract_combo_kernel<<<grid_for(n), kThreads, 0, s>>>(w.as<double>(), Vp, n, hdev.as<double>(), k + 1, n);
-        cuda_check(cudaGetLastError(), "subtract_combo_kernel");
-        for (int j = 0; j <= k; ++j) hk[j] = (pass == 0 ? 0.0 : hk[j]) + h[j];
-      }
-      const double hn = std::sqrt(R.dot(w.as<double>(), w.as<double>(), n));
-      hk[k + 1] = hn;
-      if (hn > 0.0) {
-        scale_kernel<<<grid_for(n), kThreads, 0, s>>>(vn, w.as<double>(), 1.0 / hn, n);
-      }
-      for (int j = 0; j < k; ++j) {  // previous Givens rotations
-        const double t = cs[j] * hk[j] + sn[j] * hk[j + 1];
-        hk[j + 1] = -sn[j] * hk[j] + cs[j] * hk[j + 1];
-        hk[j] = t;
-      }
-      const double rr = std::hypot(hk[k], hk[k + 1]);
-      cs[k] = rr > 0 ? hk[k] / rr : 1.0;
-      sn[k] = rr > 0 ? hk[k + 1] / rr : 0.0;
-      hk[k] = rr;
-      hk[k + 1] = 0.0;
-      g[k + 1] = -sn[k] * g[k];
-      g[k] = cs[k] * g[k];
-      if (std::fabs(g[k + 1]) <= target || hn == 0.0) {
-        ++k;
-        break;
+      R.dots_device(Vp, n, k + 1, w.as<double>(), n, hk);                          // CGS pass 1
+      subtract_combo_kernel<<<grid_for(n), kThreads, 0, s>>>(w.as<double>(), Vp, n, hk, k + 1, n);
+      R.dots_device(Vp, n, k + 1, w.as<double>(), n, hdev.as<double>());           // CGS pass 2
+      subtract_combo_kernel<<<grid_for(n), kThreads, 0, s>>>(w.as<double>(), Vp, n, hdev.as<double>(), k + 1, n);
+      add_small_kernel<<<1, kMaxRestart + 1, 0, s>>>(hk, hdev.as<double>(), k + 1);
+      R.dots_device(w.as<double>(), 0, 1, w.as<double>(), n, nrm.as<double>());
+      normalize_kernel<<<grid_for(n), kThreads, 0, s>>>(vn, w.as<double>(), nrm.as<double>(), hk + k + 1, n);
+      givens_kernel<<<1, 1, 0, s>>>(Hd.as<double>(), m + 1, csd.as<double>(), snd.as<double>(),
+                                    gd.as<double>(), k, resd.as<double>());
+      cuda_check(cudaGetLastError(), "arnoldi step");
+      if ((k + 1) % kCheck == 0 || k + 1 == m || its >= o.max_iterations) {
+        cuda_check(cudaMemcpyAsync(est.p, resd.p, sizeof(double), cudaMemcpyDeviceToHost, s), "D2H(res)");
+        cuda_check(cudaStreamSynchronize(s), "cudaStreamSynchronize(res)");
+        done = *est.p <= target;
       }
     }
-    // y = H(0:k, 0:k)^-1 g, then x += M^-1 (V y)
+    // y = H(0:k, 0:k)^-1 g (host, one copy per cycle), then x += M^-1 (V y)
+    cuda_check(cudaMemcpyAsync(H.data(), Hd.p, sizeof(double) * (m + 1) * k, cudaMemcpyDeviceToHost, s), "D2H(H)");
+    cuda_check(cudaMemcpyAsync(g.data(), gd.p, sizeof(double) * (m + 1), cudaMemcpyDeviceToHost, s), "D2H(g)");
+    cuda_check(cudaStreamSynchronize(s), "cudaStreamSynchronize(H)");
     for (int i = k - 1; i >= 0; --i) {
       double t = g[i];
       for (int j = i + 1; j < k; ++j) t -= H[static_cast<size_t>(j) * (m + 1) + i] * y[j];
@@ -479,7 +580,7 @@ void dgb_solve_options_default(dgb_solve_options* opt) {
   if (!opt) return;
   opt->tolerance_scale = 0.1;
   opt->max_iterations = 20000;
-  opt->restart = 60;
+  opt->restart = 30;
 }
 
 void dgb_newton_config_default(dgb_newton_config* cfg) {
@@ -517,6 +618,7 @@ int dgb_newton_solve(dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_bsr*
     const int nl = k->block_dim, E = k->n_block_rows;
     if (E != mesh->n_elements) throw dgb::Error(DGB_STATUS_DIMENSION_MISMATCH, "system / mesh size mismatch");
     const long long n = static_cast<long long>(E) * nl, nvals = k->nnzb * static_cast<long long>(nl) * nl;
+    alloc_stream() = s;
     DevBuf h(sizeof(double) * n), res(sizeof(double) * n), neg(sizeof(double) * n), step(sizeof(double) * n),
         jw(sizeof(double) * n), hjv(sizeof(double) * E * nl * nl), hjr(sizeof(int32_t) * (E + 1)),
         hjc(sizeof(int32_t) * std::max(E, 1)), jval(sizeof(double) * nvals);
