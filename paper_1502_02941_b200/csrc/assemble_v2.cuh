@@ -54,7 +54,9 @@ struct Tab {
 };
 
 // The tensor-core kernel (P2, constant velocity) takes the compact parameter block.
-constexpr bool full_tensors(int NL, int BK) { return !(NL == 6 && BK == 0); }
+constexpr bool full_tensors(int NL, int BK) {
+  return !((NL == 6 && BK == 0) || (NL == 10 && (BK == 0 || BK == 1)));
+}
 
 // One assembly of a launch: its penalty parameters and its outputs.  A launch assembles
 // n_batch parameter sets of the same mesh and problem (grid.y = n_batch; the tensor-core
@@ -209,21 +211,29 @@ struct Smem {
   // FP64 tensor-core (DMMA m8n8k4) path for P2 with constant velocity: every block (diagonal:
   // 15 terms; neighbour: 5 terms x 3 possible lf, zero-padded) is one [32 x 16] . [16 x 36]
   // product whose fragments are stored straight to global -- no block staging at all
-  static constexpr bool kMma = NL == 6 && BK == 0;
-  static constexpr int kTerms = 15;                              // S0 S1 S2 M T0 T1 W[6] P[3]
+  // Tensor-core path: P2 with constant velocity, P3 with constant or affine velocity.
+  //  P-form (constant b): diagonal S0 S1 S2 M T0 T1 W[6] P[3] (15), neighbour X Y0 Y1 Z0 Z1 (5)
+  //  U-form (affine b):   diagonal S0 S1 S2 M T0 T1 TA[4] W[6] U[3][NQE] (22 + 3 NQE),
+  //                       neighbour X[NQE] Y0 Y1 Z0 Z1 (4 + NQE) -- per-point upwind terms
+  static constexpr bool kMma = (NL == 6 && BK == 0) || (NL == 10 && (BK == 0 || BK == 1));
+  static constexpr bool kUForm = BK == 1;
+  static constexpr int kTerms = kUForm ? 16 + 3 * NQE : 15;
+  static constexpr int kOffT = kUForm ? 4 + NQE : 5;            // neighbour terms (K <= 8)
+  static constexpr int kWRow = kUForm ? 10 : 6;                 // first W row of the diagonal
   static constexpr int kKS = (kTerms + 3) / 4, kNT = (N2 + 7) / 8;
+  static constexpr int kDRows = 4 * kKS;                         // diagonal rows (zero padded)
   static constexpr int kCT = 36;                                 // coefficient table stride [k][lane]
   static constexpr int kStage = kMma ? 0 : (kRowMode ? ((32 * 4 * N2 + 2 + 1) & ~1) : 32 * SS);
   // MMA path: the stash is the A operand itself, [term][lane] rows of stride kCT: diagonal
   // terms 0..15 (15 = zero pad), then the neighbour terms [l][X Y0 Y1 Z0 Z1]
-  static constexpr int kStash = kMma ? (16 + 15) * kCT : 3 * NF * 32;
+  static constexpr int kStash = kMma ? (kDRows + 3 * kOffT) * kCT : 3 * NF * 32;
   static constexpr int kMeta = (3 * 32 + (kMma ? 48 : 0)) / 2; // 3 ints per lane (+ MMA row map)
   static constexpr int kTrig = BK == 2 ? 2 * NQV * 32 : 0;     // pointwise transport weights
   static constexpr int kRhs = (32 * NL + 1) & ~1;               // packed RHS slice of the warp
   static constexpr int kWarp = kStage + kStash + kMeta + kTrig + kRhs;
   static constexpr int kTr = (3 * NQE * 3 * NL + 1) & ~1;      // trace table (per CTA)
   static constexpr int kFragTile = kKS * kNT * 32;               // one B operand, fragment order
-  // neighbour operands per (l, lf): K = 8 (5 terms), fragment order [ks 2][nt][lane]
+  // neighbour operands per (l, lf): K = 8 (kOffT terms), fragment order [ks 2][nt][lane]
   static constexpr int kOffTile = 2 * kNT * 32;
   static constexpr int kBt = kMma ? kFragTile + 9 * kOffTile : 0;
 };
@@ -347,9 +357,18 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
   double* srhs = sq + SM::kTrig;                     // [32][NL] packed RHS
   auto K = [&](int f, int l) -> double& {
     if constexpr (SM::kMma) {
-      constexpr int CT = SM::kCT;
-      const int row = f == F_W0 ? 6 + 2 * l : f == F_W1 ? 7 + 2 * l : f == F_P ? 12 + l
-                    : 16 + 5 * l + (f == F_X ? 0 : f - F_Y0 + 1);
+      constexpr int CT = SM::kCT, OB = SM::kDRows;  // OB: first neighbour row
+      int row;
+      if constexpr (SM::kUForm) {
+        // F_U + p: diagonal point term U[l][p]; F_U + NQE + p: neighbour point term X[p]
+        row = f == F_W0 ? SM::kWRow + 2 * l : f == F_W1 ? SM::kWRow + 1 + 2 * l
+            : (f >= F_U && f < F_U + NQE) ? 16 + l * NQE + (f - F_U)
+            : f >= F_U + NQE ? OB + SM::kOffT * l + (f - F_U - NQE)
+            : OB + SM::kOffT * l + NQE + (f - F_Y0);
+      } else {
+        row = f == F_W0 ? 6 + 2 * l : f == F_W1 ? 7 + 2 * l : f == F_P ? 12 + l
+            : OB + 5 * l + (f == F_X ? 0 : f - F_Y0 + 1);
+      }
       return sk[row * CT + lane];
     } else {
       return sk[(f * 3 + l) * 32 + lane];
@@ -559,7 +578,7 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
     }
     K(F_W0, l) = w0;
     K(F_W1, l) = w1;
-    K(F_P, l) = cp;
+    if constexpr (!SM::kUForm) K(F_P, l) = cp;  // U-form: per-point terms instead
     K(F_Y0, l) = y0;
     K(F_Y1, l) = y1;
     K(F_Z0, l) = z0;
@@ -660,10 +679,11 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
     if constexpr (SM::kMma) {
       // D[32 elements x 36 entries] = C[32 x 16 coefficients] . T[16 x 36] on the FP64 tensor
       // cores, stored from the fragments
-      const double cv[6] = {cD0, cD1, cD2, cR, cC0, cC1};
+      const double cv[10] = {cD0, cD1, cD2, cR, cC0, cC1, cA[0], cA[1], cA[2], cA[3]};
 #pragma unroll
-      for (int k = 0; k < 6; ++k) sk[k * SM::kCT + lane] = cv[k];
-      sk[15 * SM::kCT + lane] = 0.0;
+      for (int k = 0; k < (SM::kUForm ? 10 : 6); ++k) sk[k * SM::kCT + lane] = cv[k];
+#pragma unroll
+      for (int k = SM::kTerms; k < SM::kDRows; ++k) sk[k * SM::kCT + lane] = 0.0;  // K padding
       __syncwarp();
       const int g = lane >> 2, t = lane & 3;
       if (!(P.ablate & 8)) {
@@ -801,14 +821,14 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
       }
       __syncwarp();
       const long long my_base = store ? static_cast<long long>(rp + slot) * N2 : -1LL;
-      const double* so = sk + (16 + 5 * l) * SM::kCT;
+      const double* so = sk + (SM::kDRows + SM::kOffT * l) * SM::kCT;
       // class-major: each lf's operand is loaded once into registers, and the next tile's
       // row operands are fetched while the current tile's products run
       auto tile_rows = [&](int r, double& a0, double& a1, long long& bm) {
         const int src = pmap[8 * r + g];
         const int sl = src < 0 ? 0 : src;
         a0 = src < 0 ? 0.0 : so[t * SM::kCT + sl];
-        a1 = (src < 0 || t != 0) ? 0.0 : so[4 * SM::kCT + sl];
+        a1 = (src < 0 || 4 + t >= SM::kOffT) ? 0.0 : so[(4 + t) * SM::kCT + sl];
         bm = __shfl_sync(0xffffffffu, my_base, sl);
         if (src < 0) bm = -1;
       };

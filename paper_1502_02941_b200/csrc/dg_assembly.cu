@@ -1078,22 +1078,39 @@ void launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_prob
         const int ln = r & 31, tile = r >> 5;
         const int ks = tile / SM::kNT, nt = tile - ks * SM::kNT;
         const int k = 4 * ks + (ln & 3), n = 8 * nt + (ln >> 2);
-        if (k >= (diag ? SM::kTerms : 5) || n >= N2) continue;
+        if (k >= (diag ? SM::kTerms : SM::kOffT) || n >= N2) continue;
+        const int bi = n / NL, bj = n % NL;
         if (which == 0) {
-          int off;
-          if (k < 3) off = L::S + k * N2;
-          else if (k == 3) off = L::M;
-          else if (k < 6) off = L::T + (k - 4) * N2;
-          else if (k < 12) off = -1;  // W = kappa Q^T - Q for this set's kappa
-          else off = L::P + (k - 12) * N2;
-          if (off >= 0) {
-            hb[i] = x[off + n];
-          } else {
-            const int la = k - 6, bi = n / NL, bj = n % NL;
+          // diagonal terms: S0 S1 S2 M T0 T1 [TA0..3] W[6] then P[3] (P-form) / U[3][NQE] (U-form)
+          const int kw = SM::kWRow;
+          if (k < 3) {
+            hb[i] = x[L::S + k * N2 + n];
+          } else if (k == 3) {
+            hb[i] = x[L::M + n];
+          } else if (k < 6) {
+            hb[i] = x[L::T + (k - 4) * N2 + n];
+          } else if (k < kw) {
+            hb[i] = x[L::TA + (k - 6) * N2 + n];
+          } else if (k < kw + 6) {  // W = kappa Q^T - Q for this set's kappa
+            const int la = k - kw;
             hb[i] = kap * h[V.Q + la * N2 + bj * NL + bi] - h[V.Q + la * N2 + bi * NL + bj];
+          } else if constexpr (SM::kUForm) {
+            const int l = (k - kw - 6) / NQE, p = (k - kw - 6) % NQE;
+            hb[i] = ephi(l, p, bi) * ephi(l, p, bj);  // U[l][p] = phi^l_p (x) phi^l_p
+          } else {
+            hb[i] = x[L::P + (k - kw - 6) * N2 + n];
           }
         } else {
-          const int l = (which - 1) / 3, lf = (which - 1) % 3, term = k, bi = n / NL, bj = n % NL;
+          // neighbour terms of (l, lf): P-form X Y0 Y1 Z0 Z1; U-form X[p] (per point) Y0 Y1 Z0 Z1
+          const int l = (which - 1) / 3, lf = (which - 1) % 3;
+          int term = k;
+          if constexpr (SM::kUForm) {
+            if (k < NQE) {
+              hb[i] = ephi(l, k, bi) * ephi(lf, NQE - 1 - k, bj);  // X[p], point weight in cV
+              continue;
+            }
+            term = k - NQE + 1;  // Y0 Y1 Z0 Z1 as terms 1..4 below
+          }
           double acc = 0.0;
           for (int p = 0; p < NQE; ++p) {
             const int q = NQE - 1 - p;
@@ -1204,8 +1221,8 @@ bool try_launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_
   DGB_V2(3, 6, 2, 2, 128, 4)
   DGB_V2(6, 7, 3, 0, 128, 4)
   DGB_V2(6, 12, 3, 0, 128, 4)
-  DGB_V2(10, 16, 4, 0, 160, 1)
-  DGB_V2(10, 16, 4, 1, 160, 1)
+  DGB_V2(10, 16, 4, 0, 128, 2)
+  DGB_V2(10, 16, 4, 1, 128, 2)
 #undef DGB_V2
   return false;
 }
@@ -1530,7 +1547,9 @@ int dgb_assemble_batch(dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_pr
                      plan->bound_begin == row_begin && plan->bound_end == row_end;
   // one launch for all parameter sets: the tensor-core P2 kernel on a bound mesh
   const bool one_launch = n > 1 && n <= dgb::v2::kMaxBatch && bound && same_drop && E > 0 &&
-                          plan->nl == 6 && problem->advection.kind == DGB_VEC_CONSTANT &&
+                          ((plan->nl == 6 && problem->advection.kind == DGB_VEC_CONSTANT) ||
+                           (plan->nl == 10 && plan->nqv == 16 && plan->nqe == 4 &&
+                            problem->advection.kind != DGB_VEC_TRIG)) &&
                           !plan->force_generic;
   if (one_launch) {
     // validate exactly as a single assembly would (and reject mismatched outputs)
