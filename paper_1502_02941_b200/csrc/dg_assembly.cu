@@ -1221,8 +1221,8 @@ bool try_launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_
   DGB_V2(3, 6, 2, 2, 128, 4)
   DGB_V2(6, 7, 3, 0, 128, 4)
   DGB_V2(6, 12, 3, 0, 128, 4)
-  DGB_V2(10, 16, 4, 0, 128, 2)
-  DGB_V2(10, 16, 4, 1, 128, 2)
+  DGB_V2(10, 16, 4, 0, 128, 3)  // measured: 168 registers, 12 warps/SM (C3 81% of roofline)
+  DGB_V2(10, 16, 4, 1, 128, 3)
 #undef DGB_V2
   return false;
 }
