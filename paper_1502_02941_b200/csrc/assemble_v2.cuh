@@ -55,7 +55,7 @@ struct Tab {
 
 // The tensor-core kernel (P2, constant velocity) takes the compact parameter block.
 constexpr bool full_tensors(int NL, int BK) {
-  return !((NL == 6 && BK == 0) || (NL == 10 && (BK == 0 || BK == 1)));
+  return !((NL == 6 && BK == 0) || (NL == 10 && (BK == 0 || BK == 1)) || (NL == 15 && BK == 2));
 }
 
 // One assembly of a launch: its penalty parameters and its outputs.  A launch assembles
@@ -207,7 +207,10 @@ struct Smem {
   static constexpr int NF = BK == 0 ? 8 : 7 + 2 * NQE;         // stashed coefficients per edge
   // even N2: one staged block per lane (bulk-copied per lane); odd N2 (P1): the warp's whole
   // contiguous row range (<= 4 blocks per lane), bulk-copied once per warp
-  static constexpr bool kRowMode = N2 % 2 == 1;
+  // (the tensor-core path writes from fragments: never row mode, whatever N2's parity)
+  static constexpr bool kRowMode = N2 % 2 == 1 &&
+                                   !((NL == 6 && BK == 0) || (NL == 10 && (BK == 0 || BK == 1)) ||
+                                     (NL == 15 && BK == 2));
   // FP64 tensor-core (DMMA m8n8k4) path for P2 with constant velocity: every block (diagonal:
   // 15 terms; neighbour: 5 terms x 3 possible lf, zero-padded) is one [32 x 16] . [16 x 36]
   // product whose fragments are stored straight to global -- no block staging at all
@@ -215,12 +218,18 @@ struct Smem {
   //  P-form (constant b): diagonal S0 S1 S2 M T0 T1 W[6] P[3] (15), neighbour X Y0 Y1 Z0 Z1 (5)
   //  U-form (affine b):   diagonal S0 S1 S2 M T0 T1 TA[4] W[6] U[3][NQE] (22 + 3 NQE),
   //                       neighbour X[NQE] Y0 Y1 Z0 Z1 (4 + NQE) -- per-point upwind terms
-  static constexpr bool kMma = (NL == 6 && BK == 0) || (NL == 10 && (BK == 0 || BK == 1));
-  static constexpr bool kUForm = BK == 1;
-  static constexpr int kTerms = kUForm ? 16 + 3 * NQE : 15;
-  static constexpr int kOffT = kUForm ? 4 + NQE : 5;            // neighbour terms (K <= 8)
-  static constexpr int kWRow = kUForm ? 10 : 6;                 // first W row of the diagonal
+  //  T-form (trigonometric b, P4): diagonal S0 S1 S2 M TQ[NQV][2] W[6] U[3][NQE], the
+  //                       per-point transport phi_q (x) d_a phi_q as 2 NQV rank-1 operands
+  static constexpr bool kMma = (NL == 6 && BK == 0) || (NL == 10 && (BK == 0 || BK == 1)) ||
+                               (NL == 15 && BK == 2);
+  static constexpr bool kTForm = BK == 2;
+  static constexpr bool kUForm = BK == 1 || BK == 2;            // per-point upwind terms
+  static constexpr int kTerms = kTForm ? 4 + 2 * NQV + 6 + 3 * NQE : (kUForm ? 16 + 3 * NQE : 15);
+  static constexpr int kOffT = kUForm ? 4 + NQE : 5;            // neighbour terms
+  static constexpr int kWRow = kTForm ? 4 + 2 * NQV : (kUForm ? 10 : 6);  // first W row
+  static constexpr int kURow = kWRow + 6;                       // first U row (U-/T-form)
   static constexpr int kKS = (kTerms + 3) / 4, kNT = (N2 + 7) / 8;
+  static constexpr int kKO = (kOffT + 3) / 4;                   // neighbour k-steps
   static constexpr int kDRows = 4 * kKS;                         // diagonal rows (zero padded)
   static constexpr int kCT = 36;                                 // coefficient table stride [k][lane]
   static constexpr int kStage = kMma ? 0 : (kRowMode ? ((32 * 4 * N2 + 2 + 1) & ~1) : 32 * SS);
@@ -228,13 +237,13 @@ struct Smem {
   // terms 0..15 (15 = zero pad), then the neighbour terms [l][X Y0 Y1 Z0 Z1]
   static constexpr int kStash = kMma ? (kDRows + 3 * kOffT) * kCT : 3 * NF * 32;
   static constexpr int kMeta = (3 * 32 + (kMma ? 48 : 0)) / 2; // 3 ints per lane (+ MMA row map)
-  static constexpr int kTrig = BK == 2 ? 2 * NQV * 32 : 0;     // pointwise transport weights
+  static constexpr int kTrig = BK == 2 && !kMma ? 2 * NQV * 32 : 0;  // pointwise transport weights
   static constexpr int kRhs = (32 * NL + 1) & ~1;               // packed RHS slice of the warp
   static constexpr int kWarp = kStage + kStash + kMeta + kTrig + kRhs;
   static constexpr int kTr = (3 * NQE * 3 * NL + 1) & ~1;      // trace table (per CTA)
   static constexpr int kFragTile = kKS * kNT * 32;               // one B operand, fragment order
-  // neighbour operands per (l, lf): K = 8 (kOffT terms), fragment order [ks 2][nt][lane]
-  static constexpr int kOffTile = 2 * kNT * 32;
+  // neighbour operands per (l, lf): K = 4 kKO (kOffT terms), fragment order [ks][nt][lane]
+  static constexpr int kOffTile = kKO * kNT * 32;
   static constexpr int kBt = kMma ? kFragTile + 9 * kOffTile : 0;
 };
 
@@ -267,6 +276,22 @@ __device__ __forceinline__ void store_pair(double* g, double a, double b, unsign
   asm volatile("st.global.L1::no_allocate.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;\n"
                :: "l"(g), "d"(a), "d"(b), "l"(pol) : "memory");
 }
+__device__ __forceinline__ void store_one(double* g, double a, unsigned long long pol) {
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.f64 [%0], %1, %2;\n"
+               :: "l"(g), "d"(a), "l"(pol) : "memory");
+}
+// Entries n0, n0 + 1 of an element block at `blk`: one 16-byte store when N2 is even (block
+// starts 16-byte aligned), two 8-byte stores otherwise; entries past N2 are padding.
+template <int N2>
+__device__ __forceinline__ void store_entries(double* blk, int n0, double a, double b,
+                                              unsigned long long pol) {
+  if constexpr (N2 % 2 == 0) {
+    if (N2 % 8 == 0 || n0 < N2) store_pair(blk + n0, a, b, pol);
+  } else {
+    if (n0 < N2) store_one(blk + n0, a, pol);
+    if (n0 + 1 < N2) store_one(blk + n0 + 1, b, pol);
+  }
+}
 
 // One warp-wide block product on the FP64 tensor cores: D[32 elements x N2] = C . B, where
 // a_at(m, ks) returns C[8 m + g][4 ks + t] for this lane (g, t) and B is a fragment-ordered
@@ -279,11 +304,15 @@ __device__ __forceinline__ void mma_block_store(AF a_at, const double* __restric
                                                 long long base, double* val, int lane,
                                                 unsigned long long pol) {
   const int g = lane >> 2, t = lane & 3;
-  double af[4][KS];
+  // small K: the A fragments stay in registers across the n-tiles; large K (P4): re-read
+  constexpr bool kKeepA = KS <= 7;
+  double af[4][kKeepA ? KS : 1];
+  if constexpr (kKeepA) {
 #pragma unroll
-  for (int m = 0; m < 4; ++m) {
+    for (int m = 0; m < 4; ++m) {
 #pragma unroll
-    for (int ks = 0; ks < KS; ++ks) af[m][ks] = a_at(m, ks);
+      for (int ks = 0; ks < KS; ++ks) af[m][ks] = a_at(m, ks);
+    }
   }
   long long bm[4];
 #pragma unroll
@@ -298,8 +327,10 @@ __device__ __forceinline__ void mma_block_store(AF a_at, const double* __restric
     for (int m = 0; m < 4; ++m) {
       double d0 = 0.0, d1 = 0.0;
 #pragma unroll
-      for (int ks = 0; ks < KS; ++ks) dmma_8x8x4(d0, d1, af[m][ks], bf[ks]);
-      if ((N2 % 8 == 0 || n0 < N2) && bm[m] >= 0) store_pair(val + bm[m] + n0, d0, d1, pol);
+      for (int ks = 0; ks < KS; ++ks) {
+        dmma_8x8x4(d0, d1, kKeepA ? af[m][kKeepA ? ks : 0] : a_at(m, ks), bf[ks]);
+      }
+      if (bm[m] >= 0) store_entries<N2>(val + bm[m], n0, d0, d1, pol);
     }
   }
 }
@@ -362,7 +393,7 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
       if constexpr (SM::kUForm) {
         // F_U + p: diagonal point term U[l][p]; F_U + NQE + p: neighbour point term X[p]
         row = f == F_W0 ? SM::kWRow + 2 * l : f == F_W1 ? SM::kWRow + 1 + 2 * l
-            : (f >= F_U && f < F_U + NQE) ? 16 + l * NQE + (f - F_U)
+            : (f >= F_U && f < F_U + NQE) ? SM::kURow + l * NQE + (f - F_U)
             : f >= F_U + NQE ? OB + SM::kOffT * l + (f - F_U - NQE)
             : OB + SM::kOffT * l + NQE + (f - F_Y0);
       } else {
@@ -429,8 +460,13 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
       if constexpr (TRIG) {
         double bx, by;
         velocity_k<BK>(bf, px, py, bx, by);
-        sq[(2 * q) * 32 + lane] = dw * (G00 * bx + G10 * by);
-        sq[(2 * q + 1) * 32 + lane] = dw * (G01 * bx + G11 * by);
+        if constexpr (SM::kMma) {  // T-form: the transport coefficients are A-operand rows
+          sk[(4 + 2 * q) * SM::kCT + lane] = dw * (G00 * bx + G10 * by);
+          sk[(4 + 2 * q + 1) * SM::kCT + lane] = dw * (G01 * bx + G11 * by);
+        } else {
+          sq[(2 * q) * 32 + lane] = dw * (G00 * bx + G10 * by);
+          sq[(2 * q + 1) * 32 + lane] = dw * (G01 * bx + G11 * by);
+        }
       }
     }
   }
@@ -681,7 +717,7 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
       // cores, stored from the fragments
       const double cv[10] = {cD0, cD1, cD2, cR, cC0, cC1, cA[0], cA[1], cA[2], cA[3]};
 #pragma unroll
-      for (int k = 0; k < (SM::kUForm ? 10 : 6); ++k) sk[k * SM::kCT + lane] = cv[k];
+      for (int k = 0; k < (SM::kTForm ? 4 : (SM::kUForm ? 10 : 6)); ++k) sk[k * SM::kCT + lane] = cv[k];
 #pragma unroll
       for (int k = SM::kTerms; k < SM::kDRows; ++k) sk[k * SM::kCT + lane] = 0.0;  // K padding
       __syncwarp();
@@ -824,40 +860,53 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
       const double* so = sk + (SM::kDRows + SM::kOffT * l) * SM::kCT;
       // class-major: each lf's operand is loaded once into registers, and the next tile's
       // row operands are fetched while the current tile's products run
-      auto tile_rows = [&](int r, double& a0, double& a1, long long& bm) {
+      constexpr int KO = SM::kKO;
+      auto tile_rows = [&](int r, double (&aa)[KO], long long& bm) {
         const int src = pmap[8 * r + g];
         const int sl = src < 0 ? 0 : src;
-        a0 = src < 0 ? 0.0 : so[t * SM::kCT + sl];
-        a1 = (src < 0 || 4 + t >= SM::kOffT) ? 0.0 : so[(4 + t) * SM::kCT + sl];
+#pragma unroll
+        for (int ks = 0; ks < KO; ++ks) {
+          aa[ks] = (src < 0 || 4 * ks + t >= SM::kOffT) ? 0.0 : so[(4 * ks + t) * SM::kCT + sl];
+        }
         bm = __shfl_sync(0xffffffffu, my_base, sl);
         if (src < 0) bm = -1;
       };
-      double a0, a1;
+      double aa[KO];
       long long bm;
-      if (ntiles > 0) tile_rows(0, a0, a1, bm);
+      if (ntiles > 0) tile_rows(0, aa, bm);
+      // small operands (P2, P3): the class's B fragments live in registers across its tiles
+      constexpr bool kPreload = KO * SM::kNT <= 26;
 #pragma unroll
       for (int v = 0; v < 3; ++v) {
         const int tb = v == 0 ? 0 : (v == 1 ? t1 : t2), te = v == 0 ? t1 : (v == 1 ? t2 : ntiles);
         if (tb == te) continue;
         const double* fr = o_bfrag + SM::kFragTile + (l * 3 + v) * SM::kOffTile + lane;
-        double bv[2][SM::kNT];
+        double bv[kPreload ? KO : 1][kPreload ? SM::kNT : 1];
+        if constexpr (kPreload) {
 #pragma unroll
-        for (int nt = 0; nt < SM::kNT; ++nt) {
-          bv[0][nt] = __ldg(fr + nt * 32);
-          bv[1][nt] = __ldg(fr + (SM::kNT + nt) * 32);
+          for (int nt = 0; nt < SM::kNT; ++nt) {
+#pragma unroll
+            for (int ks = 0; ks < KO; ++ks) bv[ks][nt] = __ldg(fr + (ks * SM::kNT + nt) * 32);
+          }
         }
 #pragma unroll 1
         for (int r = tb; r < te; ++r) {
-          const double c0 = a0, c1 = a1;
-          const long long cb = bm;
-          if (r + 1 < ntiles) tile_rows(r + 1, a0, a1, bm);
+          double ca[KO];
 #pragma unroll
+          for (int ks = 0; ks < KO; ++ks) ca[ks] = aa[ks];
+          const long long cb = bm;
+          if (r + 1 < ntiles) tile_rows(r + 1, aa, bm);
+#pragma unroll(kPreload ? SM::kNT : 1)
           for (int nt = 0; nt < SM::kNT; ++nt) {
             double d0 = 0.0, d1 = 0.0;
-            dmma_8x8x4(d0, d1, c0, bv[0][nt]);
-            dmma_8x8x4(d0, d1, c1, bv[1][nt]);
+#pragma unroll
+            for (int ks = 0; ks < KO; ++ks) {
+              const double bk = kPreload ? bv[kPreload ? ks : 0][kPreload ? nt : 0]
+                                         : __ldg(fr + (ks * SM::kNT + nt) * 32);
+              dmma_8x8x4(d0, d1, ca[ks], bk);
+            }
             const int n0 = 8 * nt + 2 * t;
-            if ((N2 % 8 == 0 || n0 < N2) && cb >= 0 && !(P.ablate & 1)) store_pair(o_val + cb + n0, d0, d1, pol);
+            if (cb >= 0 && !(P.ablate & 1)) store_entries<N2>(o_val + cb, n0, d0, d1, pol);
           }
         }
       }

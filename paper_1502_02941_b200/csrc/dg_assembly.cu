@@ -1087,6 +1087,9 @@ void launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_prob
             hb[i] = x[L::S + k * N2 + n];
           } else if (k == 3) {
             hb[i] = x[L::M + n];
+          } else if (SM::kTForm && k < kw) {  // TQ[q][a] = phi_q (x) d_a phi_q
+            const int q = (k - 4) / 2, a = (k - 4) % 2;
+            hb[i] = plan->h_tens[plan->L.PHI + q * NL + bi] * plan->h_dphi[(q * 2 + a) * NL + bj];
           } else if (k < 6) {
             hb[i] = x[L::T + (k - 4) * N2 + n];
           } else if (k < kw) {
@@ -1221,6 +1224,7 @@ bool try_launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_
   DGB_V2(3, 6, 2, 2, 128, 4)
   DGB_V2(6, 7, 3, 0, 128, 4)
   DGB_V2(6, 12, 3, 0, 128, 4)
+  DGB_V2(15, 19, 5, 2, 64, 3)   // P4, trigonometric velocity (config 5)
   DGB_V2(10, 16, 4, 0, 128, 3)  // measured: 168 registers, 12 warps/SM (C3 81% of roofline)
   DGB_V2(10, 16, 4, 1, 128, 3)
 #undef DGB_V2
