@@ -896,17 +896,44 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
           for (int ks = 0; ks < KO; ++ks) ca[ks] = aa[ks];
           const long long cb = bm;
           if (r + 1 < ntiles) tile_rows(r + 1, aa, bm);
-#pragma unroll(kPreload ? SM::kNT : 1)
-          for (int nt = 0; nt < SM::kNT; ++nt) {
-            double d0 = 0.0, d1 = 0.0;
+          if constexpr (kPreload) {
 #pragma unroll
-            for (int ks = 0; ks < KO; ++ks) {
-              const double bk = kPreload ? bv[kPreload ? ks : 0][kPreload ? nt : 0]
-                                         : __ldg(fr + (ks * SM::kNT + nt) * 32);
-              dmma_8x8x4(d0, d1, ca[ks], bk);
+            for (int nt = 0; nt < SM::kNT; ++nt) {
+              double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+              for (int ks = 0; ks < KO; ++ks) dmma_8x8x4(d0, d1, ca[ks], bv[ks][nt]);
+              const int n0 = 8 * nt + 2 * t;
+              if (cb >= 0 && !(P.ablate & 1)) store_entries<N2>(o_val + cb, n0, d0, d1, pol);
             }
-            const int n0 = 8 * nt + 2 * t;
-            if (cb >= 0 && !(P.ablate & 1)) store_entries<N2>(o_val + cb, n0, d0, d1, pol);
+          } else {
+            // large operands (P4): stream the B fragments from L2, two n-tiles ahead
+            constexpr int PF = 2;
+            double bq[PF][KO];
+#pragma unroll
+            for (int u = 0; u < PF; ++u) {
+#pragma unroll
+              for (int ks = 0; ks < KO; ++ks) bq[u][ks] = __ldg(fr + (ks * SM::kNT + u) * 32);
+            }
+#pragma unroll 2
+            for (int nt = 0; nt < SM::kNT; ++nt) {
+              double bk[KO];
+#pragma unroll
+              for (int ks = 0; ks < KO; ++ks) bk[ks] = bq[0][ks];
+#pragma unroll
+              for (int u = 0; u + 1 < PF; ++u) {
+#pragma unroll
+                for (int ks = 0; ks < KO; ++ks) bq[u][ks] = bq[u + 1][ks];
+              }
+              if (nt + PF < SM::kNT) {
+#pragma unroll
+                for (int ks = 0; ks < KO; ++ks) bq[PF - 1][ks] = __ldg(fr + (ks * SM::kNT + nt + PF) * 32);
+              }
+              double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+              for (int ks = 0; ks < KO; ++ks) dmma_8x8x4(d0, d1, ca[ks], bk[ks]);
+              const int n0 = 8 * nt + 2 * t;
+              if (cb >= 0 && !(P.ablate & 1)) store_entries<N2>(o_val + cb, n0, d0, d1, pol);
+            }
           }
         }
       }
