@@ -889,14 +889,14 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
             for (int ks = 0; ks < KO; ++ks) bv[ks][nt] = __ldg(fr + (ks * SM::kNT + nt) * 32);
           }
         }
+        if constexpr (kPreload) {
 #pragma unroll 1
-        for (int r = tb; r < te; ++r) {
-          double ca[KO];
+          for (int r = tb; r < te; ++r) {
+            double ca[KO];
 #pragma unroll
-          for (int ks = 0; ks < KO; ++ks) ca[ks] = aa[ks];
-          const long long cb = bm;
-          if (r + 1 < ntiles) tile_rows(r + 1, aa, bm);
-          if constexpr (kPreload) {
+            for (int ks = 0; ks < KO; ++ks) ca[ks] = aa[ks];
+            const long long cb = bm;
+            if (r + 1 < ntiles) tile_rows(r + 1, aa, bm);
 #pragma unroll
             for (int nt = 0; nt < SM::kNT; ++nt) {
               double d0 = 0.0, d1 = 0.0;
@@ -905,34 +905,50 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
               const int n0 = 8 * nt + 2 * t;
               if (cb >= 0 && !(P.ablate & 1)) store_entries<N2>(o_val + cb, n0, d0, d1, pol);
             }
-          } else {
-            // large operands (P4): stream the B fragments from L2, two n-tiles ahead
-            constexpr int PF = 2;
-            double bq[PF][KO];
+          }
+        } else {
+          // large operands (P4): n-tile outer -- each B fragment (streamed from L2 a few
+          // n-tiles ahead) serves every tile of the class; the tiles' rows stay in registers
+          constexpr int MT = 4;  // tiles per class: at most 32 rows
+          double at[MT][KO];
+          long long bt_[MT];
 #pragma unroll
-            for (int u = 0; u < PF; ++u) {
+          for (int u = 0; u < MT; ++u) {
+            bt_[u] = -1;
 #pragma unroll
-              for (int ks = 0; ks < KO; ++ks) bq[u][ks] = __ldg(fr + (ks * SM::kNT + u) * 32);
+            for (int ks = 0; ks < KO; ++ks) at[u][ks] = 0.0;
+            if (tb + u < te) tile_rows(tb + u, at[u], bt_[u]);
+          }
+          constexpr int PF = 3;
+          double bq[PF][KO];
+#pragma unroll
+          for (int u = 0; u < PF; ++u) {
+#pragma unroll
+            for (int ks = 0; ks < KO; ++ks) bq[u][ks] = __ldg(fr + (ks * SM::kNT + u) * 32);
+          }
+#pragma unroll 1
+          for (int nt = 0; nt < SM::kNT; ++nt) {
+            double bk[KO];
+#pragma unroll
+            for (int ks = 0; ks < KO; ++ks) bk[ks] = bq[0][ks];
+#pragma unroll
+            for (int u = 0; u + 1 < PF; ++u) {
+#pragma unroll
+              for (int ks = 0; ks < KO; ++ks) bq[u][ks] = bq[u + 1][ks];
             }
-#pragma unroll 2
-            for (int nt = 0; nt < SM::kNT; ++nt) {
-              double bk[KO];
+            if (nt + PF < SM::kNT) {
 #pragma unroll
-              for (int ks = 0; ks < KO; ++ks) bk[ks] = bq[0][ks];
+              for (int ks = 0; ks < KO; ++ks) bq[PF - 1][ks] = __ldg(fr + (ks * SM::kNT + nt + PF) * 32);
+            }
+            const int n0 = 8 * nt + 2 * t;
 #pragma unroll
-              for (int u = 0; u + 1 < PF; ++u) {
+            for (int u = 0; u < MT; ++u) {
+              if (tb + u < te) {
+                double d0 = 0.0, d1 = 0.0;
 #pragma unroll
-                for (int ks = 0; ks < KO; ++ks) bq[u][ks] = bq[u + 1][ks];
+                for (int ks = 0; ks < KO; ++ks) dmma_8x8x4(d0, d1, at[u][ks], bk[ks]);
+                if (bt_[u] >= 0 && !(P.ablate & 1)) store_entries<N2>(o_val + bt_[u], n0, d0, d1, pol);
               }
-              if (nt + PF < SM::kNT) {
-#pragma unroll
-                for (int ks = 0; ks < KO; ++ks) bq[PF - 1][ks] = __ldg(fr + (ks * SM::kNT + nt + PF) * 32);
-              }
-              double d0 = 0.0, d1 = 0.0;
-#pragma unroll
-              for (int ks = 0; ks < KO; ++ks) dmma_8x8x4(d0, d1, ca[ks], bk[ks]);
-              const int n0 = 8 * nt + 2 * t;
-              if (cb >= 0 && !(P.ablate & 1)) store_entries<N2>(o_val + cb, n0, d0, d1, pol);
             }
           }
         }
