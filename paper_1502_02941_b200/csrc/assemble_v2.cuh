@@ -317,20 +317,47 @@ __device__ __forceinline__ void mma_block_store(AF a_at, const double* __restric
   long long bm[4];
 #pragma unroll
   for (int m = 0; m < 4; ++m) bm[m] = __shfl_sync(0xffffffffu, base, 8 * m + g);
+  if constexpr (kKeepA) {
 #pragma unroll
-  for (int nt = 0; nt < NT; ++nt) {
-    double bf[KS];
+    for (int nt = 0; nt < NT; ++nt) {
+      double bf[KS];
 #pragma unroll
-    for (int ks = 0; ks < KS; ++ks) bf[ks] = __ldg(frag + (ks * NT + nt) * 32 + lane);
-    const int n0 = 8 * nt + 2 * t;
+      for (int ks = 0; ks < KS; ++ks) bf[ks] = __ldg(frag + (ks * NT + nt) * 32 + lane);
+      const int n0 = 8 * nt + 2 * t;
 #pragma unroll
-    for (int m = 0; m < 4; ++m) {
-      double d0 = 0.0, d1 = 0.0;
+      for (int m = 0; m < 4; ++m) {
+        double d0 = 0.0, d1 = 0.0;
 #pragma unroll
-      for (int ks = 0; ks < KS; ++ks) {
-        dmma_8x8x4(d0, d1, kKeepA ? af[m][kKeepA ? ks : 0] : a_at(m, ks), bf[ks]);
+        for (int ks = 0; ks < KS; ++ks) dmma_8x8x4(d0, d1, af[m][ks], bf[ks]);
+        if (bm[m] >= 0) store_entries<N2>(val + bm[m], n0, d0, d1, pol);
       }
-      if (bm[m] >= 0) store_entries<N2>(val + bm[m], n0, d0, d1, pol);
+    }
+  } else {
+    // large K (P4): the B fragments of the next n-tile are loaded (from L2) while this one's
+    // products run, and each product splits its K chain over two accumulators
+    double bq[KS];
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) bq[ks] = __ldg(frag + ks * NT * 32 + lane);
+#pragma unroll 1
+    for (int nt = 0; nt < NT; ++nt) {
+      double bf[KS];
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) bf[ks] = bq[ks];
+      if (nt + 1 < NT) {
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) bq[ks] = __ldg(frag + (ks * NT + nt + 1) * 32 + lane);
+      }
+      const int n0 = 8 * nt + 2 * t;
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        double d0 = 0.0, d1 = 0.0, e0 = 0.0, e1 = 0.0;
+#pragma unroll
+        for (int ks = 0; ks < KS; ks += 2) {
+          dmma_8x8x4(d0, d1, a_at(m, ks), bf[ks]);
+          if (ks + 1 < KS) dmma_8x8x4(e0, e1, a_at(m, ks + 1), bf[ks + 1]);
+        }
+        if (bm[m] >= 0) store_entries<N2>(val + bm[m], n0, d0 + e0, d1 + e1, pol);
+      }
     }
   }
 }
