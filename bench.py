@@ -234,7 +234,7 @@ def run_ours(args, world, rank, local):
     if args.minblocks:
         plan.set_option(capi.OPTION_MIN_BLOCKS, args.minblocks)
     if args.ablate:
-        plan.set_option(1000, args.ablate)
+        plan.set_option(capi.OPTION_PROFILE_ABLATE, args.ablate)
     stream = torch.cuda.current_stream(local)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=f"cuda:{local}")  # 256 MiB > L2
 

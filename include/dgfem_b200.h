@@ -300,9 +300,13 @@ int dgb_plan_set_kernel_events(dgb_plan* plan, void* start, void* stop);
 enum dgb_plan_option {
   DGB_OPTION_FORCE_GENERIC_KERNEL = 1,
   DGB_OPTION_MIN_BLOCKS = 2, /* tuning knob: register budget of the P2 kernel (CTAs per SM) */
-  DGB_OPTION_L2_POLICY = 3   /* bit 0: keep node coordinates persisting in L2 (access-policy
+  DGB_OPTION_L2_POLICY = 3,  /* bit 0: keep node coordinates persisting in L2 (access-policy
                                 window, carve-out sized to the node array at bind time);
                                 bit 1: evict-first L2 hint on the output stream */
+  DGB_OPTION_PROFILE_ABLATE = 1000 /* DIAGNOSTICS ONLY -- RESULTS ARE WRONG while nonzero: skip
+                                      kernel parts to attribute time (bits: 1 block stores,
+                                      2 source evaluation, 4 neighbour blocks, 8 diagonal
+                                      block, 16 exit after the prologue, 32 after own geometry) */
 };
 int dgb_plan_set_option(dgb_plan* plan, int32_t option, int32_t value);
 

@@ -1732,10 +1732,8 @@ int dgb_plan_set_option(dgb_plan* plan, int32_t option, int32_t value) {
     case DGB_OPTION_FORCE_GENERIC_KERNEL: plan->force_generic = value; return DGB_OK;
     case DGB_OPTION_MIN_BLOCKS: plan->minblocks = value; return DGB_OK;
     case DGB_OPTION_L2_POLICY: plan->l2_policy = value; return DGB_OK;
-    // Profiling diagnostics, deliberately not in the public header: skip parts of the P2
-    // tensor-core kernel to attribute time (results are WRONG while set).  Bits: 1 no block
-    // stores, 2 no source evaluation, 4 no neighbour blocks, 8 no diagonal block.
-    case 1000: plan->ablate = value; return DGB_OK;
+    // profiling diagnostics (results are WRONG while set): see the header
+    case DGB_OPTION_PROFILE_ABLATE: plan->ablate = value; return DGB_OK;
     default: return DGB_STATUS_INVALID_ARGUMENT;
   }
 }
