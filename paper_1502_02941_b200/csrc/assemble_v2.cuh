@@ -702,15 +702,13 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
   {
 #pragma unroll
     for (int i = 0; i < NL; ++i) srhs[lane * NL + i] = F[i];
+    fence_smem_to_async();  // every writer: its shared-memory stores -> the async (TMA) proxy
     __syncwarp();
     const int e_first = blockIdx.x * blockDim.x + warp * 32;  // relative to row_begin
     const int n_here = min(32, P.row_end - P.row_begin - e_first);
     double* dst = o_rhs + static_cast<long long>(e_first) * NL;
     const int bulk = (n_here * NL) & ~1;  // 16-byte multiple (warp slices start 16-B aligned)
-    if (lane == 0 && bulk > 0) {
-      fence_smem_to_async();
-      bulk_store(dst, srhs, bulk * sizeof(double), P.evict_first);
-    }
+    if (lane == 0 && bulk > 0) bulk_store(dst, srhs, bulk * sizeof(double), P.evict_first);
     for (int idx = bulk + lane; idx < n_here * NL; idx += 32) dst[idx] = srhs[idx];
   }
 
@@ -1036,17 +1034,16 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
   }
   if constexpr (SM::kRowMode) {
     // one bulk copy of the warp's whole row range; the unaligned head / tail doubles by hand
+    fence_smem_to_async();  // every writer: its staged blocks -> the async (TMA) proxy
     __syncwarp();
     const int n = (rp_last - rp_first) * N2;
     double* dst = o_val + static_cast<long long>(rp_first) * N2;
     const int head = rp_first & 1;
     const int body = (n - head) & ~1;
-    if (lane == 0 && body > 0) {
-      fence_smem_to_async();
-      bulk_store(dst + head, srow + head, body * sizeof(double), P.evict_first);
-    }
-    if (lane == 1 && head) dst[0] = srow[0];
-    if (lane == 2 && head + body < n) dst[n - 1] = srow[n - 1];
+    if (lane == 0 && body > 0) bulk_store(dst + head, srow + head, body * sizeof(double), P.evict_first);
+    // (a warp past the last row has no range: n <= 0, nothing to write)
+    if (lane == 1 && head && n > 0) dst[0] = srow[0];
+    if (lane == 2 && n > 0 && head + body < n) dst[n - 1] = srow[n - 1];
   } else {
     bulk_wait_all();  // shared memory must outlive the copies
   }

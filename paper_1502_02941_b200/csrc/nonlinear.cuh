@@ -109,6 +109,7 @@ __global__ void __launch_bounds__(128) nonlinear_kernel(const __grid_constant__ 
   // H: the warp's contiguous slice, one bulk copy
 #pragma unroll
   for (int i = 0; i < NL; ++i) sh[lane * NL + i] = H[i];
+  v2::fence_smem_to_async();  // every writer: its shared-memory stores -> the async (TMA) proxy
   if (active) {
     P.row_ptr[e + 1] = e + 1;
     P.col[e] = e;
@@ -119,10 +120,7 @@ __global__ void __launch_bounds__(128) nonlinear_kernel(const __grid_constant__ 
     const int n_here = min(32, P.n_elements - e0);
     double* dst = P.h + static_cast<long long>(e0) * NL;
     const int bulk = (n_here * NL) & ~1;  // 16-byte multiple; warp slices start 16-B aligned
-    if (lane == 0 && bulk > 0) {
-      v2::fence_smem_to_async();
-      v2::bulk_store(dst, sh, bulk * sizeof(double), false);
-    }
+    if (lane == 0 && bulk > 0) v2::bulk_store(dst, sh, bulk * sizeof(double), false);
     for (int idx = bulk + lane; idx < n_here * NL; idx += 32) dst[idx] = sh[idx];
   }
 

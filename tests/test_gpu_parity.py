@@ -101,3 +101,35 @@ def test_velocity_kinds_on_p1(oracle):
             params = dgfem.set_parameters(method, 1)
             compare_system(run_gpu(mesh, ref, spec, params),
                            oracle.assemble(mesh.arrays(), ref.tables(), spec.c, params))
+
+
+# Every specialised kernel -- (degree, quad_order) -> (nl, nq_vol, nq_edge) -- with each velocity
+# kind it is built for, per-element eps / alpha (the edge average of eps, element alpha), a
+# Neumann side (outflow-only convention), every method, on a jittered permuted mesh.
+KERNEL_CASES = [
+    (1, 3, "const"), (1, 3, "affine"), (1, 3, "trig"),   # P1 stash-free / general kernels
+    (2, 5, "const"), (2, 6, "const"),                    # P2 tensor cores (P-form)
+    (3, 7, "const"), (3, 7, "affine"),                   # P3 tensor cores (P-form, U-form)
+    (4, 9, "trig"),                                      # P4 tensor cores (T-form)
+    (2, 5, "affine"), (3, 7, "trig"),                    # generic kernel
+]
+
+
+@pytest.mark.parametrize("degree,quad_order,vel", KERNEL_CASES)
+def test_every_kernel_per_element_fields(oracle, degree, quad_order, vel):
+    mesh = dgfem.unit_square_mesh(10, 0.2, 31, True, 32, 2)
+    ref = dgfem.ReferenceElement(degree, quad_order)
+    b = {"const": problems.vec_constant(0.8, -0.3),
+         "affine": problems.vec_affine(0.5, -0.5, 0.0, -1.0, 1.0, 0.0),
+         "trig": problems.vec_trig(2 * problems.PI, 2 * problems.PI)}[vel]
+    u = (capi.FN_SIN_SIN, (1.0,))
+    spec = problems.make_problem("kernels", 1.0, b, 1.0, problems.function(*u),
+                                 problems.function(*u), neumann_sides=2)
+    r = problems.uniform01(777 + degree, 2 * mesh.n_elements)
+    spec.set_per_element("diffusion", 10.0 ** (-4.0 + 4.0 * r[:mesh.n_elements]))
+    spec.set_per_element("linear_reaction", 2.0 * r[mesh.n_elements:])
+    for method in (capi.SIPG, capi.NIPG, capi.IIPG):
+        params = dgfem.set_parameters(method, degree, capi.INFLOW_DROP)
+        g = run_gpu(mesh, ref, spec, params)
+        o = oracle.assemble(mesh.arrays(), ref.tables(), spec.c, params)
+        compare_system(g, o)
