@@ -263,7 +263,7 @@ def test_bound_pattern_single_kernel_matches_unbound():
     assert capi.load().dgb_plan_launch_count(plan._h) == 4
 
 
-@pytest.mark.parametrize("cfg_index", [2, 4])
+@pytest.mark.parametrize("cfg_index", [2, 3, 4])
 def test_batch_equals_separate_assemblies(cfg_index):
     """dgb_assemble_batch (SIPG, NIPG, IIPG in one launch for P2 on a bound mesh; a loop
     otherwise) writes exactly what three dgb_assemble_rows calls write."""
