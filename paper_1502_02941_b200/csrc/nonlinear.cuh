@@ -132,17 +132,27 @@ __global__ void __launch_bounds__(128) nonlinear_kernel(const __grid_constant__ 
     const int em = e0 + 8 * m + g;
     bm[m] = em < P.n_elements ? static_cast<long long>(em) * N2 : -1LL;
   }
-#pragma unroll 1
+#pragma unroll 2
   for (int nt = 0; nt < NT; ++nt) {
     double d[4][2];
 #pragma unroll
     for (int m = 0; m < 4; ++m) d[m][0] = d[m][1] = 0.0;
+    // k-steps in chunks of 4: the chunk's B fragments are loaded together, then the products
 #pragma unroll 1
-    for (int ks = 0; ks < P.ks; ++ks) {
-      const double b = __ldg(P.bfrag + (static_cast<long long>(ks) * NT + nt) * 32 + lane);
+    for (int k0 = 0; k0 < P.ks; k0 += 4) {
+      double b[4];
 #pragma unroll
-      for (int m = 0; m < 4; ++m) {
-        v2::dmma_8x8x4(d[m][0], d[m][1], S[(4 * ks + t) * kCT + 8 * m + g], b);
+      for (int u = 0; u < 4; ++u) {
+        b[u] = k0 + u < P.ks ? __ldg(P.bfrag + (static_cast<long long>(k0 + u) * NT + nt) * 32 + lane) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (k0 + u < P.ks) {
+#pragma unroll
+          for (int m = 0; m < 4; ++m) {
+            v2::dmma_8x8x4(d[m][0], d[m][1], S[(4 * (k0 + u) + t) * kCT + 8 * m + g], b[u]);
+          }
+        }
       }
     }
     const int n0 = 8 * nt + 2 * t;
