@@ -284,7 +284,7 @@ class RefSystem:
 
     def matvec(self, x: np.ndarray) -> np.ndarray:
         x = np.ascontiguousarray(x, dtype=np.float64)
-        y = np.zeros_like(x)
+        y = np.zeros((row_ptr.shape[0] - 1) * nl)  # rows of the (possibly sharded) BSR
         self.lib._check(self.lib.lib.dgref_matvec(self.h, _ptr(x), _ptr(y)))
         return y
 
@@ -401,7 +401,7 @@ class OracleLib:
     def spmv(self, row_ptr, col, val, x, threads: int = 0) -> np.ndarray:
         nl = val.shape[1]
         x = np.ascontiguousarray(x, dtype=np.float64)
-        y = np.zeros_like(x)
+        y = np.zeros((row_ptr.shape[0] - 1) * nl)  # rows of the (possibly sharded) BSR
         self.lib.dgo_spmv(_ptr(row_ptr), _ptr(col), _ptr(val), nl, row_ptr.shape[0] - 1,
                           _ptr(x), _ptr(y), threads if threads > 0 else (os.cpu_count() or 1))
         return y
