@@ -61,6 +61,9 @@ def parse_args():
                          "-1: the default for the config")
     ap.add_argument("--no-batch", action="store_true",
                     help="one dgb_assemble launch per method instead of one dgb_assemble_batch")
+    ap.add_argument("--no-fuse", action="store_true",
+                    help="batched launch with one CTA row per set (grid.y = methods) instead of "
+                         "one per-element pass writing every set")
     ap.add_argument("--no-bind", action="store_true",
                     help="recompute the BSR pattern in every assembly (count + scan launches)")
     return ap.parse_args()
@@ -75,8 +78,10 @@ def peak_hbm():
         return HBM_FALLBACK_GBS, "fallback"
 
 
-def algorithmic_bytes(mesh, nl: int, per_element_fields: int) -> int:
-    """every input read once, every output written once.
+def algorithmic_bytes(mesh, nl: int, per_element_fields: int, sets: int = 1, world: int = 1) -> int:
+    """every input read once, every output written once -- for a batched
+    launch of `sets` parameter sets, the inputs once and the outputs once per set; a shard
+    (world > 1) does 1/world of it.
     reads : 16 n_nodes + 12 E (elements) + 12 E (element_edges) + 8 n_edges (edge_elements)
             + 1 n_edges (edge_kind) + 8 E per per-element coefficient field
     writes: 8 nl^2 (E + 2I) (values) + 4 (E + 2I) (block cols) + 4 (E + 1) (row ptr)
@@ -85,7 +90,7 @@ def algorithmic_bytes(mesh, nl: int, per_element_fields: int) -> int:
     nb = E + 2 * I
     reads = 16 * nn + 12 * E + 12 * E + 8 * ne + ne + 8 * E * per_element_fields
     writes = 8 * nl * nl * nb + 4 * nb + 4 * (E + 1) + 8 * nl * E
-    return reads + writes
+    return (reads + sets * writes) // world
 
 
 class ClockSampler:
@@ -235,6 +240,8 @@ def run_ours(args, world, rank, local):
         plan.set_option(capi.OPTION_MIN_BLOCKS, args.minblocks)
     if args.ablate:
         plan.set_option(capi.OPTION_PROFILE_ABLATE, args.ablate)
+    if args.no_fuse:
+        plan.set_option(capi.OPTION_BATCH_FUSE, 0)
     stream = torch.cuda.current_stream(local)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=f"cuda:{local}")  # 256 MiB > L2
 
@@ -295,7 +302,7 @@ def run_ours(args, world, rank, local):
     # roofline of the block-row kernel (dominant launch)
     per_elem_fields = len(spec.per_element)
     sets_per_launch = len(params) if batched else 1
-    bytes_per_launch = sets_per_launch * (algorithmic_bytes(mesh, ref.n_local, per_elem_fields) // world)
+    bytes_per_launch = algorithmic_bytes(mesh, ref.n_local, per_elem_fields, sets_per_launch, world)
     kern_avg_ms = sum(kern_ms) / len(kern_ms)
     achieved = bytes_per_launch / (kern_avg_ms / 1e3) / 1e9
     peak, peak_kind = peak_hbm()

@@ -303,6 +303,9 @@ enum dgb_plan_option {
   DGB_OPTION_L2_POLICY = 3,  /* bit 0: keep node coordinates persisting in L2 (access-policy
                                 window, carve-out sized to the node array at bind time);
                                 bit 1: evict-first L2 hint on the output stream */
+  DGB_OPTION_BATCH_FUSE = 4, /* dgb_assemble_batch on the tensor-core kernels (default 1): sets
+                                with equal penalties share the per-element work and each CTA
+                                writes every set; 0 = one CTA row per set (grid.y = n) */
   DGB_OPTION_PROFILE_ABLATE = 1000 /* DIAGNOSTICS ONLY -- RESULTS ARE WRONG while nonzero: skip
                                       kernel parts to attribute time (bits: 1 block stores,
                                       2 source evaluation, 4 neighbour blocks, 8 diagonal

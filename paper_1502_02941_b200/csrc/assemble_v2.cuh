@@ -381,7 +381,12 @@ __device__ __forceinline__ void velocity_k(const dgb_vector_field& b, double x, 
 // Stash field indices (per edge l, per lane): see the diagonal / neighbour passes.
 enum { F_W0 = 0, F_W1, F_P, F_Y0, F_Y1, F_Z0, F_Z1, F_X, F_U = 7 };
 
-template <int NL, int NQV, int NQE, int BK, int THREADS, int MINB>
+// FUSE (tensor-core kernels, n_batch > 1 sets with equal penalties): one CTA assembles its
+// rows for EVERY set.  The A operand (the per-element stash) does not depend on kappa --
+// kappa lives in the B fragments (W = kappa Q^T - Q, kappa Z) and in one RHS term, kept apart
+// (F = F0 + kappa Fk) -- so the gathers, geometry, source and edge terms run once and only the
+// products and stores repeat per set.
+template <int NL, int NQV, int NQE, int BK, int THREADS, int MINB, bool FUSE = false>
 __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
     const __grid_constant__ Params2<NL, NQV, NQE, BK == 2, full_tensors(NL, BK)> P) {
   constexpr bool TRIG = BK == 2;
@@ -400,7 +405,8 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
   if (P.ablate & 16) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   // this CTA's parameter set (grid.y) and its outputs
-  const int mset = blockIdx.y;
+  const int mset = FUSE ? 0 : blockIdx.y;
+  const int n_sets = FUSE ? P.n_batch : 1;  // sets this CTA writes: bt[mset .. mset + n_sets)
   const double kappa = P.bt[mset].kappa, sigma_i = P.bt[mset].sigma_i, sigma_b = P.bt[mset].sigma_b;
   int32_t* const o_row_ptr = P.bt[mset].row_ptr;
   int32_t* const o_col = P.bt[mset].col;
@@ -433,6 +439,10 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
     }
   };
 
+  if constexpr (FUSE) {
+#pragma unroll
+    for (int i = 0; i < NL; ++i) srhs[lane * NL + i] = 0.0;  // Fk: this lane's row
+  }
   const int e = P.row_begin + blockIdx.x * blockDim.x + threadIdx.x;
   const bool active = e < P.row_end;
   const int ee = active ? e : P.row_end - 1;  // inactive lanes mirror a valid element
@@ -558,8 +568,10 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
       w1 = base * ge1;
       y0 = -base * (gf.G00 * nx + gf.G10 * ny);
       y1 = -base * (gf.G01 * nx + gf.G11 * ny);
-      z0 = -kappa * base * ge0;
-      z1 = -kappa * base * ge1;
+      // tensor-core path: kappa is folded into the Z rows of the B operand
+      const double kz = SM::kMma ? 1.0 : kappa;
+      z0 = -kz * base * ge0;
+      z1 = -kz * base * ge1;
       const double sh = sigma_i * rh;
       if constexpr (BK == 0) {
         // constant b: every point has the same flux, so the point weights factor out
@@ -624,7 +636,7 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
           const double win = (inflow && fls[p] < 0.0) ? -FMUL(w, fls[p]) : 0.0;
           const double wgd = w * gb[p];
           cG[p] = wgd * (sh * eps) + win * gb[p];  // emit_dirichlet_rhs + inflow data term
-          cH[p] = wgd * (kappa * eps);
+          cH[p] = FUSE ? wgd * eps : wgd * (kappa * eps);  // FUSE: into Fk, kappa per set
           if constexpr (BK != 0) K(F_U + p, l) = FMUL(sh, FMUL(w, eps)) + win;
         }
       }
@@ -633,9 +645,16 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
         const double h0 = cH[p] * ge0, h1 = cH[p] * ge1;
 #pragma unroll
         for (int i = 0; i < NL; ++i) {
-          F[i] = fma(cG[p], P.t.x[L::EPHI + (l * NQE + p) * NL + i],
-                     fma(h0, P.t.x[L::EDPHI + ((l * NQE + p) * 2) * NL + i],
-                         fma(h1, P.t.x[L::EDPHI + ((l * NQE + p) * 2 + 1) * NL + i], F[i])));
+          if constexpr (FUSE) {
+            F[i] = fma(cG[p], P.t.x[L::EPHI + (l * NQE + p) * NL + i], F[i]);
+            srhs[lane * NL + i] =
+                fma(h0, P.t.x[L::EDPHI + ((l * NQE + p) * 2) * NL + i],
+                    fma(h1, P.t.x[L::EDPHI + ((l * NQE + p) * 2 + 1) * NL + i], srhs[lane * NL + i]));
+          } else {
+            F[i] = fma(cG[p], P.t.x[L::EPHI + (l * NQE + p) * NL + i],
+                       fma(h0, P.t.x[L::EDPHI + ((l * NQE + p) * 2) * NL + i],
+                           fma(h1, P.t.x[L::EDPHI + ((l * NQE + p) * 2 + 1) * NL + i], F[i])));
+          }
         }
       }
     }
@@ -668,20 +687,30 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
   if (P.row_ptr_src) {  // pattern computed once per mesh: copy this element's entry
     rp = __ldg(P.row_ptr_src + (ee - P.row_begin));
     if (active) {
-      o_row_ptr[ee - P.row_begin + 1] = __ldg(P.row_ptr_src + (ee - P.row_begin + 1));
-      if (ee == P.row_begin) o_row_ptr[0] = 0;
+      const int rp1 = __ldg(P.row_ptr_src + (ee - P.row_begin + 1));
+#pragma unroll 1
+      for (int s = 0; s < n_sets; ++s) {
+        int32_t* rpo = P.bt[mset + s].row_ptr;
+        rpo[ee - P.row_begin + 1] = rp1;
+        if (ee == P.row_begin) rpo[0] = 0;
+      }
     }
   } else {
     rp = o_row_ptr[ee - P.row_begin];
   }
   const int diag_slot = slot_of[0];
-  if (active) o_col[rp + diag_slot] = ee;
+#pragma unroll 1
+  for (int s = 0; s < n_sets; ++s) {
+    int32_t* co = FUSE ? P.bt[mset + s].col : o_col;
+    if (active) co[rp + diag_slot] = ee;
+#pragma unroll
+    for (int l = 0; l < 3; ++l) {
+      if (active && fcol[l] >= 0) co[rp + slot_of[1 + l]] = fcol[l];
+    }
+  }
 #pragma unroll
   for (int l = 0; l < 3; ++l) {
-    if (fcol[l] >= 0) {
-      if (active) o_col[rp + slot_of[1 + l]] = fcol[l];
-      mk[l * 32 + lane] |= slot_of[1 + l] << 4;
-    }
+    if (fcol[l] >= 0) mk[l * 32 + lane] |= slot_of[1 + l] << 4;
   }
 
   // odd N2: this lane's row inside the warp's contiguous staged row range
@@ -699,7 +728,28 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
 
   const unsigned long long pol = output_policy(P.evict_first);
   // ---- RHS: the warp's contiguous slice, packed in shared memory and written in one go ------
-  {
+  if constexpr (FUSE) {
+    // per set: F0 + kappa_s Fk staged, then coalesced 16-byte stores (slices 16-B aligned)
+    double fk[NL];
+#pragma unroll
+    for (int i = 0; i < NL; ++i) fk[i] = srhs[lane * NL + i];
+    const int e_first = blockIdx.x * blockDim.x + warp * 32;  // relative to row_begin
+    const int n_here = min(32, P.row_end - P.row_begin - e_first);
+    const int n = n_here * NL;
+#pragma unroll 1
+    for (int s = 0; s < n_sets; ++s) {
+      const double ks = P.bt[mset + s].kappa;
+      __syncwarp();
+#pragma unroll
+      for (int i = 0; i < NL; ++i) srhs[lane * NL + i] = fma(ks, fk[i], F[i]);
+      __syncwarp();
+      double* dst = P.bt[mset + s].rhs + static_cast<long long>(e_first) * NL;
+      for (int idx = 2 * lane; idx + 1 < n; idx += 64) {
+        store_pair(dst + idx, srhs[idx], srhs[idx + 1], pol);
+      }
+      if (n > 0 && (n & 1) && lane == 0) store_one(dst + n - 1, srhs[n - 1], pol);
+    }
+  } else {
 #pragma unroll
     for (int i = 0; i < NL; ++i) srhs[lane * NL + i] = F[i];
     fence_smem_to_async();  // every writer: its shared-memory stores -> the async (TMA) proxy
@@ -748,10 +798,14 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
       __syncwarp();
       const int g = lane >> 2, t = lane & 3;
       if (!(P.ablate & 8)) {
-        mma_block_store<SM::kKS, SM::kNT, N2>(
-            [&](int m, int ks) { return sk[(4 * ks + t) * SM::kCT + 8 * m + g]; }, o_bfrag,
-            (active && !(P.ablate & 1)) ? static_cast<long long>(rp + diag_slot) * N2 : -1LL,
-            o_val, lane, pol);
+#pragma unroll 1
+        for (int s = 0; s < n_sets; ++s) {
+          mma_block_store<SM::kKS, SM::kNT, N2>(
+              [&](int m, int ks) { return sk[(4 * ks + t) * SM::kCT + 8 * m + g]; },
+              P.bt[mset + s].bfrag,
+              (active && !(P.ablate & 1)) ? static_cast<long long>(rp + diag_slot) * N2 : -1LL,
+              P.bt[mset + s].val, lane, pol);
+        }
       }
     } else {
     constexpr int RC = NL <= 6 ? NL : (NL <= 10 ? 2 : 1);  // rows per register chunk
@@ -896,6 +950,10 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
         bm = __shfl_sync(0xffffffffu, my_base, sl);
         if (src < 0) bm = -1;
       };
+#pragma unroll 1
+      for (int s = 0; s < n_sets; ++s) {
+      const double* const o_bfrag = P.bt[mset + s].bfrag;
+      double* const o_val = P.bt[mset + s].val;
       double aa[KO];
       long long bm;
       if (ntiles > 0) tile_rows(0, aa, bm);
@@ -978,6 +1036,7 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
           }
         }
       }
+      }  // sets
       __syncwarp();  // the row map is rebuilt for the next l
       continue;
     }

@@ -900,6 +900,7 @@ struct dgb_plan {
   size_t l2_window_max = 0;     // cudaDevAttrMaxAccessPolicyWindowSize
   size_t l2_persist_max = 0;    // cudaDevAttrMaxPersistingL2CacheSize
   int l2_policy = 0;            // bit 0: persist nodes in L2, bit 1: evict-first output
+  bool batch_fuse = true;       // dgb_assemble_batch: one CTA writes every kappa set
   // DMMA B fragments of the diagonal terms, one table per kappa (W depends on kappa)
   std::vector<std::pair<double, double*>> bfrag_cache;
   int ablate = 0;  // profiling diagnostics (dgb_plan_set_option 1000)
@@ -1057,9 +1058,10 @@ void launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_prob
     // at entry 8 nt + g.  First the diagonal terms (K = 16), then per (l, lf) the five
     // neighbour terms of local edge l against the neighbour's local edge lf (K = 8),
     //   X  = sum_p w_p phi^l_p (x) phi^lf_(n-1-p)      Y_a = sum_p phi^l_p (x) w dphi_a^lf_(n-1-p)
-    //   Z_a = sum_p w dphi_a^l_p (x) phi^lf_(n-1-p)
-    // (the factored neighbour block of the CUDA-core path, expanded).  Built once per
-    // (plan, kappa) on the host.
+    //   Z_a = kappa sum_p w dphi_a^l_p (x) phi^lf_(n-1-p)
+    // (the factored neighbour block of the CUDA-core path, expanded; kappa sits here, not in
+    // the per-element A rows, so sets differing only in kappa share one A operand -- FUSE).
+    // Built once per (plan, kappa) on the host.
     dgb_plan* mp = const_cast<dgb_plan*>(plan);
     for (int bi_ = 0; bi_ < nb; ++bi_) {
     const double kap = params[bi_].kappa;
@@ -1125,7 +1127,7 @@ void launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_prob
               default: acc += edw(l, p, 1, bi) * ephi(lf, q, bj); break;
             }
           }
-          hb[i] = acc;
+          hb[i] = term >= 3 ? kap * acc : acc;
         }
       }
       cuda_check(cudaMalloc(&frag, hb.size() * sizeof(double)), "cudaMalloc(bfrag)");
@@ -1138,6 +1140,16 @@ void launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_prob
     }
   }
   auto kernel = dgb::v2::assemble_kernel<NL, NQV, NQE, BK, THREADS, MINB>;
+  // tensor-core kernel, sets differing only in kappa: one CTA writes every set (FUSE)
+  bool fuse = false;
+  if constexpr (SM::kMma) {
+    fuse = nb > 1 && plan->batch_fuse;
+    for (int i = 1; i < nb; ++i) {
+      fuse = fuse && params[i].sigma_interior == params[0].sigma_interior &&
+             params[i].sigma_boundary == params[0].sigma_boundary;
+    }
+    if (fuse) kernel = dgb::v2::assemble_kernel<NL, NQV, NQE, BK, THREADS, MINB, true>;
+  }
   size_t smem_bytes = smem;
   if constexpr (NL == 3 && BK == 0) {
     // P1, constant velocity: the stash-free kernel (assemble_p1.cuh); option MIN_BLOCKS = 11
@@ -1155,6 +1167,11 @@ void launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_prob
     cuda_check(cudaFuncSetAttribute(dgb::v2::assemble_kernel<NL, NQV, NQE, BK, THREADS, MINB>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, bytes),
                "cudaFuncSetAttribute(v2)");
+    if constexpr (SM::kMma) {
+      cuda_check(cudaFuncSetAttribute(dgb::v2::assemble_kernel<NL, NQV, NQE, BK, THREADS, MINB, true>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, bytes),
+                 "cudaFuncSetAttribute(v2 fused)");
+    }
     if constexpr (NL == 3 && BK == 0) {
       cuda_check(cudaFuncSetAttribute(dgb::v2::assemble_p1_kernel<NQV, NQE, THREADS, MINB, true>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, bytes),
@@ -1169,7 +1186,7 @@ void launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_prob
   // Keep the node coordinates (gathered by every element and its neighbours, in random order
   // for permuted meshes) persisting in L2 while the output streams through with evict-first.
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid, nb);
+  cfg.gridDim = dim3(grid, fuse ? 1 : nb);
   cfg.blockDim = dim3(THREADS);
   cfg.dynamicSmemBytes = smem_bytes;
   cfg.stream = s;
@@ -1732,6 +1749,7 @@ int dgb_plan_set_option(dgb_plan* plan, int32_t option, int32_t value) {
     case DGB_OPTION_FORCE_GENERIC_KERNEL: plan->force_generic = value; return DGB_OK;
     case DGB_OPTION_MIN_BLOCKS: plan->minblocks = value; return DGB_OK;
     case DGB_OPTION_L2_POLICY: plan->l2_policy = value; return DGB_OK;
+    case DGB_OPTION_BATCH_FUSE: plan->batch_fuse = value != 0; return DGB_OK;
     // profiling diagnostics (results are WRONG while set): see the header
     case DGB_OPTION_PROFILE_ABLATE: plan->ablate = value; return DGB_OK;
     default: return DGB_STATUS_INVALID_ARGUMENT;

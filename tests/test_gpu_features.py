@@ -263,10 +263,13 @@ def test_bound_pattern_single_kernel_matches_unbound():
     assert capi.load().dgb_plan_launch_count(plan._h) == 4
 
 
+@pytest.mark.parametrize("fuse", [True, False])
 @pytest.mark.parametrize("cfg_index", [2, 3, 4])
-def test_batch_equals_separate_assemblies(cfg_index):
-    """dgb_assemble_batch (SIPG, NIPG, IIPG in one launch for P2 on a bound mesh; a loop
-    otherwise) writes exactly what three dgb_assemble_rows calls write."""
+def test_batch_equals_separate_assemblies(cfg_index, fuse):
+    """dgb_assemble_batch (SIPG, NIPG, IIPG in one launch for the tensor-core kernels on a
+    bound mesh; a loop otherwise) writes what three dgb_assemble_rows calls write.  Fused
+    (each CTA writes every set from one per-element pass): pattern and K bitwise, F within
+    rounding (F0 + kappa Fk is summed in another order); unfused: everything bitwise."""
     cfg = problems.CONFIGS[cfg_index]
     mesh = dgfem.unit_square_mesh(48, cfg.jitter, problems.SEED_JITTER, cfg.permute,
                                   problems.SEED_PERMUTE, cfg.neumann_sides)
@@ -276,10 +279,33 @@ def test_batch_equals_separate_assemblies(cfg_index):
     params = [dgfem.config_parameters(cfg, m) for m in methods]
     a = [shard.ShardAssembler(mesh, ref, spec, 0, 0, mesh.n_elements, bind=True)]
     a += [shard.ShardAssembler(mesh, ref, spec, 0, 0, mesh.n_elements, share=a[0]) for _ in methods[1:]]
+    a[0].plan.set_option(capi.OPTION_BATCH_FUSE, int(fuse))
     shard.assemble_batch(a, params)
     got = [to_np(x.out) for x in a]
     for p, g in zip(params, got):
         single = shard.ShardAssembler(mesh, ref, spec, 0, 0, mesh.n_elements, share=a[0])
         want = to_np(single.assemble(p))
-        for x, y in zip(g, want):
+        for x, y in zip(g[:3], want[:3]):
             assert np.array_equal(x, y)
+        if fuse:
+            np.testing.assert_allclose(g[3], want[3], rtol=0, atol=1e-14 * np.abs(want[3]).max())
+        else:
+            assert np.array_equal(g[3], want[3])
+
+
+def test_batch_mixed_penalties_not_fused():
+    """Sets whose penalties differ cannot share the per-element pass: the batch still matches
+    the separate assemblies bitwise (one CTA row per set)."""
+    cfg = problems.CONFIGS[2]
+    mesh = dgfem.unit_square_mesh(40)
+    ref = dgfem.ReferenceElement(cfg.degree, cfg.quad_order)
+    spec = problems.config_problem(2, mesh.n_elements)
+    params = [dgfem.config_parameters(cfg, m) for m in (capi.SIPG, capi.NIPG)]
+    params[1].sigma_interior *= 2.0
+    a = [shard.ShardAssembler(mesh, ref, spec, 0, 0, mesh.n_elements, bind=True)]
+    a.append(shard.ShardAssembler(mesh, ref, spec, 0, 0, mesh.n_elements, share=a[0]))
+    shard.assemble_batch(a, params)
+    for p, x in zip(params, a):
+        single = shard.ShardAssembler(mesh, ref, spec, 0, 0, mesh.n_elements, share=a[0])
+        for u, v in zip(to_np(x.out), to_np(single.assemble(p))):
+            assert np.array_equal(u, v)
