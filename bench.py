@@ -228,7 +228,7 @@ def run_ours(args, world, rank, local):
     spec = problems.config_problem(args.config, mesh.n_elements)
     params = [dgfem.config_parameters(cfg, m) for m in cfg.methods]
     begin, end = shard.row_range(mesh.n_elements, rank, world)
-    l2 = args.l2_policy if args.l2_policy >= 0 else 2  # measured: evict-first output (profiles/NOTES.md)
+    l2 = args.l2_policy  # -1: the library's per-kernel default (profiles/NOTES.md)
     shards = [shard.ShardAssembler(mesh, ref, spec, local, begin, end, bind=False)]
     shards[0].plan.set_option(capi.OPTION_L2_POLICY, l2)
     if not args.no_bind:
@@ -361,7 +361,8 @@ def run_ours(args, world, rank, local):
             "global_mesh": f"{world * cfg.n}x{cfg.n} cells on [0,{world}]x[0,1]" if world > 1 else None,
             "nq_vol": ref.nq_vol, "nq_edge": ref.nq_edge,
             "l2": "flushed between timed steps by a 256 MiB write (outside the timed events)",
-            "l2_policy": {0: "default", 1: "node coordinates persisting in L2",
+            "l2_policy": {-1: "auto: evict-first output for odd block sizes", 0: "default",
+                          1: "node coordinates persisting in L2",
                           2: "evict-first output", 3: "persisting nodes + evict-first output"}[l2],
             "pattern": ("recomputed in every assembly (count + scan)" if args.no_bind else
                         "bound once per mesh (dgb_plan_bind_mesh, untimed setup); every assembly "

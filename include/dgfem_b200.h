@@ -302,7 +302,8 @@ enum dgb_plan_option {
   DGB_OPTION_MIN_BLOCKS = 2, /* tuning knob: register budget of the P2 kernel (CTAs per SM) */
   DGB_OPTION_L2_POLICY = 3,  /* bit 0: keep node coordinates persisting in L2 (access-policy
                                 window, carve-out sized to the node array at bind time);
-                                bit 1: evict-first L2 hint on the output stream */
+                                bit 1: evict-first L2 hint on the output stream;
+                                -1 (default): evict-first for odd block sizes only */
   DGB_OPTION_BATCH_FUSE = 4, /* dgb_assemble_batch on the tensor-core kernels (default 1): sets
                                 with equal penalties share the per-element work and each CTA
                                 writes every set; 0 = one CTA row per set (grid.y = n) */

@@ -899,7 +899,7 @@ struct dgb_plan {
   size_t l2_persist_bytes = 0;  // persisting-L2 carve-out available to the node window
   size_t l2_window_max = 0;     // cudaDevAttrMaxAccessPolicyWindowSize
   size_t l2_persist_max = 0;    // cudaDevAttrMaxPersistingL2CacheSize
-  int l2_policy = 0;            // bit 0: persist nodes in L2, bit 1: evict-first output
+  int l2_policy = -1;           // bit 0: persist nodes in L2, bit 1: evict-first output; -1 auto
   bool batch_fuse = true;       // dgb_assemble_batch: one CTA writes every kappa set
   // DMMA B fragments of the diagonal terms, one table per kappa (W depends on kappa)
   std::vector<std::pair<double, double*>> bfrag_cache;
@@ -1014,7 +1014,10 @@ void launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_prob
   P.row_begin = out_row_begin;
   P.row_end = out_row_end;
   P.drop_neumann = params->neumann_inflow == DGB_INFLOW_DROP;
-  P.evict_first = (plan->l2_policy & 2) != 0;
+  // auto (-1): evict-first output for odd N2 only (measured, profiles/NOTES.md: P4's 8-byte
+  // fragment stores gain 33%; P2's 16-byte fragment stores lose 5%: the L2 must hold a block
+  // line until its n-tiles have all landed)
+  P.evict_first = plan->l2_policy < 0 ? (N2 % 2 == 1) : (plan->l2_policy & 2) != 0;
   P.ablate = plan->ablate;
   P.prob = *problem;
   const double* h = plan->h_tens.data();
@@ -1193,7 +1196,7 @@ void launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_prob
   cudaLaunchAttribute attr[1];
   int nattr = 0;
   const size_t node_bytes = sizeof(double) * 2 * static_cast<size_t>(mesh->n_nodes);
-  if ((plan->l2_policy & 1) && plan->l2_persist_bytes > 0 && node_bytes > 0) {
+  if (plan->l2_policy > 0 && (plan->l2_policy & 1) && plan->l2_persist_bytes > 0 && node_bytes > 0) {
     attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
     attr[0].val.accessPolicyWindow.base_ptr = const_cast<double*>(mesh->nodes);
     attr[0].val.accessPolicyWindow.num_bytes = std::min(node_bytes, plan->l2_window_max);
@@ -1436,7 +1439,7 @@ int dgb_plan_bind_mesh(dgb_plan* plan, const dgb_mesh_arrays* mesh, int32_t row_
       // carve-out is sized to the node array, never more (it is taken from the write stream).
       static bool carve_out_is_ours = false;
       const size_t node_bytes = sizeof(double) * 2 * static_cast<size_t>(mesh->n_nodes);
-      const size_t want = (plan->l2_policy & 1) ? std::min(node_bytes, plan->l2_persist_max) : 0;
+      const size_t want = (plan->l2_policy > 0 && (plan->l2_policy & 1)) ? std::min(node_bytes, plan->l2_persist_max) : 0;
       plan->l2_persist_bytes = 0;
       if (want == 0 && carve_out_is_ours) {
         cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);
