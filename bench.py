@@ -64,6 +64,8 @@ def parse_args():
     ap.add_argument("--no-fuse", action="store_true",
                     help="batched launch with one CTA row per set (grid.y = methods) instead of "
                          "one per-element pass writing every set")
+    ap.add_argument("--ws", type=int, default=-1,
+                    help="warp-specialised kernel: 0 off, 1 default, 4..12 producer warps of 16")
     ap.add_argument("--no-bind", action="store_true",
                     help="recompute the BSR pattern in every assembly (count + scan launches)")
     return ap.parse_args()
@@ -242,6 +244,8 @@ def run_ours(args, world, rank, local):
         plan.set_option(capi.OPTION_PROFILE_ABLATE, args.ablate)
     if args.no_fuse:
         plan.set_option(capi.OPTION_BATCH_FUSE, 0)
+    if args.ws >= 0:
+        plan.set_option(capi.OPTION_WARP_SPECIALIZED, args.ws)
     stream = torch.cuda.current_stream(local)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=f"cuda:{local}")  # 256 MiB > L2
 

@@ -307,6 +307,9 @@ enum dgb_plan_option {
   DGB_OPTION_BATCH_FUSE = 4, /* dgb_assemble_batch on the tensor-core kernels (default 1): sets
                                 with equal penalties share the per-element work and each CTA
                                 writes every set; 0 = one CTA row per set (grid.y = n) */
+  DGB_OPTION_WARP_SPECIALIZED = 5, /* P-form tensor-core kernels on a bound mesh (default 1):
+                                      persistent producer / consumer warps; 0 = the
+                                      monolithic kernel; 4..12 = producer warps of 16 (tuning) */
   DGB_OPTION_PROFILE_ABLATE = 1000 /* DIAGNOSTICS ONLY -- RESULTS ARE WRONG while nonzero: skip
                                       kernel parts to attribute time (bits: 1 block stores,
                                       2 source evaluation, 4 neighbour blocks, 8 diagonal

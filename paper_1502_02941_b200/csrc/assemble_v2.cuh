@@ -362,6 +362,54 @@ __device__ __forceinline__ void mma_block_store(AF a_at, const double* __restric
   }
 }
 
+// Split form of a fused batch (P-form, sets differing only in kappa): D_s = C . Bc + kappa_s
+// (C . Bq), where Bc is the kappa = 0 table and Bq holds the kappa coefficient of the W rows
+// (Q^T, k-steps 1 and 2: rows 4..11, rows 4 and 5 zero).  Each product runs once; every set
+// costs two DFMAs and a store per fragment.
+template <int KS, int NT, int N2, class AF>
+__device__ __forceinline__ void mma_block_store_split(AF a_at, const double* __restrict__ frag,
+                                                      long long base, const MethodOut* bt,
+                                                      int n_sets, int lane,
+                                                      unsigned long long pol) {
+  static_assert(KS >= 3 && KS <= 7, "split form: W rows in k-steps 1 and 2, A in registers");
+  const int g = lane >> 2, t = lane & 3;
+  double af[4][KS];
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) af[m][ks] = a_at(m, ks);
+  }
+  long long bm[4];
+#pragma unroll
+  for (int m = 0; m < 4; ++m) bm[m] = __shfl_sync(0xffffffffu, base, 8 * m + g);
+  const double* fq = frag + KS * NT * 32;
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) {
+    double bf[KS];
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) bf[ks] = __ldg(frag + (ks * NT + nt) * 32 + lane);
+    const double bq0 = __ldg(fq + nt * 32 + lane), bq1 = __ldg(fq + (NT + nt) * 32 + lane);
+    const int n0 = 8 * nt + 2 * t;
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      double d0 = 0.0, d1 = 0.0, q0 = 0.0, q1 = 0.0;
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) dmma_8x8x4(d0, d1, af[m][ks], bf[ks]);
+      dmma_8x8x4(q0, q1, af[m][1], bq0);
+      dmma_8x8x4(q0, q1, af[m][2], bq1);
+      if (bm[m] >= 0) {
+#pragma unroll
+        for (int s = 0; s < kMaxBatch; ++s) {
+          if (s < n_sets) {
+            const double k = bt[s].kappa;
+            store_entries<N2>(bt[s].val + bm[m], n0, fma(k, q0, d0), fma(k, q1, d1), pol);
+          }
+        }
+      }
+    }
+  }
+}
+
 // Velocity of the kernel's specialised kind (BK = dgb_vector_field kind): no dead branches,
 // so a constant-velocity kernel carries no call into the trigonometric form.
 template <int BK>
@@ -405,6 +453,8 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
   if (P.ablate & 16) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   // this CTA's parameter set (grid.y) and its outputs
+  // split form (fused P-form batch): shared products, kappa applied per set at the store
+  constexpr bool kSplit = FUSE && SM::kMma && !SM::kUForm;
   const int mset = FUSE ? 0 : blockIdx.y;
   const int n_sets = FUSE ? P.n_batch : 1;  // sets this CTA writes: bt[mset .. mset + n_sets)
   const double kappa = P.bt[mset].kappa, sigma_i = P.bt[mset].sigma_i, sigma_b = P.bt[mset].sigma_b;
@@ -797,7 +847,14 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
       for (int k = SM::kTerms; k < SM::kDRows; ++k) sk[k * SM::kCT + lane] = 0.0;  // K padding
       __syncwarp();
       const int g = lane >> 2, t = lane & 3;
-      if (!(P.ablate & 8)) {
+      if constexpr (kSplit) {
+        if (!(P.ablate & 8)) {
+          mma_block_store_split<SM::kKS, SM::kNT, N2>(
+              [&](int m, int ks) { return sk[(4 * ks + t) * SM::kCT + 8 * m + g]; }, o_bfrag,
+              (active && !(P.ablate & 1)) ? static_cast<long long>(rp + diag_slot) * N2 : -1LL,
+              P.bt + mset, n_sets, lane, pol);
+        }
+      } else if (!(P.ablate & 8)) {
 #pragma unroll 1
         for (int s = 0; s < n_sets; ++s) {
           mma_block_store<SM::kKS, SM::kNT, N2>(
@@ -950,6 +1007,56 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
         bm = __shfl_sync(0xffffffffu, my_base, sl);
         if (src < 0) bm = -1;
       };
+      if constexpr (kSplit) {
+        // fused P-form batch: D_s = [X Y0 Y1] . Bxy + kappa_s [Z0 Z1] . Bz, one k-step each
+        static_assert(KO == 2, "split form: neighbour terms X Y0 Y1 | Z0 Z1");
+        auto rows_split = [&](int r, double (&aa)[2], long long& bm) {
+          const int src = pmap[8 * r + g];
+          const int sl = src < 0 ? 0 : src;
+          aa[0] = (src < 0 || t >= 3) ? 0.0 : so[t * SM::kCT + sl];
+          aa[1] = (src < 0 || t >= 2) ? 0.0 : so[(3 + t) * SM::kCT + sl];
+          bm = __shfl_sync(0xffffffffu, my_base, sl);
+          if (src < 0) bm = -1;
+        };
+        double aa[2];
+        long long bm;
+        if (ntiles > 0) rows_split(0, aa, bm);
+#pragma unroll
+        for (int v = 0; v < 3; ++v) {
+          const int tb = v == 0 ? 0 : (v == 1 ? t1 : t2), te = v == 0 ? t1 : (v == 1 ? t2 : ntiles);
+          if (tb == te) continue;
+          const double* fr = o_bfrag + SM::kFragTile + 2 * SM::kNT * 32 +
+                             (l * 3 + v) * SM::kOffTile + lane;
+          double bv[2][SM::kNT];
+#pragma unroll
+          for (int nt = 0; nt < SM::kNT; ++nt) {
+            bv[0][nt] = __ldg(fr + nt * 32);
+            bv[1][nt] = __ldg(fr + (SM::kNT + nt) * 32);
+          }
+#pragma unroll 1
+          for (int r = tb; r < te; ++r) {
+            const double c0 = aa[0], c1 = aa[1];
+            const long long cb = bm;
+            if (r + 1 < ntiles) rows_split(r + 1, aa, bm);
+#pragma unroll
+            for (int nt = 0; nt < SM::kNT; ++nt) {
+              double d0 = 0.0, d1 = 0.0, z0 = 0.0, z1 = 0.0;
+              dmma_8x8x4(d0, d1, c0, bv[0][nt]);
+              dmma_8x8x4(z0, z1, c1, bv[1][nt]);
+              const int n0 = 8 * nt + 2 * t;
+              if (cb >= 0 && !(P.ablate & 1)) {
+#pragma unroll
+                for (int s = 0; s < kMaxBatch; ++s) {
+                  if (s < n_sets) {
+                    const double k = P.bt[mset + s].kappa;
+                    store_entries<N2>(P.bt[mset + s].val + cb, n0, fma(k, z0, d0), fma(k, z1, d1), pol);
+                  }
+                }
+              }
+            }
+          }
+        }
+      } else {
 #pragma unroll 1
       for (int s = 0; s < n_sets; ++s) {
       const double* const o_bfrag = P.bt[mset + s].bfrag;
@@ -1037,6 +1144,7 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
         }
       }
       }  // sets
+      }  // !kSplit
       __syncwarp();  // the row map is rebuilt for the next l
       continue;
     }

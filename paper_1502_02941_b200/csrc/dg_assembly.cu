@@ -25,6 +25,8 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <limits>
+#include <type_traits>
 #include <vector>
 
 #include <cub/device/device_scan.cuh>
@@ -291,6 +293,7 @@ constexpr int kGeo = 13;  // doubles per element: B(4) G(4) det ox oy eps alpha
 }  // namespace dgb
 
 #include "assemble_v2.cuh"
+#include "assemble_ws.cuh"
 #include "assemble_p1.cuh"
 #include "nonlinear.cuh"
 #include "postprocess.cuh"
@@ -901,6 +904,8 @@ struct dgb_plan {
   size_t l2_persist_max = 0;    // cudaDevAttrMaxPersistingL2CacheSize
   int l2_policy = -1;           // bit 0: persist nodes in L2, bit 1: evict-first output; -1 auto
   bool batch_fuse = true;       // dgb_assemble_batch: one CTA writes every kappa set
+  int warp_specialized = 1;     // P-form tensor-core kernel: 0 off, 1 default split, n producers
+  int sm_count = 0;
   // DMMA B fragments of the diagonal terms, one table per kappa (W depends on kappa)
   std::vector<std::pair<double, double*>> bfrag_cache;
   int ablate = 0;  // profiling diagnostics (dgb_plan_set_option 1000)
@@ -1056,6 +1061,17 @@ void launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_prob
   static_assert(LK::TOTAL - LK::PHI == L::TOTAL - L::PHI, "compact layout mismatch");
   std::memcpy(P.t.x, x + (L::PHI - LK::PHI), sizeof(double) * LK::TOTAL);
   const size_t smem = sizeof(double) * (SM::kTr + (THREADS / 32) * SM::kWarp);
+  // tensor-core kernel, sets differing only in kappa: one CTA writes every set (FUSE); in the
+  // P-form the products are shared too (split tables, kappa applied at the store)
+  bool fuse = false, split = false;
+  if constexpr (SM::kMma) {
+    fuse = nb > 1 && plan->batch_fuse;
+    for (int i = 1; i < nb; ++i) {
+      fuse = fuse && params[i].sigma_interior == params[0].sigma_interior &&
+             params[i].sigma_boundary == params[0].sigma_boundary;
+    }
+    split = fuse && !SM::kUForm;
+  }
   if constexpr (SM::kMma) {
     // B operands in mma.m8n8k4 fragment order: lane (g, t) of tile (ks, nt) holds term 4 ks + t
     // at entry 8 nt + g.  First the diagonal terms (K = 16), then per (l, lf) the five
@@ -1066,48 +1082,116 @@ void launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_prob
     // the per-element A rows, so sets differing only in kappa share one A operand -- FUSE).
     // Built once per (plan, kappa) on the host.
     dgb_plan* mp = const_cast<dgb_plan*>(plan);
+    auto ephi = [&](int l, int p, int i) { return x[L::EPHI + (l * NQE + p) * NL + i]; };
+    auto edw = [&](int l, int p, int a, int i) { return x[L::EDW + ((l * NQE + p) * 2 + a) * NL + i]; };
+    // neighbour term of (l, lf) at entry (bi, bj): 0 X, 1 Y0, 2 Y1, 3 Z0, 4 Z1 (Z unscaled)
+    auto neigh = [&](int term, int l, int lf, int bi, int bj) {
+      double acc = 0.0;
+      for (int p = 0; p < NQE; ++p) {
+        const int q = NQE - 1 - p;
+        switch (term) {
+          case 0: acc += x[L::EW + p] * ephi(l, p, bi) * ephi(lf, q, bj); break;
+          case 1: acc += ephi(l, p, bi) * edw(lf, q, 0, bj); break;
+          case 2: acc += ephi(l, p, bi) * edw(lf, q, 1, bj); break;
+          case 3: acc += edw(l, p, 0, bi) * ephi(lf, q, bj); break;
+          default: acc += edw(l, p, 1, bi) * ephi(lf, q, bj); break;
+        }
+      }
+      return acc;
+    };
+    // diagonal term k at entry n for this kappa
+    auto diag = [&](int k, int n, double kap) -> double {
+      const int bi = n / NL, bj = n % NL;
+      const int kw = SM::kWRow;
+      if (k < 3) return x[L::S + k * N2 + n];
+      if (k == 3) return x[L::M + n];
+      if (SM::kTForm && k < kw) {  // TQ[q][a] = phi_q (x) d_a phi_q
+        const int q = (k - 4) / 2, a = (k - 4) % 2;
+        return plan->h_tens[plan->L.PHI + q * NL + bi] * plan->h_dphi[(q * 2 + a) * NL + bj];
+      }
+      if (k < 6) return x[L::T + (k - 4) * N2 + n];
+      if (k < kw) return x[L::TA + (k - 6) * N2 + n];
+      if (k < kw + 6) {  // W = kappa Q^T - Q for this set's kappa
+        const int la = k - kw;
+        return kap * h[V.Q + la * N2 + bj * NL + bi] - h[V.Q + la * N2 + bi * NL + bj];
+      }
+      if constexpr (SM::kUForm) {
+        const int l = (k - kw - 6) / NQE, p = (k - kw - 6) % NQE;
+        return ephi(l, p, bi) * ephi(l, p, bj);  // U[l][p] = phi^l_p (x) phi^l_p
+      }
+      return x[L::P + (k - kw - 6) * N2 + n];
+    };
+    // fragment-order position i of a [ks][nt][lane] table -> (k, n)
+    auto kn = [&](int r, int& k, int& n) {
+      const int ln = r & 31, tile = r >> 5;
+      const int ks = tile / SM::kNT, nt = tile - ks * SM::kNT;
+      k = 4 * ks + (ln & 3);
+      n = 8 * nt + (ln >> 2);
+    };
+    auto upload = [&](const std::vector<double>& hb, double key) {
+      double* frag = nullptr;
+      cuda_check(cudaMalloc(&frag, hb.size() * sizeof(double)), "cudaMalloc(bfrag)");
+      cuda_check(cudaMemcpyAsync(frag, hb.data(), hb.size() * sizeof(double),
+                                 cudaMemcpyHostToDevice, s), "cudaMemcpyAsync(bfrag)");
+      cuda_check(cudaStreamSynchronize(s), "cudaStreamSynchronize(bfrag)");
+      mp->bfrag_cache.emplace_back(key, frag);
+      return frag;
+    };
+    auto cached = [&](double key) -> double* {
+      for (auto& c : mp->bfrag_cache) {
+        if (c.first == key) return c.second;
+      }
+      return nullptr;
+    };
+    if (split) {
+      // fused P-form batch: [diag, kappa = 0][diag kappa coefficient: Q^T at rows 4..11]
+      // [per (l, lf): k-step 0 = X Y0 Y1 0, k-step 1 = Z0 Z1 0 0]
+      const double key = std::numeric_limits<double>::infinity();
+      double* frag = cached(key);
+      if (!frag) {
+        const int nq = 2 * SM::kNT * 32, nn = 2 * SM::kNT * 32;
+        std::vector<double> hb(SM::kFragTile + nq + 9 * nn, 0.0);
+        for (int i = 0; i < SM::kFragTile; ++i) {
+          int k, n;
+          kn(i, k, n);
+          if (k < SM::kTerms && n < N2) hb[i] = diag(k, n, 0.0);
+        }
+        for (int i = 0; i < nq; ++i) {
+          int k, n;
+          kn(i, k, n);
+          k += 4;  // k-steps 1 and 2 of the diagonal operand
+          const int la = k - SM::kWRow;
+          if (n < N2 && la >= 0 && la < 6) hb[SM::kFragTile + i] = h[V.Q + la * N2 + (n % NL) * NL + n / NL];
+        }
+        for (int w = 0; w < 9; ++w) {
+          for (int i = 0; i < nn; ++i) {
+            int k, n;
+            kn(i, k, n);
+            const int term = k < 4 ? (k < 3 ? k : -1) : (k - 4 < 2 ? 3 + (k - 4) : -1);
+            if (n < N2 && term >= 0) {
+              hb[SM::kFragTile + nq + w * nn + i] = neigh(term, w / 3, w % 3, n / NL, n % NL);
+            }
+          }
+        }
+        frag = upload(hb, key);
+      }
+      for (int bi_ = 0; bi_ < nb; ++bi_) P.bt[bi_].bfrag = frag;
+    } else {
     for (int bi_ = 0; bi_ < nb; ++bi_) {
     const double kap = params[bi_].kappa;
-    double* frag = nullptr;
-    for (auto& c : mp->bfrag_cache) {
-      if (c.first == kap) frag = c.second;
-    }
+    double* frag = cached(kap);
     if (!frag) {  // first assembly with this kappa: build and upload (stream-ordered) once
-      auto ephi = [&](int l, int p, int i) { return x[L::EPHI + (l * NQE + p) * NL + i]; };
-      auto edw = [&](int l, int p, int a, int i) { return x[L::EDW + ((l * NQE + p) * 2 + a) * NL + i]; };
       std::vector<double> hb(SM::kBt, 0.0);
       for (int i = 0; i < SM::kBt; ++i) {
-        const bool diag = i < SM::kFragTile;
-        const int which = diag ? 0 : 1 + (i - SM::kFragTile) / SM::kOffTile;  // 1 + l * 3 + lf
-        const int r = diag ? i : (i - SM::kFragTile) % SM::kOffTile;
-        const int ln = r & 31, tile = r >> 5;
-        const int ks = tile / SM::kNT, nt = tile - ks * SM::kNT;
-        const int k = 4 * ks + (ln & 3), n = 8 * nt + (ln >> 2);
-        if (k >= (diag ? SM::kTerms : SM::kOffT) || n >= N2) continue;
+        const bool dg = i < SM::kFragTile;
+        const int which = dg ? 0 : 1 + (i - SM::kFragTile) / SM::kOffTile;  // 1 + l * 3 + lf
+        int k, n;
+        kn(dg ? i : (i - SM::kFragTile) % SM::kOffTile, k, n);
+        if (k >= (dg ? SM::kTerms : SM::kOffT) || n >= N2) continue;
         const int bi = n / NL, bj = n % NL;
         if (which == 0) {
           // diagonal terms: S0 S1 S2 M T0 T1 [TA0..3] W[6] then P[3] (P-form) / U[3][NQE] (U-form)
-          const int kw = SM::kWRow;
-          if (k < 3) {
-            hb[i] = x[L::S + k * N2 + n];
-          } else if (k == 3) {
-            hb[i] = x[L::M + n];
-          } else if (SM::kTForm && k < kw) {  // TQ[q][a] = phi_q (x) d_a phi_q
-            const int q = (k - 4) / 2, a = (k - 4) % 2;
-            hb[i] = plan->h_tens[plan->L.PHI + q * NL + bi] * plan->h_dphi[(q * 2 + a) * NL + bj];
-          } else if (k < 6) {
-            hb[i] = x[L::T + (k - 4) * N2 + n];
-          } else if (k < kw) {
-            hb[i] = x[L::TA + (k - 6) * N2 + n];
-          } else if (k < kw + 6) {  // W = kappa Q^T - Q for this set's kappa
-            const int la = k - kw;
-            hb[i] = kap * h[V.Q + la * N2 + bj * NL + bi] - h[V.Q + la * N2 + bi * NL + bj];
-          } else if constexpr (SM::kUForm) {
-            const int l = (k - kw - 6) / NQE, p = (k - kw - 6) % NQE;
-            hb[i] = ephi(l, p, bi) * ephi(l, p, bj);  // U[l][p] = phi^l_p (x) phi^l_p
-          } else {
-            hb[i] = x[L::P + (k - kw - 6) * N2 + n];
-          }
+          hb[i] = diag(k, n, kap);
         } else {
           // neighbour terms of (l, lf): P-form X Y0 Y1 Z0 Z1; U-form X[p] (per point) Y0 Y1 Z0 Z1
           const int l = (which - 1) / 3, lf = (which - 1) % 3;
@@ -1117,42 +1201,20 @@ void launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_prob
               hb[i] = ephi(l, k, bi) * ephi(lf, NQE - 1 - k, bj);  // X[p], point weight in cV
               continue;
             }
-            term = k - NQE + 1;  // Y0 Y1 Z0 Z1 as terms 1..4 below
+            term = k - NQE + 1;  // Y0 Y1 Z0 Z1 as terms 1..4
           }
-          double acc = 0.0;
-          for (int p = 0; p < NQE; ++p) {
-            const int q = NQE - 1 - p;
-            switch (term) {
-              case 0: acc += x[L::EW + p] * ephi(l, p, bi) * ephi(lf, q, bj); break;
-              case 1: acc += ephi(l, p, bi) * edw(lf, q, 0, bj); break;
-              case 2: acc += ephi(l, p, bi) * edw(lf, q, 1, bj); break;
-              case 3: acc += edw(l, p, 0, bi) * ephi(lf, q, bj); break;
-              default: acc += edw(l, p, 1, bi) * ephi(lf, q, bj); break;
-            }
-          }
+          const double acc = neigh(term, l, lf, bi, bj);
           hb[i] = term >= 3 ? kap * acc : acc;
         }
       }
-      cuda_check(cudaMalloc(&frag, hb.size() * sizeof(double)), "cudaMalloc(bfrag)");
-      cuda_check(cudaMemcpyAsync(frag, hb.data(), hb.size() * sizeof(double),
-                                 cudaMemcpyHostToDevice, s), "cudaMemcpyAsync(bfrag)");
-      cuda_check(cudaStreamSynchronize(s), "cudaStreamSynchronize(bfrag)");
-      mp->bfrag_cache.emplace_back(kap, frag);
+      frag = upload(hb, kap);
     }
     P.bt[bi_].bfrag = frag;
     }
+    }
   }
   auto kernel = dgb::v2::assemble_kernel<NL, NQV, NQE, BK, THREADS, MINB>;
-  // tensor-core kernel, sets differing only in kappa: one CTA writes every set (FUSE)
-  bool fuse = false;
-  if constexpr (SM::kMma) {
-    fuse = nb > 1 && plan->batch_fuse;
-    for (int i = 1; i < nb; ++i) {
-      fuse = fuse && params[i].sigma_interior == params[0].sigma_interior &&
-             params[i].sigma_boundary == params[0].sigma_boundary;
-    }
-    if (fuse) kernel = dgb::v2::assemble_kernel<NL, NQV, NQE, BK, THREADS, MINB, true>;
-  }
+  if (fuse) kernel = dgb::v2::assemble_kernel<NL, NQV, NQE, BK, THREADS, MINB, true>;
   size_t smem_bytes = smem;
   if constexpr (NL == 3 && BK == 0) {
     // P1, constant velocity: the stash-free kernel (assemble_p1.cuh); option MIN_BLOCKS = 11
@@ -1209,6 +1271,46 @@ void launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_prob
   }
   cfg.attrs = attr;
   cfg.numAttrs = nattr;
+  if constexpr (SM::kMma && !SM::kUForm) {
+    // P-form tensor-core kernel on a bound mesh: the warp-specialised persistent kernel
+    // (assemble_ws.cuh), one CTA per SM
+    // measured (profiles/NOTES.md): the split pays off for fused batches only so far
+    if (plan->warp_specialized > 0 && row_ptr_src && (fuse || plan->warp_specialized > 1)) {
+      if (plan->sm_count <= 0) {
+        int dev = 0, n = 0;
+        cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+        cuda_check(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev), "sm count");
+        const_cast<dgb_plan*>(plan)->sm_count = n;
+      }
+      const int n_chunks = (out_row_end - out_row_begin + 31) / 32;
+      cfg.gridDim = dim3(std::max(1, std::min(plan->sm_count, n_chunks)), 1);
+      // producer : consumer warps (16 per CTA): option value 1 = the default per batch kind
+      const int np = plan->warp_specialized == 1 ? 8 : plan->warp_specialized;
+      auto launch = [&](auto tag) {
+        constexpr int NPW = decltype(tag)::value;
+        using WS = dgb::v2::SmemWs<NL, NQV, NQE, NPW, 16 - NPW>;
+        auto wk = fuse ? dgb::v2::assemble_ws_kernel<NL, NQV, NQE, true, NPW, 16 - NPW>
+                       : dgb::v2::assemble_ws_kernel<NL, NQV, NQE, false, NPW, 16 - NPW>;
+        cuda_check(cudaFuncSetAttribute(wk, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        int(WS::kBytes)), "cudaFuncSetAttribute(ws)");
+        cfg.blockDim = dim3(WS::kThreads);
+        cfg.dynamicSmemBytes = WS::kBytes;
+        cuda_check(cudaLaunchKernelEx(&cfg, wk, P), "cudaLaunchKernelEx(ws)");
+      };
+      if constexpr (NL == 6 && NQV == 7) {  // config 2's kernel: producer share tunable
+        switch (np) {
+          case 4: launch(std::integral_constant<int, 4>{}); break;
+          case 6: launch(std::integral_constant<int, 6>{}); break;
+          case 10: launch(std::integral_constant<int, 10>{}); break;
+          case 12: launch(std::integral_constant<int, 12>{}); break;
+          default: launch(std::integral_constant<int, 8>{}); break;
+        }
+      } else {
+        launch(std::integral_constant<int, 8>{});
+      }
+      return;
+    }
+  }
   cuda_check(cudaLaunchKernelEx(&cfg, kernel, P), "cudaLaunchKernelEx(v2)");
 }
 
@@ -1753,6 +1855,7 @@ int dgb_plan_set_option(dgb_plan* plan, int32_t option, int32_t value) {
     case DGB_OPTION_MIN_BLOCKS: plan->minblocks = value; return DGB_OK;
     case DGB_OPTION_L2_POLICY: plan->l2_policy = value; return DGB_OK;
     case DGB_OPTION_BATCH_FUSE: plan->batch_fuse = value != 0; return DGB_OK;
+    case DGB_OPTION_WARP_SPECIALIZED: plan->warp_specialized = value; return DGB_OK;
     // profiling diagnostics (results are WRONG while set): see the header
     case DGB_OPTION_PROFILE_ABLATE: plan->ablate = value; return DGB_OK;
     default: return DGB_STATUS_INVALID_ARGUMENT;

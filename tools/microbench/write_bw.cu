@@ -40,6 +40,26 @@ __global__ void fragment(double* out, int n_elem, int ef) {
       }
 }
 
+__device__ __forceinline__ void st4(double* g, double a, double b, unsigned long long pol) {
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.f64 [%0], {%1, %2, %3, %4}, %5;\n"
+               :: "l"(g), "d"(a), "d"(b), "d"(a), "d"(b), "l"(pol) : "memory");
+}
+// as `fragment`, but each lane stores 32 bytes (256-bit STG): lane (g, t) of n-tile pair
+// (2p, 2p+1) writes entries 16p + 4t .. +3 of row g -- 8 rows x 128 bytes per instruction
+__global__ void fragment32(double* out, int n_elem, int ef) {
+  const unsigned long long pol = pol_of(ef);
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int e0 = warp * 32;
+  if (e0 >= n_elem) return;
+  for (int b = 0; b < 4; ++b)
+    for (int np = 0; np < 3; ++np)
+      for (int m = 0; m < 4; ++m) {
+        const int e = e0 + 8 * m + g, n0 = 16 * np + 4 * t;
+        if (e < n_elem && n0 < 36) st4(out + (long long)e * 144 + b * 36 + n0, 1.0, 2.0, pol);
+      }
+}
+
 int main() {
   const int n_elem = 3 * 131072;            // the config-2 batch: 3 x 131072 element rows
   const long long n = (long long)n_elem * 144;
@@ -51,20 +71,21 @@ int main() {
   cudaEventCreate(&a);
   cudaEventCreate(&b);
   for (int ef = 0; ef < 2; ++ef) {
-    for (int kind = 0; kind < 2; ++kind) {
+    for (int kind = 0; kind < 3; ++kind) {
       float best = 1e9;
       for (int it = 0; it < 10; ++it) {
         cudaMemset(flush, it, 256 << 20);
         cudaEventRecord(a);
         if (kind == 0) coalesced<<<148 * 16, 256>>>(out, n / 2, ef);
-        else fragment<<<(n_elem / 32 * 32 + 127) / 128, 128>>>(out, n_elem, ef);
+        else if (kind == 1) fragment<<<(n_elem + 127) / 128, 128>>>(out, n_elem, ef);
+        else fragment32<<<(n_elem + 127) / 128, 128>>>(out, n_elem, ef);
         cudaEventRecord(b);
         cudaEventSynchronize(b);
         float ms;
         cudaEventElapsedTime(&ms, a, b);
         if (ms < best) best = ms;
       }
-      printf("%-10s evict_first=%d: %.4f ms, %.1f GB/s (%.0f MB)\n", kind ? "fragment" : "coalesced",
+      printf("%-10s evict_first=%d: %.4f ms, %.1f GB/s (%.0f MB)\n", kind == 0 ? "coalesced" : (kind == 1 ? "fragment" : "fragment32"),
              ef, best, n * 8.0 / best / 1e6, n * 8.0 / 1e6);
     }
   }
