@@ -365,9 +365,7 @@ def run_ours(args, world, rank, local):
             "global_mesh": f"{world * cfg.n}x{cfg.n} cells on [0,{world}]x[0,1]" if world > 1 else None,
             "nq_vol": ref.nq_vol, "nq_edge": ref.nq_edge,
             "l2": "flushed between timed steps by a 256 MiB write (outside the timed events)",
-            "l2_policy": {-1: "auto: evict-first output for odd block sizes", 0: "default",
-                          1: "node coordinates persisting in L2",
-                          2: "evict-first output", 3: "persisting nodes + evict-first output"}[l2],
+            "l2_policy": l2_policy_text(l2),
             "pattern": ("recomputed in every assembly (count + scan)" if args.no_bind else
                         "bound once per mesh (dgb_plan_bind_mesh, untimed setup); every assembly "
                         "still writes row_ptr, block columns, values and RHS"),
@@ -877,6 +875,16 @@ def run_mesh(args, world, rank, local):
         "roofline": None, "cpu_baseline": cpu, "e2e": None, "gpu_launches": None,
         "clocks": clocks.summary(),
     }), flush=True)
+
+
+def l2_policy_text(l2: int) -> str:
+    """The bench line's description of DGB_OPTION_L2_POLICY (include/dgfem_b200.h)."""
+    if l2 < 0:
+        return "auto (library default per kernel)"
+    parts = [t for bit, t in ((1, "node coordinates persisting in L2"), (2, "evict-first output"),
+                              (4, "load hints: node gathers evict-last, records evict-first"))
+             if l2 & bit]
+    return " + ".join(parts) or "default"
 
 
 def main():

@@ -303,6 +303,8 @@ enum dgb_plan_option {
   DGB_OPTION_L2_POLICY = 3,  /* bit 0: keep node coordinates persisting in L2 (access-policy
                                 window, carve-out sized to the node array at bind time);
                                 bit 1: evict-first L2 hint on the output stream;
+                                bit 2: L2 hints on the P1 kernel's loads (node gathers
+                                evict-last, per-element records evict-first);
                                 -1 (default): evict-first for odd block sizes only */
   DGB_OPTION_BATCH_FUSE = 4, /* dgb_assemble_batch on the tensor-core kernels (default 1): sets
                                 with equal penalties share the per-element work and each CTA

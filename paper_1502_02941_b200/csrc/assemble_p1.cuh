@@ -54,27 +54,34 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_p1_kernel(
   constexpr bool bound = BOUND;  // bound adjacency record (dgb_plan_bind_mesh) or not
 
   // ---- gathers up front ------------------------------------------------------------------------
+  const bool hints = BOUND && P.load_hints;
+  const unsigned long long pol_g = evict_last_policy(), pol_s = evict_first_policy();
   int v[3];
 #pragma unroll
-  for (int k = 0; k < 3; ++k) v[k] = __ldg(P.elements + 3 * ee + k);
+  for (int k = 0; k < 3; ++k) v[k] = hints ? ld_stream(P.elements + 3 * ee + k, pol_s) : __ldg(P.elements + 3 * ee + k);
   int4 anb = make_int4(0, 0, 0, 0), aop = make_int4(0, 0, 0, 0);
   int rp = 0, rp_next = 0;
   if constexpr (bound) {
-    anb = __ldg(P.adj_nb + (ee - P.row_begin));
-    aop = __ldg(P.adj_op + (ee - P.row_begin));
+    anb = hints ? ld_stream(P.adj_nb + (ee - P.row_begin), pol_s) : __ldg(P.adj_nb + (ee - P.row_begin));
+    aop = hints ? ld_stream(P.adj_op + (ee - P.row_begin), pol_s) : __ldg(P.adj_op + (ee - P.row_begin));
   }
   if (P.row_ptr_src) {
     rp = __ldg(P.row_ptr_src + (ee - P.row_begin));
     rp_next = __ldg(P.row_ptr_src + (ee - P.row_begin + 1));
   }
+  if (P.ablate & 64) {  // (profiling ablation: index records only)
+    if (active) o_rhs[ee - P.row_begin] = double(v[0] + v[1] + v[2] + anb.x + anb.w + aop.x + aop.z + rp + rp_next);
+    return;
+  }
+  const double2* nodes2 = reinterpret_cast<const double2*>(P.nodes);
   double2 pv[3];
 #pragma unroll
-  for (int k = 0; k < 3; ++k) pv[k] = __ldg(reinterpret_cast<const double2*>(P.nodes) + v[k]);
+  for (int k = 0; k < 3; ++k) pv[k] = hints ? ld_hint(nodes2 + v[k], pol_g) : __ldg(nodes2 + v[k]);
   double2 po[3];
   if constexpr (bound) {
-    po[0] = __ldg(reinterpret_cast<const double2*>(P.nodes) + max(aop.x, 0));
-    po[1] = __ldg(reinterpret_cast<const double2*>(P.nodes) + max(aop.y, 0));
-    po[2] = __ldg(reinterpret_cast<const double2*>(P.nodes) + max(aop.z, 0));
+    po[0] = hints ? ld_hint(nodes2 + max(aop.x, 0), pol_g) : __ldg(nodes2 + max(aop.x, 0));
+    po[1] = hints ? ld_hint(nodes2 + max(aop.y, 0), pol_g) : __ldg(nodes2 + max(aop.y, 0));
+    po[2] = hints ? ld_hint(nodes2 + max(aop.z, 0), pol_g) : __ldg(nodes2 + max(aop.z, 0));
   }
   // neighbours first: kind, neighbour, its local edge (and, unbound, its vertices)
   int kindv[3], lfv[3], fv[3], edgev[3], vfv[3][3];
@@ -138,10 +145,14 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_p1_kernel(
   const double B00 = FSUB(pv[1].x, pv[0].x), B01 = FSUB(pv[2].x, pv[0].x);
   const double B10 = FSUB(pv[1].y, pv[0].y), B11 = FSUB(pv[2].y, pv[0].y);
   const double det = FSUB(FMUL(B00, B11), FMUL(B01, B10));
-  const double rdet = 1.0 / det;
+  const double rdet = rcp_nr(det);
   const double G00 = B11 * rdet, G01 = -B10 * rdet;
   const double G10 = -B01 * rdet, G11 = B00 * rdet;
   const double eps = scalar_element(P.prob.diffusion, ee);
+  if (P.ablate & 32) {  // (profiling ablation: gathers and own geometry only)
+    if (active) o_rhs[ee - P.row_begin] = det + po[0].x + po[1].x + po[2].x;
+    return;
+  }
 
   // RHS volume term
   double F[NL];
@@ -154,7 +165,7 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_p1_kernel(
       const double px = FADD(FADD(pv[0].x, FMUL(B00, P.t.x[L::VX + q])), FMUL(B01, P.t.x[L::VY + q]));
       const double py = FADD(FADD(pv[0].y, FMUL(B10, P.t.x[L::VX + q])), FMUL(B11, P.t.x[L::VY + q]));
       const double f = fs.kind == DGB_FIELD_PER_ELEMENT ? __ldg(fs.per_element + ee)
-                                                        : scalar_point_inline(fs, px, py);
+                       : (P.ablate & 2) ? px : scalar_point_inline(fs, px, py);
       const double c = (det * P.t.x[L::VW + q]) * f;
 #pragma unroll
       for (int i = 0; i < NL; ++i) F[i] = fma(c, P.t.x[L::PHI + q * NL + i], F[i]);
@@ -192,8 +203,8 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_p1_kernel(
     const double2 A = o == 0 ? pv[(l + 1) % 3] : pv[(l + 2) % 3];
     const double2 Bn = o == 0 ? pv[(l + 2) % 3] : pv[(l + 1) % 3];
     const double dx = FSUB(Bn.x, A.x), dy = FSUB(Bn.y, A.y);
-    const double h = hypot_dd(dx, dy);  // edge_geometry (mesh.cpp:232-257)
-    const double rh = 1.0 / h;
+    const double h = hypot_fast(dx, dy);  // edge_geometry (mesh.cpp:232-257)
+    const double rh = rcp_nr(h);
     const double tx = dx * rh, ty = dy * rh;
     const double nx = o == 0 ? ty : -ty, ny = o == 0 ? -tx : tx;
     const double ge0 = G00 * nx + G10 * ny, ge1 = G01 * nx + G11 * ny;
@@ -230,6 +241,7 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_p1_kernel(
       cp = sh * (h * eps_e) - up;
       const double cx = up - sh * (h * eps_e);
       // K_ef = sum_p phi^l_p (x) b1_p + a2_p (x) phi^lf_(n-1-p)
+      if (!(P.ablate & 4)) {  // (profiling ablation: skip the neighbour block)
       const double* trm = tr + lf * (NQE * 3 * NL);
       double pm[NQE][NL], b1[NQE][NL];
 #pragma unroll
@@ -259,6 +271,7 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_p1_kernel(
         }
 #pragma unroll
         for (int j = 0; j < NL; ++j) if (active) blk[i * NL + j] = r[j];
+      }
       }
     } else {
       // boundary edge: diffusion (Dirichlet), inflow upwind, and the boundary RHS terms
@@ -343,7 +356,7 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_p1_kernel(
     double* dst = o_val + static_cast<long long>(rp_first) * N2;
     const int head = rp_first & 1;
     const int body = (n - head) & ~1;
-    if (lane == 0 && body > 0) bulk_store(dst + head, srow + head, body * sizeof(double), P.evict_first);
+    if (lane == 0 && body > 0 && !(P.ablate & 1)) bulk_store(dst + head, srow + head, body * sizeof(double), P.evict_first);
     // (a warp past the last row has no range: n <= 0, nothing to write)
     if (lane == 1 && head && n > 0) dst[0] = srow[0];
     if (lane == 2 && n > 0 && head + body < n) dst[n - 1] = srow[n - 1];

@@ -88,6 +88,7 @@ struct Params2 {
   int32_t drop_neumann;
   int32_t evict_first;           // L2 evict-first hint on the output stream
   int32_t ablate;                // profiling diagnostics only (wrong results): see dg_assembly.cu
+  int32_t load_hints;            // L2 hints on loads: gathers evict-last, streamed records evict-first
   int32_t n_batch;
   MethodOut bt[kMaxBatch];
   dgb_problem prob;
@@ -111,6 +112,30 @@ __device__ __forceinline__ unsigned long long evict_first_policy() {
   unsigned long long pol;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
   return pol;
+}
+__device__ __forceinline__ unsigned long long evict_last_policy() {
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol));
+  return pol;
+}
+// Loads with an L2 eviction-priority hint.  Gathered data (node coordinates, read by several
+// elements in random order on a permuted mesh) is kept with evict-last; records read once per
+// element (connectivity, adjacency, row pointers) go evict-first without an L1 allocation.
+__device__ __forceinline__ double2 ld_hint(const double2* p, unsigned long long pol) {
+  double2 r;
+  asm("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;\n" : "=d"(r.x), "=d"(r.y) : "l"(p), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ int4 ld_stream(const int4* p, unsigned long long pol) {
+  int4 r;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0, %1, %2, %3}, [%4], %5;\n"
+      : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ int ld_stream(const int* p, unsigned long long pol) {
+  int r;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;\n" : "=r"(r) : "l"(p), "l"(pol));
+  return r;
 }
 __device__ __forceinline__ void bulk_store(void* g, const void* sm, unsigned bytes,
                                            bool evict_first = false) {
@@ -519,7 +544,7 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
   const double B00 = FSUB(pv[1].x, pv[0].x), B01 = FSUB(pv[2].x, pv[0].x);
   const double B10 = FSUB(pv[1].y, pv[0].y), B11 = FSUB(pv[2].y, pv[0].y);
   const double det = FSUB(FMUL(B00, B11), FMUL(B01, B10));
-  const double rdet = 1.0 / det;
+  const double rdet = rcp_nr(det);
   const double G00 = B11 * rdet, G01 = -B10 * rdet;
   const double G10 = -B01 * rdet, G11 = B00 * rdet;
   const double eps = scalar_element(P.prob.diffusion, ee);
@@ -567,8 +592,8 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
     const double2 A = o == 0 ? pv[(l + 1) % 3] : pv[(l + 2) % 3];
     const double2 Bn = o == 0 ? pv[(l + 2) % 3] : pv[(l + 1) % 3];
     const double dx = FSUB(Bn.x, A.x), dy = FSUB(Bn.y, A.y);
-    const double h = hypot_dd(dx, dy);  // edge_geometry (mesh.cpp:232-257)
-    const double rh = 1.0 / h;
+    const double h = hypot_fast(dx, dy);  // edge_geometry (mesh.cpp:232-257)
+    const double rh = rcp_nr(h);
     const double tx = dx * rh, ty = dy * rh;
     const double nx = o == 0 ? ty : -ty, ny = o == 0 ? -tx : tx;  // outward normal of e
     const double ge0 = G00 * nx + G10 * ny, ge1 = G01 * nx + G11 * ny;

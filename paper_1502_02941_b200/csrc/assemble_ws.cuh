@@ -82,7 +82,7 @@ __device__ __forceinline__ void ws_produce(const Params2<NL, NQV, NQE, false, fa
   const double B00 = FSUB(pv[1].x, pv[0].x), B01 = FSUB(pv[2].x, pv[0].x);
   const double B10 = FSUB(pv[1].y, pv[0].y), B11 = FSUB(pv[2].y, pv[0].y);
   const double det = FSUB(FMUL(B00, B11), FMUL(B01, B10));
-  const double rdet = 1.0 / det;
+  const double rdet = rcp_nr(det);
   const double G00 = B11 * rdet, G01 = -B10 * rdet;
   const double G10 = -B01 * rdet, G11 = B00 * rdet;
   const double eps = scalar_element(P.prob.diffusion, ee);
@@ -114,8 +114,8 @@ __device__ __forceinline__ void ws_produce(const Params2<NL, NQV, NQE, false, fa
     const double2 A = o == 0 ? pv[(l + 1) % 3] : pv[(l + 2) % 3];
     const double2 Bn = o == 0 ? pv[(l + 2) % 3] : pv[(l + 1) % 3];
     const double dx = FSUB(Bn.x, A.x), dy = FSUB(Bn.y, A.y);
-    const double h = hypot_dd(dx, dy);  // edge_geometry (mesh.cpp:232-257)
-    const double rh = 1.0 / h;
+    const double h = hypot_fast(dx, dy);  // edge_geometry (mesh.cpp:232-257)
+    const double rh = rcp_nr(h);
     const double tx = dx * rh, ty = dy * rh;
     const double nx = o == 0 ? ty : -ty, ny = o == 0 ? -tx : tx;
     const double ge0 = G00 * nx + G10 * ny, ge1 = G01 * nx + G11 * ny;

@@ -132,7 +132,7 @@ __device__ __forceinline__ void family(int fn, const double* p, double x, double
     case DGB_FN_GAUSSIAN: {
       const double dx = x - p[1], dy = y - p[2];
       const double r2 = dx * dx + dy * dy;
-      const double v = exp(-p[0] * r2);
+      const double v = exp_fast(-p[0] * r2);
       u = v;
       ux = -2.0 * p[0] * dx * v;
       uy = -2.0 * p[0] * dy * v;
@@ -253,7 +253,7 @@ __device__ __forceinline__ Geo element_geo_coords(double2 p0, double2 p1, double
   g.B10 = p1.y - p0.y;
   g.B11 = p2.y - p0.y;
   g.det = FSUB(FMUL(g.B00, g.B11), FMUL(g.B01, g.B10));
-  const double rd = 1.0 / g.det;
+  const double rd = rcp_nr(g.det);
   g.G00 = g.B11 * rd;
   g.G01 = -g.B10 * rd;
   g.G10 = -g.B01 * rd;
@@ -274,7 +274,7 @@ __device__ __forceinline__ Geo element_geo_fast(const double* __restrict__ nodes
   g.B10 = p1.y - p0.y;
   g.B11 = p2.y - p0.y;
   g.det = FSUB(FMUL(g.B00, g.B11), FMUL(g.B01, g.B10));
-  const double rd = 1.0 / g.det;
+  const double rd = rcp_nr(g.det);
   g.G00 = g.B11 * rd;
   g.G01 = -g.B10 * rd;
   g.G10 = -g.B01 * rd;
@@ -1024,6 +1024,7 @@ void launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_prob
   // line until its n-tiles have all landed)
   P.evict_first = plan->l2_policy < 0 ? (N2 % 2 == 1) : (plan->l2_policy & 2) != 0;
   P.ablate = plan->ablate;
+  P.load_hints = plan->l2_policy > 0 && (plan->l2_policy & 4) != 0;
   P.prob = *problem;
   const double* h = plan->h_tens.data();
   const dgb::Layout& V = plan->L;
@@ -1541,7 +1542,7 @@ int dgb_plan_bind_mesh(dgb_plan* plan, const dgb_mesh_arrays* mesh, int32_t row_
       // carve-out is sized to the node array, never more (it is taken from the write stream).
       static bool carve_out_is_ours = false;
       const size_t node_bytes = sizeof(double) * 2 * static_cast<size_t>(mesh->n_nodes);
-      const size_t want = (plan->l2_policy > 0 && (plan->l2_policy & 1)) ? std::min(node_bytes, plan->l2_persist_max) : 0;
+      const size_t want = (plan->l2_policy > 0 && (plan->l2_policy & 5)) ? std::min(node_bytes, plan->l2_persist_max) : 0;
       plan->l2_persist_bytes = 0;
       if (want == 0 && carve_out_is_ours) {
         cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);

@@ -18,4 +18,9 @@ for c in 2 3 4; do
   ncu --set full --clock-control none --import-source on -k regex:assemble_ -s 1 -c 1 \
       -o gpurun_out/prof_c$c $CMD > gpurun_out/ncu_c$c.log 2>&1
 done
+# summaries on the box (the reports themselves exceed gpurun's 64 MiB return limit)
+mkdir -p gpurun_out/prof_new
+cp profiles/ncu_summary.json gpurun_out/prof_new/ 2>/dev/null
+PROF_DIR=gpurun_out/prof_new python tools/summarize_ncu.py ${TAG:-r01} > gpurun_out/summ.log 2>&1
+rm -f gpurun_out/prof_c2.ncu-rep gpurun_out/prof_c3.ncu-rep
 ls -la gpurun_out

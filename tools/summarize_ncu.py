@@ -18,8 +18,8 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-OUT = os.path.join(ROOT, "gpurun_out")
-PROF = os.path.join(ROOT, "profiles")
+OUT = os.environ.get("NCU_IN", os.path.join(ROOT, "gpurun_out"))
+PROF = os.environ.get("PROF_DIR", os.path.join(ROOT, "profiles"))
 ELEMENTS = {1: 2048, 2: 131072, 3: 2097152, 4: 8388608, 5: 524288}
 
 DETAILS = ["Duration", "DRAM Throughput", "Memory Throughput", "Executed Ipc Active",
