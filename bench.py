@@ -57,7 +57,7 @@ def parse_args():
     ap.add_argument("--ablate", type=int, default=0,
                     help="profiling only, results wrong: skip kernel parts (see dg_assembly.cu)")
     ap.add_argument("--l2-policy", type=int, default=-1,
-                    help="plan L2 policy bits (1: persist nodes, 2: evict-first output); "
+                    help="plan L2 policy bits (1: persist nodes, 2: evict-first output, 4: P1 load hints); "
                          "-1: the default for the config")
     ap.add_argument("--no-batch", action="store_true",
                     help="one dgb_assemble launch per method instead of one dgb_assemble_batch")
@@ -66,6 +66,10 @@ def parse_args():
                          "one per-element pass writing every set")
     ap.add_argument("--ws", type=int, default=-1,
                     help="warp-specialised kernel: 0 off, 1 default, 4..12 producer warps of 16")
+    ap.add_argument("--p1-pipe", type=int, default=-1,
+                    help="P1 pipelined persistent kernel: 0 off, 1 default, 8..10 warps per CTA")
+    ap.add_argument("--l2-carve-mb", type=int, default=0,
+                    help="cap on the persisting-L2 carve-out of L2 policy bits 0/2 (MiB; tuning)")
     ap.add_argument("--no-bind", action="store_true",
                     help="recompute the BSR pattern in every assembly (count + scan launches)")
     return ap.parse_args()
@@ -233,6 +237,8 @@ def run_ours(args, world, rank, local):
     l2 = args.l2_policy  # -1: the library's per-kernel default (profiles/NOTES.md)
     shards = [shard.ShardAssembler(mesh, ref, spec, local, begin, end, bind=False)]
     shards[0].plan.set_option(capi.OPTION_L2_POLICY, l2)
+    if args.l2_carve_mb:  # read at bind time
+        shards[0].plan.set_option(capi.OPTION_L2_CARVEOUT_MB, args.l2_carve_mb)
     if not args.no_bind:
         shards[0].plan.bind_mesh(shards[0].dmesh, begin, end)
     shards += [shard.ShardAssembler(mesh, ref, spec, local, begin, end, share=shards[0])
@@ -246,6 +252,8 @@ def run_ours(args, world, rank, local):
         plan.set_option(capi.OPTION_BATCH_FUSE, 0)
     if args.ws >= 0:
         plan.set_option(capi.OPTION_WARP_SPECIALIZED, args.ws)
+    if args.p1_pipe >= 0:
+        plan.set_option(capi.OPTION_P1_PIPELINE, args.p1_pipe)
     stream = torch.cuda.current_stream(local)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=f"cuda:{local}")  # 256 MiB > L2
 

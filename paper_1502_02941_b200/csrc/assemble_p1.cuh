@@ -23,66 +23,40 @@ struct SmemP1 {
   static constexpr int kTr = (3 * NQE * 3 * NL + 1) & ~1;
 };
 
-template <int NQV, int NQE, int THREADS, int MINB, bool BOUND>
-__global__ void __launch_bounds__(THREADS, MINB) assemble_p1_kernel(
-    const __grid_constant__ Params2<3, NQV, NQE, false, true> P) {
-  constexpr int NL = 3, N2 = 9;
+// Per-CTA trace table tr[l][p][c][j]: phi, w d0 phi, w d1 phi of local edge l's points.
+template <int NQV, int NQE>
+__device__ __forceinline__ void p1_tables(const Params2<3, NQV, NQE, false, true>& P, double* tr) {
+  constexpr int NL = 3;
   using L = Lay<NL, NQV, NQE, false, true>;
-  using SM = SmemP1<NQV, NQE>;
-  extern __shared__ double smem[];
-  double* tr = smem;  // [3][NQE][3][NL]: phi, w d0 phi, w d1 phi of each local edge's points
   for (int i = threadIdx.x; i < 3 * NQE * 3 * NL; i += blockDim.x) {
     const int j = i % NL, c = (i / NL) % 3, p = (i / (3 * NL)) % NQE, l = i / (3 * NL * NQE);
     tr[i] = c == 0 ? P.t.x[L::EPHI + (l * NQE + p) * NL + j]
                    : P.t.x[L::EDW + ((l * NQE + p) * 2 + c - 1) * NL + j];
   }
-  __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int mset = blockIdx.y;
+}
+
+// The block row of one element (one lane), after its gathers: neighbours, slots, block columns,
+// geometry, volume and face terms, the neighbour blocks staged in the warp's row range, and the
+// warp's RHS slice and row range sent by bulk copies.  `wait_stage`: a previous chunk's bulk
+// copies may still be reading the staging (persistent kernel): wait before the first write.
+// `mid()` runs between the volume terms and the edge loop (the persistent kernel issues the next
+// chunk's node gathers there).
+template <int NQV, int NQE, bool BOUND, class MID>
+__device__ __forceinline__ void p1_row(const Params2<3, NQV, NQE, false, true>& P, const double* tr,
+                                       int mset, double* stw, double* srhs, int lane, int e_first,
+                                       int ee, bool active, const int (&v)[3], int4 anb, int4 aop,
+                                       int rp, int rp_next, const double2 (&pv)[3],
+                                       const double2 (&po)[3], bool wait_stage, MID&& mid) {
+  constexpr int NL = 3, N2 = 9;
+  using L = Lay<NL, NQV, NQE, false, true>;
+  using SM = SmemP1<NQV, NQE>;
   const double kappa = P.bt[mset].kappa, sigma_i = P.bt[mset].sigma_i, sigma_b = P.bt[mset].sigma_b;
   int32_t* const o_row_ptr = P.bt[mset].row_ptr;
   int32_t* const o_col = P.bt[mset].col;
   double* const o_val = P.bt[mset].val;
   double* const o_rhs = P.bt[mset].rhs;
-  double* stw = smem + SM::kTr + warp * SM::kWarp;
-  double* srhs = stw + SM::kStage;
-
-  const int e = P.row_begin + blockIdx.x * blockDim.x + threadIdx.x;
-  const bool active = e < P.row_end;
-  const int ee = active ? e : P.row_end - 1;
   const dgb_vector_field& bf = P.prob.advection;
-  constexpr bool bound = BOUND;  // bound adjacency record (dgb_plan_bind_mesh) or not
-
-  // ---- gathers up front ------------------------------------------------------------------------
-  const bool hints = BOUND && P.load_hints;
-  const unsigned long long pol_g = evict_last_policy(), pol_s = evict_first_policy();
-  int v[3];
-#pragma unroll
-  for (int k = 0; k < 3; ++k) v[k] = hints ? ld_stream(P.elements + 3 * ee + k, pol_s) : __ldg(P.elements + 3 * ee + k);
-  int4 anb = make_int4(0, 0, 0, 0), aop = make_int4(0, 0, 0, 0);
-  int rp = 0, rp_next = 0;
-  if constexpr (bound) {
-    anb = hints ? ld_stream(P.adj_nb + (ee - P.row_begin), pol_s) : __ldg(P.adj_nb + (ee - P.row_begin));
-    aop = hints ? ld_stream(P.adj_op + (ee - P.row_begin), pol_s) : __ldg(P.adj_op + (ee - P.row_begin));
-  }
-  if (P.row_ptr_src) {
-    rp = __ldg(P.row_ptr_src + (ee - P.row_begin));
-    rp_next = __ldg(P.row_ptr_src + (ee - P.row_begin + 1));
-  }
-  if (P.ablate & 64) {  // (profiling ablation: index records only)
-    if (active) o_rhs[ee - P.row_begin] = double(v[0] + v[1] + v[2] + anb.x + anb.w + aop.x + aop.z + rp + rp_next);
-    return;
-  }
-  const double2* nodes2 = reinterpret_cast<const double2*>(P.nodes);
-  double2 pv[3];
-#pragma unroll
-  for (int k = 0; k < 3; ++k) pv[k] = hints ? ld_hint(nodes2 + v[k], pol_g) : __ldg(nodes2 + v[k]);
-  double2 po[3];
-  if constexpr (bound) {
-    po[0] = hints ? ld_hint(nodes2 + max(aop.x, 0), pol_g) : __ldg(nodes2 + max(aop.x, 0));
-    po[1] = hints ? ld_hint(nodes2 + max(aop.y, 0), pol_g) : __ldg(nodes2 + max(aop.y, 0));
-    po[2] = hints ? ld_hint(nodes2 + max(aop.z, 0), pol_g) : __ldg(nodes2 + max(aop.z, 0));
-  }
+  constexpr bool bound = BOUND;
   // neighbours first: kind, neighbour, its local edge (and, unbound, its vertices)
   int kindv[3], lfv[3], fv[3], edgev[3], vfv[3][3];
 #pragma unroll
@@ -195,6 +169,11 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_p1_kernel(
     }
   }
 
+  mid();
+  if (wait_stage) {
+    if (lane == 0) bulk_wait_read();
+    __syncwarp();
+  }
   // ---- edges: face terms into the diagonal, neighbour blocks staged at once --------------------
 #pragma unroll
   for (int l = 0; l < 3; ++l) {
@@ -341,7 +320,6 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_p1_kernel(
     for (int i = 0; i < NL; ++i) srhs[lane * NL + i] = F[i];
     fence_smem_to_async();  // every writer: its shared-memory stores -> the async (TMA) proxy
     __syncwarp();
-    const int e_first = blockIdx.x * blockDim.x + warp * 32;
     const int n_here = min(32, P.row_end - P.row_begin - e_first);
     double* dst = o_rhs + static_cast<long long>(e_first) * NL;
     const int bulk = (n_here * NL) & ~1;
@@ -360,6 +338,177 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_p1_kernel(
     // (a warp past the last row has no range: n <= 0, nothing to write)
     if (lane == 1 && head && n > 0) dst[0] = srow[0];
     if (lane == 2 && n > 0 && head + body < n) dst[n - 1] = srow[n - 1];
+  }
+}
+
+template <int NQV, int NQE, int THREADS, int MINB, bool BOUND>
+__global__ void __launch_bounds__(THREADS, MINB) assemble_p1_kernel(
+    const __grid_constant__ Params2<3, NQV, NQE, false, true> P) {
+  constexpr int NL = 3;
+  using L = Lay<NL, NQV, NQE, false, true>;
+  using SM = SmemP1<NQV, NQE>;
+  extern __shared__ double smem[];
+  double* tr = smem;
+  p1_tables<NQV, NQE>(P, tr);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int mset = blockIdx.y;
+  double* const o_rhs = P.bt[mset].rhs;
+  double* stw = smem + SM::kTr + warp * SM::kWarp;
+  double* srhs = stw + SM::kStage;
+
+  const int e = P.row_begin + blockIdx.x * blockDim.x + threadIdx.x;
+  const bool active = e < P.row_end;
+  const int ee = active ? e : P.row_end - 1;
+  constexpr bool bound = BOUND;  // bound adjacency record (dgb_plan_bind_mesh) or not
+
+  // ---- gathers up front ------------------------------------------------------------------------
+  const bool hints = BOUND && P.load_hints;
+  const unsigned long long pol_g = evict_last_policy(), pol_s = evict_first_policy();
+  int v[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) v[k] = hints ? ld_stream(P.elements + 3 * ee + k, pol_s) : __ldg(P.elements + 3 * ee + k);
+  int4 anb = make_int4(0, 0, 0, 0), aop = make_int4(0, 0, 0, 0);
+  int rp = 0, rp_next = 0;
+  if constexpr (bound) {
+    anb = hints ? ld_stream(P.adj_nb + (ee - P.row_begin), pol_s) : __ldg(P.adj_nb + (ee - P.row_begin));
+    aop = hints ? ld_stream(P.adj_op + (ee - P.row_begin), pol_s) : __ldg(P.adj_op + (ee - P.row_begin));
+  }
+  if (P.row_ptr_src) {
+    rp = __ldg(P.row_ptr_src + (ee - P.row_begin));
+    rp_next = __ldg(P.row_ptr_src + (ee - P.row_begin + 1));
+  }
+  if (P.ablate & 64) {  // (profiling ablation: index records only)
+    if (active) o_rhs[ee - P.row_begin] = double(v[0] + v[1] + v[2] + anb.x + anb.w + aop.x + aop.z + rp + rp_next);
+    return;
+  }
+  const double2* nodes2 = reinterpret_cast<const double2*>(P.nodes);
+  double2 pv[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) pv[k] = hints ? ld_hint(nodes2 + v[k], pol_g) : __ldg(nodes2 + v[k]);
+  double2 po[3];
+  if constexpr (bound) {
+    po[0] = hints ? ld_hint(nodes2 + max(aop.x, 0), pol_g) : __ldg(nodes2 + max(aop.x, 0));
+    po[1] = hints ? ld_hint(nodes2 + max(aop.y, 0), pol_g) : __ldg(nodes2 + max(aop.y, 0));
+    po[2] = hints ? ld_hint(nodes2 + max(aop.z, 0), pol_g) : __ldg(nodes2 + max(aop.z, 0));
+  }
+  p1_row<NQV, NQE, BOUND>(P, tr, mset, stw, srhs, lane, blockIdx.x * blockDim.x + warp * 32, ee,
+                          active, v, anb, aop, rp, rp_next, pv, po, false, [] {});
+  if (lane == 0) bulk_wait_all();
+}
+
+
+
+// ---- persistent, software-pipelined P1 kernel (bound mesh) ------------------------------------
+//
+// The one-shot kernel above spends its warps' time in a serial chain per 32-element chunk:
+// index records (one DRAM round trip), then the node coordinates they name (a second, random,
+// round trip), then the arithmetic and the stores.  Measured on config 4 (profiles/NOTES.md),
+// the gathers alone take 0.35-0.40 ms of the 1.17 ms kernel, and 16 warps per SM do not hide
+// them.  Here every warp walks its own sequence of chunks with both loads in flight one chunk
+// ahead, landing in shared memory through asynchronous copies (LDGSTS: no registers held while
+// they are in flight):
+//
+//   chunk j:  wait (its records and nodes have landed); read them into registers
+//             issue the record copies of chunk j+1
+//             source and volume terms of chunk j
+//             wait (records of j+1); issue the node copies of chunk j+1
+//             edge terms, neighbour blocks and stores of chunk j
+//
+// Each lane reads only what it copied itself, so the per-thread cp.async groups are the only
+// synchronisation on the input side.
+template <int NQV, int NQE, int WARPS>
+struct SmemP1Pipe {
+  using SM = SmemP1<NQV, NQE>;
+  // one chunk's records (ints): adj_nb [32] int4, adj_op [32] int4, elements [96], rp [32], rp+1 [32]
+  static constexpr int kNb = 0, kOp = 128, kV = 256, kRp = 352, kRpn = 384, kIdxInts = 416;
+  static constexpr int kIdx = kIdxInts / 2;      // doubles
+  static constexpr int kNode = 32 * 6 * 2;       // doubles: [6][32] double2
+  static constexpr int kWarp = kIdx + kNode + SM::kStage + SM::kRhs;
+  static constexpr size_t kBytes = sizeof(double) * (size_t(SM::kTr) + size_t(WARPS) * kWarp);
+};
+
+__device__ __forceinline__ void cp_async16(void* sm, const void* g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" :: "r"(smem_addr(sm)), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* sm, const void* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" :: "r"(smem_addr(sm)), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
+template <int NQV, int NQE, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32, 1) assemble_p1_pipe_kernel(
+    const __grid_constant__ Params2<3, NQV, NQE, false, true> P) {
+  constexpr int NL = 3;
+  using L = Lay<NL, NQV, NQE, false, true>;
+  using SM = SmemP1<NQV, NQE>;
+  using PS = SmemP1Pipe<NQV, NQE, WARPS>;
+  extern __shared__ double smem[];
+  double* tr = smem;
+  p1_tables<NQV, NQE>(P, tr);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int mset = blockIdx.y;
+  double* wbase = smem + SM::kTr + warp * PS::kWarp;
+  int* idx = reinterpret_cast<int*>(wbase);                     // one chunk's records
+  double2* nod = reinterpret_cast<double2*>(wbase + PS::kIdx);  // one chunk's nodes [6][32]
+  double* stw = wbase + PS::kIdx + PS::kNode;
+  double* srhs = stw + SM::kStage;
+
+  const int n_rows = P.row_end - P.row_begin;
+  const int n_chunks = (n_rows + 31) >> 5;
+  const int gw = blockIdx.x * WARPS + warp, n_gw = gridDim.x * WARPS;
+  const int n_local = gw < n_chunks ? (n_chunks - 1 - gw) / n_gw + 1 : 0;
+  const double2* nodes2 = reinterpret_cast<const double2*>(P.nodes);
+
+  auto issue_records = [&](int j) {
+    const int e = P.row_begin + (gw + j * n_gw) * 32 + lane;
+    const int r = min(e, P.row_end - 1) - P.row_begin;
+    cp_async16(idx + PS::kNb + 4 * lane, P.adj_nb + r);
+    cp_async16(idx + PS::kOp + 4 * lane, P.adj_op + r);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) cp_async4(idx + PS::kV + 3 * lane + k, P.elements + 3 * (P.row_begin + r) + k);
+    cp_async4(idx + PS::kRp + lane, P.row_ptr_src + r);
+    cp_async4(idx + PS::kRpn + lane, P.row_ptr_src + r + 1);
+    cp_async_commit();
+  };
+  auto issue_nodes = [&]() {  // from the landed records
+#pragma unroll
+    for (int k = 0; k < 3; ++k) cp_async16(nod + k * 32 + lane, nodes2 + idx[PS::kV + 3 * lane + k]);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) cp_async16(nod + (3 + k) * 32 + lane, nodes2 + max(idx[PS::kOp + 4 * lane + k], 0));
+    cp_async_commit();
+  };
+
+  if (n_local > 0) {
+    issue_records(0);
+    cp_async_wait_all();
+    issue_nodes();
+  }
+#pragma unroll 1
+  for (int j = 0; j < n_local; ++j) {
+    cp_async_wait_all();  // chunk j's records and nodes have landed
+    // everything of chunk j into registers; the buffers take chunk j + 1 from here on
+    const int v[3] = {idx[PS::kV + 3 * lane], idx[PS::kV + 3 * lane + 1], idx[PS::kV + 3 * lane + 2]};
+    const int4 anb = *reinterpret_cast<const int4*>(idx + PS::kNb + 4 * lane);
+    const int4 aop = *reinterpret_cast<const int4*>(idx + PS::kOp + 4 * lane);
+    const int rp = idx[PS::kRp + lane], rp_next = idx[PS::kRpn + lane];
+    const double2 pv[3] = {nod[lane], nod[32 + lane], nod[64 + lane]};
+    const double2 po[3] = {nod[96 + lane], nod[128 + lane], nod[160 + lane]};
+    const bool more = j + 1 < n_local;
+    if (more) issue_records(j + 1);
+    const int e_first = (gw + j * n_gw) * 32;
+    const int e = P.row_begin + e_first + lane;
+    const bool active = e < P.row_end;
+    const int ee = active ? e : P.row_end - 1;
+    p1_row<NQV, NQE, true>(P, tr, mset, stw, srhs, lane, e_first, ee, active, v, anb, aop, rp,
+                           rp_next, pv, po, j > 0, [&] {
+                             if (more) {
+                               cp_async_wait_all();  // chunk j + 1's records
+                               issue_nodes();
+                             }
+                           });
   }
   if (lane == 0) bulk_wait_all();
 }

@@ -906,6 +906,8 @@ struct dgb_plan {
   bool batch_fuse = true;       // dgb_assemble_batch: one CTA writes every kappa set
   int warp_specialized = 1;     // P-form tensor-core kernel: 0 off, 1 default split, n producers
   int sm_count = 0;
+  int l2_carve_mb = 0;          // persisting-L2 carve-out cap (MiB, 0: the node array) -- tuning
+  int p1_pipe = 0;              // P1 bound mesh: persistent pipelined kernel (0 off: measured slower, 1 on, n warps)
   // DMMA B fragments of the diagonal terms, one table per kappa (W depends on kappa)
   std::vector<std::pair<double, double*>> bfrag_cache;
   int ablate = 0;  // profiling diagnostics (dgb_plan_set_option 1000)
@@ -1312,6 +1314,35 @@ void launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_prob
       return;
     }
   }
+  if constexpr (NL == 3 && BK == 0) {
+    // P1 on a bound mesh: the persistent software-pipelined kernel (assemble_p1.cuh)
+    if (plan->p1_pipe > 0 && row_ptr_src && plan->minblocks != 11) {
+      if (plan->sm_count <= 0) {
+        int dev = 0, n = 0;
+        cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+        cuda_check(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev), "sm count");
+        const_cast<dgb_plan*>(plan)->sm_count = n;
+      }
+      auto launch = [&](auto tag) {
+        constexpr int W = decltype(tag)::value;
+        using PS = dgb::v2::SmemP1Pipe<NQV, NQE, W>;
+        auto pk = dgb::v2::assemble_p1_pipe_kernel<NQV, NQE, W>;
+        cuda_check(cudaFuncSetAttribute(pk, cudaFuncAttributeMaxDynamicSharedMemorySize, int(PS::kBytes)),
+                   "cudaFuncSetAttribute(p1 pipe)");
+        const int n_chunks = (out_row_end - out_row_begin + 31) / 32;
+        cfg.gridDim = dim3(std::max(1, std::min(plan->sm_count, (n_chunks + W - 1) / W)), nb);
+        cfg.blockDim = dim3(32 * W);
+        cfg.dynamicSmemBytes = PS::kBytes;
+        cuda_check(cudaLaunchKernelEx(&cfg, pk, P), "cudaLaunchKernelEx(p1 pipe)");
+      };
+      switch (plan->p1_pipe) {
+        case 12: launch(std::integral_constant<int, 12>{}); break;
+        case 14: launch(std::integral_constant<int, 14>{}); break;
+        default: launch(std::integral_constant<int, 15>{}); break;
+      }
+      return;
+    }
+  }
   cuda_check(cudaLaunchKernelEx(&cfg, kernel, P), "cudaLaunchKernelEx(v2)");
 }
 
@@ -1542,7 +1573,8 @@ int dgb_plan_bind_mesh(dgb_plan* plan, const dgb_mesh_arrays* mesh, int32_t row_
       // carve-out is sized to the node array, never more (it is taken from the write stream).
       static bool carve_out_is_ours = false;
       const size_t node_bytes = sizeof(double) * 2 * static_cast<size_t>(mesh->n_nodes);
-      const size_t want = (plan->l2_policy > 0 && (plan->l2_policy & 5)) ? std::min(node_bytes, plan->l2_persist_max) : 0;
+      size_t want = (plan->l2_policy > 0 && (plan->l2_policy & 5)) ? std::min(node_bytes, plan->l2_persist_max) : 0;
+      if (want > 0 && plan->l2_carve_mb > 0) want = std::min(want, size_t(plan->l2_carve_mb) << 20);
       plan->l2_persist_bytes = 0;
       if (want == 0 && carve_out_is_ours) {
         cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);
@@ -1857,6 +1889,8 @@ int dgb_plan_set_option(dgb_plan* plan, int32_t option, int32_t value) {
     case DGB_OPTION_L2_POLICY: plan->l2_policy = value; return DGB_OK;
     case DGB_OPTION_BATCH_FUSE: plan->batch_fuse = value != 0; return DGB_OK;
     case DGB_OPTION_WARP_SPECIALIZED: plan->warp_specialized = value; return DGB_OK;
+    case DGB_OPTION_P1_PIPELINE: plan->p1_pipe = value; return DGB_OK;
+    case DGB_OPTION_L2_CARVEOUT_MB: plan->l2_carve_mb = value; return DGB_OK;
     // profiling diagnostics (results are WRONG while set): see the header
     case DGB_OPTION_PROFILE_ABLATE: plan->ablate = value; return DGB_OK;
     default: return DGB_STATUS_INVALID_ARGUMENT;
