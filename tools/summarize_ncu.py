@@ -98,7 +98,7 @@ def launch_shares(path: str) -> dict:
         if len(r) <= vi:
             continue
         name = r[ki]
-        short = ("assemble_kernel" if ("assemble_kernel" in name or "assemble_p1_kernel" in name) else
+        short = ("assemble_kernel" if "assemble_" in name else
                  "count_blocks_kernel" if "count_blocks" in name else
                  "cub_scan" if "cub" in name.lower() or "Scan" in name else name[:40])
         try:
