@@ -1288,12 +1288,13 @@ void launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_prob
       const int n_chunks = (out_row_end - out_row_begin + 31) / 32;
       cfg.gridDim = dim3(std::max(1, std::min(plan->sm_count, n_chunks)), 1);
       // producer : consumer warps (16 per CTA): option value 1 = the default per batch kind
-      const int np = plan->warp_specialized == 1 ? 8 : plan->warp_specialized;
-      auto launch = [&](auto tag) {
-        constexpr int NPW = decltype(tag)::value;
-        using WS = dgb::v2::SmemWs<NL, NQV, NQE, NPW, 16 - NPW>;
-        auto wk = fuse ? dgb::v2::assemble_ws_kernel<NL, NQV, NQE, true, NPW, 16 - NPW>
-                       : dgb::v2::assemble_ws_kernel<NL, NQV, NQE, false, NPW, 16 - NPW>;
+      // measured on config 2 (profiles/NOTES.md): the per-element pass is the longer side
+      const int np = plan->warp_specialized == 1 ? 10 : plan->warp_specialized;
+      auto launch = [&](auto tag, auto ctag) {
+        constexpr int NPW = decltype(tag)::value, NCW = decltype(ctag)::value;
+        using WS = dgb::v2::SmemWs<NL, NQV, NQE, NPW, NCW>;
+        auto wk = fuse ? dgb::v2::assemble_ws_kernel<NL, NQV, NQE, true, NPW, NCW>
+                       : dgb::v2::assemble_ws_kernel<NL, NQV, NQE, false, NPW, NCW>;
         cuda_check(cudaFuncSetAttribute(wk, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         int(WS::kBytes)), "cudaFuncSetAttribute(ws)");
         cfg.blockDim = dim3(WS::kThreads);
@@ -1301,15 +1302,19 @@ void launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_prob
         cuda_check(cudaLaunchKernelEx(&cfg, wk, P), "cudaLaunchKernelEx(ws)");
       };
       if constexpr (NL == 6 && NQV == 7) {  // config 2's kernel: producer share tunable
+        // n (4..12): n producers of 16 warps; 100 p + c: p producers, c consumers
         switch (np) {
-          case 4: launch(std::integral_constant<int, 4>{}); break;
-          case 6: launch(std::integral_constant<int, 6>{}); break;
-          case 10: launch(std::integral_constant<int, 10>{}); break;
-          case 12: launch(std::integral_constant<int, 12>{}); break;
-          default: launch(std::integral_constant<int, 8>{}); break;
+          case 4: launch(std::integral_constant<int, 4>{}, std::integral_constant<int, 12>{}); break;
+          case 6: launch(std::integral_constant<int, 6>{}, std::integral_constant<int, 10>{}); break;
+          case 8: launch(std::integral_constant<int, 8>{}, std::integral_constant<int, 8>{}); break;
+          case 12: launch(std::integral_constant<int, 12>{}, std::integral_constant<int, 4>{}); break;
+          case 1105: launch(std::integral_constant<int, 11>{}, std::integral_constant<int, 5>{}); break;
+          case 1206: launch(std::integral_constant<int, 12>{}, std::integral_constant<int, 6>{}); break;
+          case 1406: launch(std::integral_constant<int, 14>{}, std::integral_constant<int, 6>{}); break;
+          default: launch(std::integral_constant<int, 10>{}, std::integral_constant<int, 6>{}); break;
         }
       } else {
-        launch(std::integral_constant<int, 8>{});
+        launch(std::integral_constant<int, 8>{}, std::integral_constant<int, 8>{});
       }
       return;
     }
