@@ -245,6 +245,8 @@ struct Smem {
   //                       neighbour X[NQE] Y0 Y1 Z0 Z1 (4 + NQE) -- per-point upwind terms
   //  T-form (trigonometric b, P4): diagonal S0 S1 S2 M TQ[NQV][2] W[6] U[3][NQE], the
   //                       per-point transport phi_q (x) d_a phi_q as 2 NQV rank-1 operands
+  // (P1 on this path, through the warp-specialised kernel, measured 1.90 ms on config 4 vs the
+  // CUDA-core P1 kernel's 1.16 ms: 9-entry blocks pad to 16 columns and store 8 bytes at a time)
   static constexpr bool kMma = (NL == 6 && BK == 0) || (NL == 10 && (BK == 0 || BK == 1)) ||
                                (NL == 15 && BK == 2);
   static constexpr bool kTForm = BK == 2;

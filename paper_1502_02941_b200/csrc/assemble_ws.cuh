@@ -49,7 +49,7 @@ struct SmemWs {
 // Producer: the per-element pass of the chunk starting at e_first (relative to row_begin).
 // Mirrors assemble_kernel phases A0-A2 (assemble_v2.cuh) for BK = 0 on a bound mesh.
 template <int NL, int NQV, int NQE, bool FUSE>
-__device__ __forceinline__ void ws_produce(const Params2<NL, NQV, NQE, false, false>& P,
+__device__ __forceinline__ void ws_produce(const Params2<NL, NQV, NQE, false, full_tensors(NL, 0)>& P,
                                            int e_first, int lane, double* slot, double* srhs,
                                            int n_sets) {
   using L = Lay<NL, NQV, NQE, false, false>;
@@ -360,7 +360,7 @@ __device__ __forceinline__ void ws_diag(AF a_at, const double* __restrict__ frag
 
 // Consumer: the block products and fragment stores of a produced chunk.
 template <int NL, int NQV, int NQE, bool FUSE>
-__device__ __forceinline__ void ws_consume(const Params2<NL, NQV, NQE, false, false>& P, int lane,
+__device__ __forceinline__ void ws_consume(const Params2<NL, NQV, NQE, false, full_tensors(NL, 0)>& P, int lane,
                                            double* slot, int n_sets) {
   using SM = Smem<NL, NQV, NQE, 0>;
   constexpr int N2 = NL * NL, CT = SM::kCT, NT = SM::kNT;
@@ -484,7 +484,7 @@ __device__ __forceinline__ void ws_consume(const Params2<NL, NQV, NQE, false, fa
 // NC consumer warps through a ring of NS slots: chunk k uses slot k % NS, round k / NS.
 template <int NL, int NQV, int NQE, bool FUSE, int NPROD, int NCONS>
 __global__ void __launch_bounds__(SmemWs<NL, NQV, NQE, NPROD, NCONS>::kThreads, 1)
-    assemble_ws_kernel(const __grid_constant__ Params2<NL, NQV, NQE, false, false> P) {
+    assemble_ws_kernel(const __grid_constant__ Params2<NL, NQV, NQE, false, full_tensors(NL, 0)> P) {
   using W = SmemWs<NL, NQV, NQE, NPROD, NCONS>;
   constexpr int NP = W::NP, NC = W::NC, NS = W::NS;
   extern __shared__ double smem[];

@@ -329,7 +329,7 @@ def test_warp_specialized_equals_monolithic(degree, batch):
     methods = [capi.SIPG, capi.NIPG, capi.IIPG] if batch else [capi.NIPG]
     params = [dgfem.config_parameters(cfg, m) for m in methods]
     got = {}
-    for ws in (1, 0):
+    for ws in (8, 0):  # 8: forced on (8 producer warps), also for single assemblies
         a = [shard.ShardAssembler(mesh, ref, spec, 0, 0, mesh.n_elements, bind=True)]
         a += [shard.ShardAssembler(mesh, ref, spec, 0, 0, mesh.n_elements, share=a[0]) for _ in methods[1:]]
         a[0].plan.set_option(capi.OPTION_WARP_SPECIALIZED, ws)
@@ -338,7 +338,7 @@ def test_warp_specialized_equals_monolithic(degree, batch):
         else:
             a[0].assemble(params[0])
         got[ws] = [to_np(x.out) for x in a]
-    for x, y in zip(got[1], got[0]):
+    for x, y in zip(got[8], got[0]):
         for u, v in zip(x[:2], y[:2]):
             assert np.array_equal(u, v)
         for u, v in zip(x[2:], y[2:]):
