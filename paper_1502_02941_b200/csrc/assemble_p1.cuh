@@ -37,8 +37,8 @@ __device__ __forceinline__ void p1_tables(const Params2<3, NQV, NQE, false, true
 
 // The block row of one element (one lane), after its gathers: neighbours, slots, block columns,
 // geometry, volume and face terms, the neighbour blocks staged in the warp's row range, and the
-// warp's RHS slice and row range sent by bulk copies.  `wait_stage`: a previous chunk's bulk
-// copies may still be reading the staging (persistent kernel): wait before the first write.
+// warp's RHS slice and row range sent by bulk copies.  `wait_stage` (persistent kernel): the
+// staging is reused by the next chunk, so the warp copies its row range out itself.
 // `mid()` runs between the volume terms and the edge loop (the persistent kernel issues the next
 // chunk's node gathers there).
 template <int NQV, int NQE, bool BOUND, class MID>
@@ -170,10 +170,6 @@ __device__ __forceinline__ void p1_row(const Params2<3, NQV, NQE, false, true>& 
   }
 
   mid();
-  if (wait_stage) {
-    if (lane == 0) bulk_wait_read();
-    __syncwarp();
-  }
   // ---- edges: face terms into the diagonal, neighbour blocks staged at once --------------------
 #pragma unroll
   for (int l = 0; l < 3; ++l) {
@@ -314,8 +310,12 @@ __device__ __forceinline__ void p1_row(const Params2<3, NQV, NQE, false, true>& 
     for (int k = 0; k < N2; ++k) myrow[slot_of[0] * N2 + k] = acc[k];
   }
 
-  // ---- RHS: the warp's contiguous slice in one bulk copy ------------------------------------------
-  {
+  // ---- RHS: the warp's contiguous slice in one bulk copy (srhs == nullptr: direct stores) ----------
+  if (srhs == nullptr) {
+    double* dst = o_rhs + static_cast<long long>(e_first + lane) * NL;
+#pragma unroll
+    for (int i = 0; i < NL; ++i) if (active) dst[i] = F[i];
+  } else {
 #pragma unroll
     for (int i = 0; i < NL; ++i) srhs[lane * NL + i] = F[i];
     fence_smem_to_async();  // every writer: its shared-memory stores -> the async (TMA) proxy
@@ -327,6 +327,21 @@ __device__ __forceinline__ void p1_row(const Params2<3, NQV, NQE, false, true>& 
     for (int idx = bulk + lane; idx < n_here * NL; idx += 32) dst[idx] = srhs[idx];
   }
   // ---- the warp's row range: one bulk copy, unaligned head / tail by hand ----------------------------
+  if (wait_stage) {
+    // persistent kernel: the warp copies its range itself (16-byte coalesced stores), so the
+    // staging is free again at once -- the bulk copy's read-back wait was 15% of the stall
+    // samples (profiles/NOTES.md)
+    __syncwarp();
+    const int n = (rp_last - rp_first) * N2;
+    double* dst = o_val + static_cast<long long>(rp_first) * N2;
+    const int head = rp_first & 1;
+    const unsigned long long pol = output_policy(P.evict_first);
+    for (int i = head + 2 * lane; i + 1 < n; i += 64) store_pair(dst + i, srow[i], srow[i + 1], pol);
+    if (lane == 1 && head && n > 0) dst[0] = srow[0];
+    if (lane == 2 && n > 0 && ((n - head) & 1)) dst[n - 1] = srow[n - 1];
+    __syncwarp();
+    return;
+  }
   fence_smem_to_async();  // every writer: its staged blocks -> the async (TMA) proxy
   __syncwarp();
   {
@@ -392,7 +407,7 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_p1_kernel(
     po[1] = hints ? ld_hint(nodes2 + max(aop.y, 0), pol_g) : __ldg(nodes2 + max(aop.y, 0));
     po[2] = hints ? ld_hint(nodes2 + max(aop.z, 0), pol_g) : __ldg(nodes2 + max(aop.z, 0));
   }
-  p1_row<NQV, NQE, BOUND>(P, tr, mset, stw, srhs, lane, blockIdx.x * blockDim.x + warp * 32, ee,
+  p1_row<NQV, NQE, BOUND>(P, tr, mset, stw, P.ablate & 128 ? srhs : nullptr, lane, blockIdx.x * blockDim.x + warp * 32, ee,
                           active, v, anb, aop, rp, rp_next, pv, po, false, [] {});
   if (lane == 0) bulk_wait_all();
 }
@@ -424,7 +439,7 @@ struct SmemP1Pipe {
   static constexpr int kNb = 0, kOp = 128, kV = 256, kRp = 352, kRpn = 384, kIdxInts = 416;
   static constexpr int kIdx = kIdxInts / 2;      // doubles
   static constexpr int kNode = 32 * 6 * 2;       // doubles: [6][32] double2
-  static constexpr int kWarp = kIdx + kNode + SM::kStage + SM::kRhs;
+  static constexpr int kWarp = kIdx + kNode + SM::kStage;  // RHS stored directly
   static constexpr size_t kBytes = sizeof(double) * (size_t(SM::kTr) + size_t(WARPS) * kWarp);
 };
 
@@ -454,7 +469,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) assemble_p1_pipe_kernel(
   int* idx = reinterpret_cast<int*>(wbase);                     // one chunk's records
   double2* nod = reinterpret_cast<double2*>(wbase + PS::kIdx);  // one chunk's nodes [6][32]
   double* stw = wbase + PS::kIdx + PS::kNode;
-  double* srhs = stw + SM::kStage;
+  double* srhs = nullptr;  // RHS stored directly (shared memory for 16 warps)
 
   const int n_rows = P.row_end - P.row_begin;
   const int n_chunks = (n_rows + 31) >> 5;
@@ -503,7 +518,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) assemble_p1_pipe_kernel(
     const bool active = e < P.row_end;
     const int ee = active ? e : P.row_end - 1;
     p1_row<NQV, NQE, true>(P, tr, mset, stw, srhs, lane, e_first, ee, active, v, anb, aop, rp,
-                           rp_next, pv, po, j > 0, [&] {
+                           rp_next, pv, po, true, [&] {
                              if (more) {
                                cp_async_wait_all();  // chunk j + 1's records
                                issue_nodes();
