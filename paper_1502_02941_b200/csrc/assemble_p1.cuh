@@ -133,17 +133,17 @@ __device__ __forceinline__ void p1_row(const Params2<3, NQV, NQE, false, true>& 
 #pragma unroll
   for (int i = 0; i < NL; ++i) F[i] = 0.0;
   {
-    const dgb_scalar_field& fs = P.prob.source;
-#pragma unroll 1
-    for (int q = 0; q < NQV; ++q) {
-      const double px = FADD(FADD(pv[0].x, FMUL(B00, P.t.x[L::VX + q])), FMUL(B01, P.t.x[L::VY + q]));
-      const double py = FADD(FADD(pv[0].y, FMUL(B10, P.t.x[L::VX + q])), FMUL(B11, P.t.x[L::VY + q]));
-      const double f = fs.kind == DGB_FIELD_PER_ELEMENT ? __ldg(fs.per_element + ee)
-                       : (P.ablate & 2) ? px : scalar_point_inline(fs, px, py);
-      const double c = (det * P.t.x[L::VW + q]) * f;
+    source_points<NQV, false>(
+        P.prob.source, ee, P.ablate & 2,
+        [&](int q, double& px, double& py) {
+          px = FADD(FADD(pv[0].x, FMUL(B00, P.t.x[L::VX + q])), FMUL(B01, P.t.x[L::VY + q]));
+          py = FADD(FADD(pv[0].y, FMUL(B10, P.t.x[L::VX + q])), FMUL(B11, P.t.x[L::VY + q]));
+        },
+        [&](int q, double f, double, double) {
+          const double c = (det * P.t.x[L::VW + q]) * f;
 #pragma unroll
-      for (int i = 0; i < NL; ++i) F[i] = fma(c, P.t.x[L::PHI + q * NL + i], F[i]);
-    }
+          for (int i = 0; i < NL; ++i) F[i] = fma(c, P.t.x[L::PHI + q * NL + i], F[i]);
+        });
   }
 
   // diagonal block: volume terms (registers)

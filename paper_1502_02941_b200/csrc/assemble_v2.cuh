@@ -560,29 +560,29 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
 #pragma unroll
   for (int i = 0; i < NL; ++i) F[i] = 0.0;
   {
-    const dgb_scalar_field& fs = P.prob.source;
-#pragma unroll 1
-    for (int q = 0; q < NQV; ++q) {
-      const double px = FADD(FADD(pv[0].x, FMUL(B00, P.t.x[L::VX + q])), FMUL(B01, P.t.x[L::VY + q]));
-      const double py = FADD(FADD(pv[0].y, FMUL(B10, P.t.x[L::VX + q])), FMUL(B11, P.t.x[L::VY + q]));
-      const double f = fs.kind == DGB_FIELD_PER_ELEMENT ? __ldg(fs.per_element + ee)
-                       : (P.ablate & 2) ? px : scalar_point_inline(fs, px, py);
-      const double dw = det * P.t.x[L::VW + q];
-      const double c = dw * f;
+    source_points<NQV, TRIG>(
+        P.prob.source, ee, P.ablate & 2,
+        [&](int q, double& px, double& py) {
+          px = FADD(FADD(pv[0].x, FMUL(B00, P.t.x[L::VX + q])), FMUL(B01, P.t.x[L::VY + q]));
+          py = FADD(FADD(pv[0].y, FMUL(B10, P.t.x[L::VX + q])), FMUL(B11, P.t.x[L::VY + q]));
+        },
+        [&](int q, double f, double px, double py) {
+          const double dw = det * P.t.x[L::VW + q];
+          const double c = dw * f;
 #pragma unroll
-      for (int i = 0; i < NL; ++i) F[i] = fma(c, P.t.x[L::PHI + q * NL + i], F[i]);
-      if constexpr (TRIG) {
-        double bx, by;
-        velocity_k<BK>(bf, px, py, bx, by);
-        if constexpr (SM::kMma) {  // T-form: the transport coefficients are A-operand rows
-          sk[(4 + 2 * q) * SM::kCT + lane] = dw * (G00 * bx + G10 * by);
-          sk[(4 + 2 * q + 1) * SM::kCT + lane] = dw * (G01 * bx + G11 * by);
-        } else {
-          sq[(2 * q) * 32 + lane] = dw * (G00 * bx + G10 * by);
-          sq[(2 * q + 1) * 32 + lane] = dw * (G01 * bx + G11 * by);
-        }
-      }
-    }
+          for (int i = 0; i < NL; ++i) F[i] = fma(c, P.t.x[L::PHI + q * NL + i], F[i]);
+          if constexpr (TRIG) {
+            double bx, by;
+            velocity_k<BK>(bf, px, py, bx, by);
+            if constexpr (SM::kMma) {  // T-form: the transport coefficients are A-operand rows
+              sk[(4 + 2 * q) * SM::kCT + lane] = dw * (G00 * bx + G10 * by);
+              sk[(4 + 2 * q + 1) * SM::kCT + lane] = dw * (G01 * bx + G11 * by);
+            } else {
+              sq[(2 * q) * 32 + lane] = dw * (G00 * bx + G10 * by);
+              sq[(2 * q + 1) * 32 + lane] = dw * (G01 * bx + G11 * by);
+            }
+          }
+        });
   }
 
   // ---- phase A2: per local edge -> stashed coefficient record, boundary RHS --------------------

@@ -101,6 +101,33 @@ struct KParams {
 // device helpers (FMUL / FADD / FSUB / FDIV and hypot_dd: device_math.cuh)
 // ------------------------------------------------------------------------------------------
 
+// The two transcendental families, out of family() so the hoisted-dispatch source loop
+// (source_points) runs them with the same expressions.
+__device__ __forceinline__ void family_tanh(const double* p, double x, double y, double& u,
+                                            double& ux, double& uy, double& lap) {
+  // Same expressions as the reference's BoundaryLayer (problems.cpp:81-98): far from the
+  // layer F is dominated by the rounding of u = (1 - tanh s) / 2, so parity needs tanh.
+  const double s = (p[0] * x + p[1] * y + p[2]) / p[3];
+  const double t = tanh(s);
+  const double c = cosh(s);
+  const double sech2 = 1.0 / (c * c);
+  const double gx = p[0] / p[3], gy = p[1] / p[3];
+  u = 0.5 * (1.0 - t);
+  ux = -0.5 * sech2 * gx;
+  uy = -0.5 * sech2 * gy;
+  lap = t * sech2 * (gx * gx + gy * gy);
+}
+__device__ __forceinline__ void family_gauss(const double* p, double x, double y, double& u,
+                                             double& ux, double& uy, double& lap) {
+  const double dx = x - p[1], dy = y - p[2];
+  const double r2 = dx * dx + dy * dy;
+  const double v = exp_fast(-p[0] * r2);
+  u = v;
+  ux = -2.0 * p[0] * dx * v;
+  uy = -2.0 * p[0] * dy * v;
+  lap = (4.0 * p[0] * p[0] * r2 - 4.0 * p[0]) * v;
+}
+
 __device__ __forceinline__ void family(int fn, const double* p, double x, double y, double& u,
                                        double& ux, double& uy, double& lap) {
   constexpr double pi = 3.14159265358979323846;
@@ -115,30 +142,12 @@ __device__ __forceinline__ void family(int fn, const double* p, double x, double
       lap = -2.0 * pi * pi * u;
       return;
     }
-    case DGB_FN_TANH_LAYER: {
-      // Same expressions as the reference's BoundaryLayer (problems.cpp:81-98): far from the
-      // layer F is dominated by the rounding of u = (1 - tanh s) / 2, so parity needs tanh.
-      const double s = (p[0] * x + p[1] * y + p[2]) / p[3];
-      const double t = tanh(s);
-      const double c = cosh(s);
-      const double sech2 = 1.0 / (c * c);
-      const double gx = p[0] / p[3], gy = p[1] / p[3];
-      u = 0.5 * (1.0 - t);
-      ux = -0.5 * sech2 * gx;
-      uy = -0.5 * sech2 * gy;
-      lap = t * sech2 * (gx * gx + gy * gy);
+    case DGB_FN_TANH_LAYER:
+      family_tanh(p, x, y, u, ux, uy, lap);
       return;
-    }
-    case DGB_FN_GAUSSIAN: {
-      const double dx = x - p[1], dy = y - p[2];
-      const double r2 = dx * dx + dy * dy;
-      const double v = exp_fast(-p[0] * r2);
-      u = v;
-      ux = -2.0 * p[0] * dx * v;
-      uy = -2.0 * p[0] * dy * v;
-      lap = (4.0 * p[0] * p[0] * r2 - 4.0 * p[0]) * v;
+    case DGB_FN_GAUSSIAN:
+      family_gauss(p, x, y, u, ux, uy, lap);
       return;
-    }
     case DGB_FN_AFFINE:
       u = p[0] + p[1] * x + p[2] * y;
       ux = p[1];
@@ -185,6 +194,53 @@ __device__ __forceinline__ double scalar_point_inline(const dgb_scalar_field& f,
     case DGB_MODE_SOURCE: return f.q[0] * u - f.q[1] * lap + f.q[2] * ux + f.q[3] * uy;
     case DGB_MODE_FLUX_X: return f.q[1] * ux;
     default: return nan("");
+  }
+}
+
+// The source at every volume point of an element, with the coefficient dispatch hoisted out
+// of the point loop: one loop per common (family, SOURCE) pair, the generic loop otherwise.
+// xy(q, x, y) gives point q, use(q, f, x, y) consumes its value; same expressions as
+// scalar_point_inline.  UseXY: the caller needs the points even for constant sources.  skip
+// (profiling ablation): f = x.
+template <int NQV, bool UseXY, class XY, class USE>
+__device__ __forceinline__ void source_points(const dgb_scalar_field& fs, int e, bool skip, XY xy,
+                                              USE use) {
+  if (fs.kind == DGB_FIELD_PER_ELEMENT || fs.kind == DGB_FIELD_CONSTANT) {
+    const double f = fs.kind == DGB_FIELD_PER_ELEMENT ? __ldg(fs.per_element + e) : fs.value;
+#pragma unroll 1
+    for (int q = 0; q < NQV; ++q) {
+      double x = 0.0, y = 0.0;
+      if (UseXY) xy(q, x, y);
+      use(q, f, x, y);
+    }
+    return;
+  }
+  if (!skip && fs.mode == DGB_MODE_SOURCE && (fs.fn == DGB_FN_GAUSSIAN || fs.fn == DGB_FN_TANH_LAYER)) {
+    const double q0 = fs.q[0], q1 = fs.q[1], q2 = fs.q[2], q3 = fs.q[3];
+    if (fs.fn == DGB_FN_GAUSSIAN) {
+#pragma unroll 1
+      for (int q = 0; q < NQV; ++q) {
+        double x, y, u, ux, uy, lap;
+        xy(q, x, y);
+        family_gauss(fs.p, x, y, u, ux, uy, lap);
+        use(q, q0 * u - q1 * lap + q2 * ux + q3 * uy, x, y);
+      }
+    } else {
+#pragma unroll 1
+      for (int q = 0; q < NQV; ++q) {
+        double x, y, u, ux, uy, lap;
+        xy(q, x, y);
+        family_tanh(fs.p, x, y, u, ux, uy, lap);
+        use(q, q0 * u - q1 * lap + q2 * ux + q3 * uy, x, y);
+      }
+    }
+    return;
+  }
+#pragma unroll 1
+  for (int q = 0; q < NQV; ++q) {
+    double x, y;
+    xy(q, x, y);
+    use(q, skip ? x : scalar_point_inline(fs, x, y), x, y);
   }
 }
 
