@@ -24,14 +24,31 @@ struct SmemP1 {
 };
 
 // Per-CTA trace table tr[l][p][c][j]: phi, w d0 phi, w d1 phi of local edge l's points.
-template <int NQV, int NQE>
+// ROTATED (bound mesh): the gradient pair of edge lf is expressed in the neighbour's vertex
+// order rotated to start at its vertex opposite the shared edge, (q_lf, q_lf+1, q_lf+2), so the
+// block-row kernel builds the neighbour's geometry from (opposite, b, a) without selecting on
+// lf.  With x = q_0 + xi e1 + eta e2, the rotated reference coordinates satisfy
+// grad' phi = M_lf grad phi, M_0 = I, M_1 = [[-1, 1], [-1, 0]], M_2 = [[0, -1], [1, -1]], and
+// G_f^T n . g = G'^T n . (M_lf g): the neighbour terms are unchanged.
+template <int NQV, int NQE, bool ROTATED = false>
 __device__ __forceinline__ void p1_tables(const Params2<3, NQV, NQE, false, true>& P, double* tr) {
   constexpr int NL = 3;
   using L = Lay<NL, NQV, NQE, false, true>;
   for (int i = threadIdx.x; i < 3 * NQE * 3 * NL; i += blockDim.x) {
     const int j = i % NL, c = (i / NL) % 3, p = (i / (3 * NL)) % NQE, l = i / (3 * NL * NQE);
-    tr[i] = c == 0 ? P.t.x[L::EPHI + (l * NQE + p) * NL + j]
-                   : P.t.x[L::EDW + ((l * NQE + p) * 2 + c - 1) * NL + j];
+    const double g0 = P.t.x[L::EDW + ((l * NQE + p) * 2) * NL + j];
+    const double g1 = P.t.x[L::EDW + ((l * NQE + p) * 2 + 1) * NL + j];
+    double v;
+    if (c == 0) {
+      v = P.t.x[L::EPHI + (l * NQE + p) * NL + j];
+    } else if (!ROTATED || l == 0) {
+      v = c == 1 ? g0 : g1;
+    } else if (l == 1) {
+      v = c == 1 ? g1 - g0 : -g0;
+    } else {
+      v = c == 1 ? -g1 : g0 - g1;
+    }
+    tr[i] = v;
   }
 }
 
@@ -188,13 +205,9 @@ __device__ __forceinline__ void p1_row(const Params2<3, NQV, NQE, false, true>& 
     if (kind == DGB_EDGE_INTERIOR) {
       Geo gf;
       if constexpr (bound) {
-        const double2 qo = po[l];
-        const double2 qa = pv[(l + 1) % 3];
-        const double2 qb = pv[(l + 2) % 3];
-        const double2 q0 = lf == 0 ? qo : (lf == 1 ? qa : qb);
-        const double2 q1 = lf == 1 ? qo : (lf == 2 ? qa : qb);
-        const double2 q2 = lf == 2 ? qo : (lf == 0 ? qa : qb);
-        gf = element_geo_coords(q0, q1, q2);
+        // the neighbour in its vertex order rotated to (opposite, b, a): the trace table's
+        // gradients are rotated to match (p1_tables<.., true>)
+        gf = element_geo_coords(po[l], pv[(l + 2) % 3], pv[(l + 1) % 3]);
       } else {
         gf = element_geo_fast(P.nodes, vfv[l]);
       }
@@ -364,7 +377,7 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_p1_kernel(
   using SM = SmemP1<NQV, NQE>;
   extern __shared__ double smem[];
   double* tr = smem;
-  p1_tables<NQV, NQE>(P, tr);
+  p1_tables<NQV, NQE, BOUND>(P, tr);
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int mset = blockIdx.y;
@@ -461,7 +474,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) assemble_p1_pipe_kernel(
   using PS = SmemP1Pipe<NQV, NQE, WARPS>;
   extern __shared__ double smem[];
   double* tr = smem;
-  p1_tables<NQV, NQE>(P, tr);
+  p1_tables<NQV, NQE, true>(P, tr);
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int mset = blockIdx.y;
