@@ -470,11 +470,16 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
   using SM = Smem<NL, NQV, NQE, BK>;
   constexpr int SS = SM::SS, NF = SM::NF;
   extern __shared__ double smem[];
-  double* tr = smem;  // [3][NQE][3][NL]: phi, d0 phi, d1 phi of each local edge's points
+  double* tr = smem;  // [3][NQE][3][NL]: phi, w d0 phi, w d1 phi of each local edge's points
   for (int i = threadIdx.x; i < 3 * NQE * 3 * NL; i += blockDim.x) {
     const int j = i % NL, c = (i / NL) % 3, p = (i / (3 * NL)) % NQE, l = i / (3 * NL * NQE);
+    // gradients rotated to the neighbour's (opposite, b, a) vertex order (p1_tables)
+    const double g0 = P.t.x[L::EDW + ((l * NQE + p) * 2) * NL + j];
+    const double g1 = P.t.x[L::EDW + ((l * NQE + p) * 2 + 1) * NL + j];
     tr[i] = c == 0 ? P.t.x[L::EPHI + (l * NQE + p) * NL + j]
-                   : P.t.x[L::EDW + ((l * NQE + p) * 2 + c - 1) * NL + j];  // w_p d phi
+            : l == 0 ? (c == 1 ? g0 : g1)
+            : l == 1 ? (c == 1 ? g1 - g0 : -g0)
+                     : (c == 1 ? -g1 : g0 - g1);
   }
   __syncthreads();
   if (P.ablate & 16) return;
@@ -627,12 +632,10 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
         const double2 qo = l == 0 ? po[0] : (l == 1 ? po[1] : po[2]);
         const double2 qa = l == 0 ? pv[1] : (l == 1 ? pv[2] : pv[0]);
         const double2 qb = l == 0 ? pv[2] : (l == 1 ? pv[0] : pv[1]);
-        const double2 q0 = lf == 0 ? qo : (lf == 1 ? qa : qb);
-        const double2 q1 = lf == 1 ? qo : (lf == 2 ? qa : qb);
-        const double2 q2 = lf == 2 ? qo : (lf == 0 ? qa : qb);
-        gf = element_geo_coords(q0, q1, q2);
+        gf = element_geo_coords(qo, qb, qa);  // rotated order (opposite, b, a): see tr
       } else {
-        gf = element_geo_fast(P.nodes, vf);
+        const int vr[3] = {lf == 0 ? vf[0] : (lf == 1 ? vf[1] : vf[2]), b, a};
+        gf = element_geo_fast(P.nodes, vr);
       }
       double eps_e = eps;
       if (P.prob.diffusion.kind == DGB_FIELD_PER_ELEMENT) {

@@ -127,10 +127,7 @@ __device__ __forceinline__ void ws_produce(const Params2<NL, NQV, NQE, false, fu
       const double2 qo = l == 0 ? po[0] : (l == 1 ? po[1] : po[2]);
       const double2 qa = l == 0 ? pv[1] : (l == 1 ? pv[2] : pv[0]);
       const double2 qb = l == 0 ? pv[2] : (l == 1 ? pv[0] : pv[1]);
-      const double2 q0 = lf == 0 ? qo : (lf == 1 ? qa : qb);
-      const double2 q1 = lf == 1 ? qo : (lf == 2 ? qa : qb);
-      const double2 q2 = lf == 2 ? qo : (lf == 0 ? qa : qb);
-      const Geo gf = element_geo_coords(q0, q1, q2);
+      const Geo gf = element_geo_coords(qo, qb, qa);  // rotated order (opposite, b, a)
       double eps_e = eps;
       if (P.prob.diffusion.kind == DGB_FIELD_PER_ELEMENT) {
         const double ef = __ldg(P.prob.diffusion.per_element + f);

@@ -1143,6 +1143,14 @@ void launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_prob
     dgb_plan* mp = const_cast<dgb_plan*>(plan);
     auto ephi = [&](int l, int p, int i) { return x[L::EPHI + (l * NQE + p) * NL + i]; };
     auto edw = [&](int l, int p, int a, int i) { return x[L::EDW + ((l * NQE + p) * 2 + a) * NL + i]; };
+    // the neighbour's gradients in its vertex order rotated to (opposite, b, a), the order
+    // the kernels build its geometry in (assemble_p1.cuh p1_tables: grad' = M_lf grad)
+    auto edw_rot = [&](int lf, int p, int a, int i) {
+      const double g0 = edw(lf, p, 0, i), g1 = edw(lf, p, 1, i);
+      if (lf == 0) return a == 0 ? g0 : g1;
+      if (lf == 1) return a == 0 ? g1 - g0 : -g0;
+      return a == 0 ? -g1 : g0 - g1;
+    };
     // neighbour term of (l, lf) at entry (bi, bj): 0 X, 1 Y0, 2 Y1, 3 Z0, 4 Z1 (Z unscaled)
     auto neigh = [&](int term, int l, int lf, int bi, int bj) {
       double acc = 0.0;
@@ -1150,8 +1158,8 @@ void launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_prob
         const int q = NQE - 1 - p;
         switch (term) {
           case 0: acc += x[L::EW + p] * ephi(l, p, bi) * ephi(lf, q, bj); break;
-          case 1: acc += ephi(l, p, bi) * edw(lf, q, 0, bj); break;
-          case 2: acc += ephi(l, p, bi) * edw(lf, q, 1, bj); break;
+          case 1: acc += ephi(l, p, bi) * edw_rot(lf, q, 0, bj); break;
+          case 2: acc += ephi(l, p, bi) * edw_rot(lf, q, 1, bj); break;
           case 3: acc += edw(l, p, 0, bi) * ephi(lf, q, bj); break;
           default: acc += edw(l, p, 1, bi) * ephi(lf, q, bj); break;
         }
