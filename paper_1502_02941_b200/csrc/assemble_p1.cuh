@@ -349,7 +349,14 @@ __device__ __forceinline__ void p1_row(const Params2<3, NQV, NQE, false, true>& 
     double* dst = o_val + static_cast<long long>(rp_first) * N2;
     const int head = rp_first & 1;
     const unsigned long long pol = output_policy(P.evict_first);
-    for (int i = head + 2 * lane; i + 1 < n; i += 64) store_pair(dst + i, srow[i], srow[i + 1], pol);
+    // srow + head is 16-byte aligned (srow has val's 16-byte phase): pairs load as one LDS.128
+    const double2* s2 = reinterpret_cast<const double2*>(srow + head);
+    const int npair = (n - head) >> 1;
+#pragma unroll 2
+    for (int k = lane; k < npair; k += 32) {
+      const double2 w = s2[k];
+      store_pair(dst + head + 2 * k, w.x, w.y, pol);
+    }
     if (lane == 1 && head && n > 0) dst[0] = srow[0];
     if (lane == 2 && n > 0 && ((n - head) & 1)) dst[n - 1] = srow[n - 1];
     __syncwarp();
