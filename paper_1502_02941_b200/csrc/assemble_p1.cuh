@@ -231,6 +231,20 @@ __device__ __forceinline__ void p1_row(const Params2<3, NQV, NQE, false, true>& 
       // K_ef = sum_p phi^l_p (x) b1_p + a2_p (x) phi^lf_(n-1-p)
       if (!(P.ablate & 4)) {  // (profiling ablation: skip the neighbour block)
       const double* trm = tr + lf * (NQE * 3 * NL);
+      // P1: the reference gradients are constant, so the neighbour's w d phi at its points are
+      // the same for every edge: read them from the constant bank (edge 0) with the
+      // coefficients rotated back to the neighbour's own vertex order, uY = M_lf^T cY
+      // (p1_tables), instead of loading the rotated gradients per lf
+      double uY0 = cY0, uY1 = cY1;
+      if constexpr (bound) {
+        if (lf == 1) {
+          uY0 = -cY0 - cY1;
+          uY1 = cY0;
+        } else if (lf == 2) {
+          uY0 = cY1;
+          uY1 = -cY0 - cY1;
+        }
+      }
       double pm[NQE][NL], b1[NQE][NL];
 #pragma unroll
       for (int p = 0; p < NQE; ++p) {
@@ -238,9 +252,11 @@ __device__ __forceinline__ void p1_row(const Params2<3, NQV, NQE, false, true>& 
         const double* row = trm + (NQE - 1 - p) * 3 * NL;
 #pragma unroll
         for (int j = 0; j < NL; ++j) {
-          const double fr = row[j], g0 = row[NL + j], g1 = row[2 * NL + j];
+          const double fr = row[j];
+          const double g0 = P.t.x[L::EDW + ((NQE - 1 - p) * 2) * NL + j];
+          const double g1 = P.t.x[L::EDW + ((NQE - 1 - p) * 2 + 1) * NL + j];
           pm[p][j] = fr;
-          b1[p][j] = fma(cV, fr, fma(cY0, g0, cY1 * g1));
+          b1[p][j] = fma(cV, fr, fma(uY0, g0, uY1 * g1));
         }
       }
       double* blk = myrow + slot_of[1 + l] * N2;
