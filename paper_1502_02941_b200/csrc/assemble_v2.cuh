@@ -568,8 +568,9 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
     source_points<NQV, TRIG>(
         P.prob.source, ee, P.ablate & 2,
         [&](int q, double& px, double& py) {
-          px = FADD(FADD(pv[0].x, FMUL(B00, P.t.x[L::VX + q])), FMUL(B01, P.t.x[L::VY + q]));
-          py = FADD(FADD(pv[0].y, FMUL(B10, P.t.x[L::VX + q])), FMUL(B11, P.t.x[L::VY + q]));
+          // volume points only evaluate coefficients (no term selection): fused
+          px = fma(B01, P.t.x[L::VY + q], fma(B00, P.t.x[L::VX + q], pv[0].x));
+          py = fma(B11, P.t.x[L::VY + q], fma(B10, P.t.x[L::VX + q], pv[0].y));
         },
         [&](int q, double f, double px, double py) {
           const double dw = det * P.t.x[L::VW + q];

@@ -95,8 +95,9 @@ __device__ __forceinline__ void ws_produce(const Params2<NL, NQV, NQE, false, fu
     source_points<NQV, false>(
         P.prob.source, ee, P.ablate & 2,
         [&](int q, double& px, double& py) {
-          px = FADD(FADD(pv[0].x, FMUL(B00, P.t.x[L::VX + q])), FMUL(B01, P.t.x[L::VY + q]));
-          py = FADD(FADD(pv[0].y, FMUL(B10, P.t.x[L::VX + q])), FMUL(B11, P.t.x[L::VY + q]));
+          // volume points only evaluate coefficients (no term selection): fused
+          px = fma(B01, P.t.x[L::VY + q], fma(B00, P.t.x[L::VX + q], pv[0].x));
+          py = fma(B11, P.t.x[L::VY + q], fma(B10, P.t.x[L::VX + q], pv[0].y));
         },
         [&](int q, double f, double, double) {
           const double c = det * P.t.x[L::VW + q] * f;
