@@ -305,7 +305,11 @@ enum dgb_plan_option {
                                 bit 1: evict-first L2 hint on the output stream;
                                 bit 2: L2 hints on the P1 kernel's loads (node gathers
                                 evict-last, per-element records evict-first);
-                                -1 (default): evict-first for odd block sizes only */
+                                -1 (default): evict-first for odd block sizes only; the
+                                P1 persistent kernel on a bound mesh instead keeps its node
+                                gathers evict-last in a persisting carve-out of at most 56 MiB
+                                (a process-wide device limit set at bind time, released when
+                                the plan is destroyed) */
   DGB_OPTION_BATCH_FUSE = 4, /* dgb_assemble_batch on the tensor-core kernels (default 1): sets
                                 with equal penalties share the per-element work and each CTA
                                 writes every set; 0 = one CTA row per set (grid.y = n) */

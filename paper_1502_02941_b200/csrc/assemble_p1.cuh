@@ -483,6 +483,9 @@ struct SmemP1Pipe {
 __device__ __forceinline__ void cp_async16(void* sm, const void* g) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" :: "r"(smem_addr(sm)), "l"(g) : "memory");
 }
+__device__ __forceinline__ void cp_async16_hint(void* sm, const void* g, unsigned long long pol) {
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" :: "r"(smem_addr(sm)), "l"(g), "l"(pol) : "memory");
+}
 __device__ __forceinline__ void cp_async4(void* sm, const void* g) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" :: "r"(smem_addr(sm)), "l"(g) : "memory");
 }
@@ -525,11 +528,21 @@ __global__ void __launch_bounds__(WARPS * 32, 1) assemble_p1_pipe_kernel(
     cp_async4(idx + PS::kRpn + lane, P.row_ptr_src + r + 1);
     cp_async_commit();
   };
+  const bool hints = P.load_hints;
+  const unsigned long long pol_g = evict_last_policy();
   auto issue_nodes = [&]() {  // from the landed records
+    if (hints) {  // L2 policy bit 2: node gathers evict-last (they are gathered again)
 #pragma unroll
-    for (int k = 0; k < 3; ++k) cp_async16(nod + k * 32 + lane, nodes2 + idx[PS::kV + 3 * lane + k]);
+      for (int k = 0; k < 3; ++k) cp_async16_hint(nod + k * 32 + lane, nodes2 + idx[PS::kV + 3 * lane + k], pol_g);
 #pragma unroll
-    for (int k = 0; k < 3; ++k) cp_async16(nod + (3 + k) * 32 + lane, nodes2 + max(idx[PS::kOp + 4 * lane + k], 0));
+      for (int k = 0; k < 3; ++k)
+        cp_async16_hint(nod + (3 + k) * 32 + lane, nodes2 + max(idx[PS::kOp + 4 * lane + k], 0), pol_g);
+    } else {
+#pragma unroll
+      for (int k = 0; k < 3; ++k) cp_async16(nod + k * 32 + lane, nodes2 + idx[PS::kV + 3 * lane + k]);
+#pragma unroll
+      for (int k = 0; k < 3; ++k) cp_async16(nod + (3 + k) * 32 + lane, nodes2 + max(idx[PS::kOp + 4 * lane + k], 0));
+    }
     cp_async_commit();
   };
 

@@ -923,6 +923,9 @@ int tile_for(int nl) { return nl <= 6 ? 64 : 32; }
 // ------------------------------------------------------------------------------------------
 // plan + C-ABI
 // ------------------------------------------------------------------------------------------
+// the persisting-L2 carve-out (process-wide device limit) was set by a plan of this library
+static bool g_carve_out_is_ours = false;
+
 struct dgb_plan {
   int device = 0;
   int degree = 0, nl = 0, nqv = 0, nqe = 0;
@@ -1083,6 +1086,10 @@ void launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_prob
   P.evict_first = plan->l2_policy < 0 ? (N2 % 2 == 1) : (plan->l2_policy & 2) != 0;
   P.ablate = plan->ablate;
   P.load_hints = plan->l2_policy > 0 && (plan->l2_policy & 4) != 0;
+  if (NL == 3 && plan->l2_policy < 0 && plan->p1_pipe > 0 && plan->l2_persist_bytes > 0 && row_ptr_src) {
+    P.load_hints = 1;  // the P1 persistent kernel's auto policy (bind time): hints, normal output
+    P.evict_first = 0;
+  }
   P.prob = *problem;
   const double* h = plan->h_tens.data();
   const dgb::Layout& V = plan->L;
@@ -1641,18 +1648,23 @@ int dgb_plan_bind_mesh(dgb_plan* plan, const dgb_mesh_arrays* mesh, int32_t row_
     {
       // L2 policy: permuted (gather-heavy) meshes keep their nodes persisting in L2; the
       // carve-out is sized to the node array, never more (it is taken from the write stream).
-      static bool carve_out_is_ours = false;
+      // auto (-1) for the P1 persistent kernel: node gathers evict-last in a carve-out of at
+      // most 56 MiB (a carve-out of the whole 67 MB node array at config 4 costs 50%; 48-56
+      // MiB halves the DRAM reads and gains 3%, profiles/NOTES.md)
       const size_t node_bytes = sizeof(double) * 2 * static_cast<size_t>(mesh->n_nodes);
-      size_t want = (plan->l2_policy > 0 && (plan->l2_policy & 5)) ? std::min(node_bytes, plan->l2_persist_max) : 0;
+      const bool p1_auto = plan->l2_policy < 0 && plan->nl == 3 && plan->p1_pipe > 0;
+      size_t want = (plan->l2_policy > 0 && (plan->l2_policy & 5)) || p1_auto
+                        ? std::min(node_bytes, plan->l2_persist_max) : 0;
+      if (p1_auto) want = std::min(want, size_t(56) << 20);
       if (want > 0 && plan->l2_carve_mb > 0) want = std::min(want, size_t(plan->l2_carve_mb) << 20);
       plan->l2_persist_bytes = 0;
-      if (want == 0 && carve_out_is_ours) {
+      if (want == 0 && g_carve_out_is_ours) {
         cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);
-        carve_out_is_ours = false;
+        g_carve_out_is_ours = false;
         cudaGetLastError();
       }
       if (want > 0) {
-        carve_out_is_ours = true;
+        g_carve_out_is_ours = true;
         size_t cur = 0;
         cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
         if (cur != want) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
@@ -1746,6 +1758,11 @@ void dgb_plan_destroy(dgb_plan* p) {
   int prev = -1;
   cudaGetDevice(&prev);
   cudaSetDevice(p->device);
+  if (p->l2_persist_bytes > 0 && g_carve_out_is_ours) {  // the carve-out this plan set up
+    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);
+    g_carve_out_is_ours = false;
+    cudaGetLastError();
+  }
   cudaFree(p->d_tens);
   cudaFree(p->d_err);
   cudaFree(p->d_scan);
