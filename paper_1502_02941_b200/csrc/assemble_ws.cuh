@@ -115,8 +115,9 @@ __device__ __forceinline__ void ws_produce(const Params2<NL, NQV, NQE, false, fu
     const double2 A = o == 0 ? pv[(l + 1) % 3] : pv[(l + 2) % 3];
     const double2 Bn = o == 0 ? pv[(l + 2) % 3] : pv[(l + 1) % 3];
     const double dx = FSUB(Bn.x, A.x), dy = FSUB(Bn.y, A.y);
-    const double h = hypot_fast(dx, dy);  // edge_geometry (mesh.cpp:232-257)
-    const double rh = rcp_nr(h);
+    // edge_geometry (mesh.cpp:232-257): length and its reciprocal from one rsqrt
+    const double rh = rsqrt_nr(fma(dx, dx, dy * dy));
+    const double h = fma(dx, dx, dy * dy) * rh;
     const double tx = dx * rh, ty = dy * rh;
     const double nx = o == 0 ? ty : -ty, ny = o == 0 ? -tx : tx;
     const double ge0 = G00 * nx + G10 * ny, ge1 = G01 * nx + G11 * ny;
