@@ -103,19 +103,25 @@ struct KParams {
 
 // The two transcendental families, out of family() so the hoisted-dispatch source loop
 // (source_points) runs them with the same expressions.
-__device__ __forceinline__ void family_tanh(const double* p, double x, double y, double& u,
-                                            double& ux, double& uy, double& lap) {
+// gx = p0 / p3, gy = p1 / p3 are point-independent: source_points computes them once per
+// element (the same divisions, so the same bits).
+__device__ __forceinline__ void family_tanh_g(const double* p, double gx, double gy, double x,
+                                              double y, double& u, double& ux, double& uy,
+                                              double& lap) {
   // Same expressions as the reference's BoundaryLayer (problems.cpp:81-98): far from the
   // layer F is dominated by the rounding of u = (1 - tanh s) / 2, so parity needs tanh.
   const double s = (p[0] * x + p[1] * y + p[2]) / p[3];
   const double t = tanh(s);
   const double c = cosh(s);
   const double sech2 = 1.0 / (c * c);
-  const double gx = p[0] / p[3], gy = p[1] / p[3];
   u = 0.5 * (1.0 - t);
   ux = -0.5 * sech2 * gx;
   uy = -0.5 * sech2 * gy;
   lap = t * sech2 * (gx * gx + gy * gy);
+}
+__device__ __forceinline__ void family_tanh(const double* p, double x, double y, double& u,
+                                            double& ux, double& uy, double& lap) {
+  family_tanh_g(p, p[0] / p[3], p[1] / p[3], x, y, u, ux, uy, lap);
 }
 __device__ __forceinline__ void family_gauss(const double* p, double x, double y, double& u,
                                              double& ux, double& uy, double& lap) {
@@ -226,11 +232,12 @@ __device__ __forceinline__ void source_points(const dgb_scalar_field& fs, int e,
         use(q, q0 * u - q1 * lap + q2 * ux + q3 * uy, x, y);
       }
     } else {
+      const double gx = fs.p[0] / fs.p[3], gy = fs.p[1] / fs.p[3];
 #pragma unroll 1
       for (int q = 0; q < NQV; ++q) {
         double x, y, u, ux, uy, lap;
         xy(q, x, y);
-        family_tanh(fs.p, x, y, u, ux, uy, lap);
+        family_tanh_g(fs.p, gx, gy, x, y, u, ux, uy, lap);
         use(q, q0 * u - q1 * lap + q2 * ux + q3 * uy, x, y);
       }
     }
