@@ -67,7 +67,7 @@ def parse_args():
     ap.add_argument("--ws", type=int, default=-1,
                     help="warp-specialised kernel: 0 off, 1 default, 4..12 producer warps of 16")
     ap.add_argument("--p1-pipe", type=int, default=-1,
-                    help="P1 pipelined persistent kernel: 0 off (one-shot kernel), 1 default (12 warps), 16")
+                    help="P1 pipelined persistent kernel: 0 off (one-shot kernel), 1 on (default)")
     ap.add_argument("--l2-carve-mb", type=int, default=0,
                     help="cap on the persisting-L2 carve-out of L2 policy bits 0/2 (MiB; tuning)")
     ap.add_argument("--no-bind", action="store_true",

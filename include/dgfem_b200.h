@@ -318,8 +318,8 @@ enum dgb_plan_option {
                                       monolithic kernel; 4..12 = producer warps of 16 (tuning) */
   DGB_OPTION_P1_PIPELINE = 6, /* P1 kernels on a bound mesh (default 1): persistent kernel with
                                  the record and node gathers in flight one chunk ahead
-                                 (asynchronous copies), 12 warps per SM at 168 registers;
-                                 0 = the one-shot kernel; 16 = 16 warps at 128 (tuning) */
+                                 (asynchronous copies), 12 warps per SM at 166 registers;
+                                 0 = the one-shot kernel */
   DGB_OPTION_L2_CARVEOUT_MB = 7, /* cap (MiB) on the persisting-L2 carve-out that L2 policy bits
                                     0 / 2 set up at bind time; 0 = the node array (tuning) */
   DGB_OPTION_PROFILE_ABLATE = 1000 /* DIAGNOSTICS ONLY -- RESULTS ARE WRONG while nonzero: skip

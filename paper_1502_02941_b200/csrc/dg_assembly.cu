@@ -973,7 +973,7 @@ struct dgb_plan {
   int warp_specialized = 1;     // P-form tensor-core kernel: 0 off, 1 default split, n producers
   int sm_count = 0;
   int l2_carve_mb = 0;          // persisting-L2 carve-out cap (MiB, 0: the node array) -- tuning
-  int p1_pipe = 1;              // P1 bound mesh: persistent pipelined kernel (0 off, 1 on: 12 warps, 16)
+  int p1_pipe = 1;              // P1 bound mesh: persistent pipelined kernel (0 off, 1 on)
   // DMMA B fragments of the diagonal terms, one table per kappa (W depends on kappa)
   std::vector<std::pair<double, double*>> bfrag_cache;
   int ablate = 0;  // profiling diagnostics (dgb_plan_set_option 1000)
@@ -1418,12 +1418,10 @@ void launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_prob
         cfg.dynamicSmemBytes = PS::kBytes;
         cuda_check(cudaLaunchKernelEx(&cfg, pk, P), "cudaLaunchKernelEx(p1 pipe)");
       };
-      // warps per CTA (one CTA per SM): 12 (168 registers) or 16 (128); registers are
-      // allocated per SM sub-partition, so other counts do not add registers
-      switch (plan->p1_pipe) {
-        case 16: launch(std::integral_constant<int, 16>{}); break;
-        default: launch(std::integral_constant<int, 12>{}); break;  // measured: 1.073 vs 1.103 ms
-      }
+      // 12 warps per CTA (one CTA per SM) at 166 registers.  Registers are allocated per SM
+      // sub-partition, so 13-15 warps get 128 like 16; 16 warps spilled and measured slower
+      // (1.103 vs 1.073 ms) and was removed.
+      launch(std::integral_constant<int, 12>{});
       return;
     }
   }

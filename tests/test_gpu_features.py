@@ -343,3 +343,40 @@ def test_warp_specialized_equals_monolithic(degree, batch):
             assert np.array_equal(u, v)
         for u, v in zip(x[2:], y[2:]):
             np.testing.assert_allclose(u, v, rtol=0, atol=1e-14 * np.abs(v).max())
+
+
+@pytest.mark.parametrize("rows", [None, (1, 3)])
+def test_p1_persistent_kernel_equals_one_shot(oracle, rows):
+    """The persistent software-pipelined P1 kernel (DGB_OPTION_P1_PIPELINE, default), with the
+    auto L2 policy (evict-last node gathers in a persisting carve-out) and
+    with plain evict-first output, writes what the one-shot P1 kernel writes and what the
+    unbound path writes: the pattern bitwise, K and F to rounding.  Permuted, jittered mesh
+    (a ragged last chunk), full mesh and a shard."""
+    import torch
+    cfg = problems.CONFIGS[4]
+    mesh = dgfem.unit_square_mesh(45, 0.2, problems.SEED_JITTER, True, problems.SEED_PERMUTE)
+    ref = dgfem.ReferenceElement(cfg.degree, cfg.quad_order)
+    spec = problems.config_problem(4, mesh.n_elements)
+    params = dgfem.config_parameters(cfg, capi.SIPG)
+    lo, hi = (0, mesh.n_elements) if rows is None else shard.row_range(mesh.n_elements, *rows)
+    got = {}
+    for key, pipe, l2 in (("pipe12", 1, -1), ("pipe12_ef", 1, 2),
+                          ("oneshot", 0, -1), ("unbound", 1, -1)):
+        a = shard.ShardAssembler(mesh, ref, spec, 0, lo, hi, bind=False)
+        a.plan.set_option(capi.OPTION_L2_POLICY, l2)
+        a.plan.set_option(capi.OPTION_P1_PIPELINE, pipe)
+        if key != "unbound":
+            a.plan.bind_mesh(a.dmesh, lo, hi)
+        got[key] = to_np(a.assemble(params))
+        torch.cuda.synchronize()
+    base = got["oneshot"]
+    for key, x in got.items():
+        np.testing.assert_array_equal(x[0], base[0])
+        np.testing.assert_array_equal(x[1], base[1])
+        for u, v in zip(x[2:], base[2:]):
+            np.testing.assert_allclose(u, v, rtol=0, atol=1e-13 * np.abs(v).max())
+    # and the whole thing against the oracle (full mesh)
+    if rows is None:
+        rp, col, val, rhs = oracle.assemble(mesh.arrays(), ref.tables(), spec.c, params)
+        assert np.array_equal(base[0], rp) and np.array_equal(base[1], col)
+        assert np.abs(got["pipe12"][2] - val).max() <= 1e-12 * np.abs(val).max()
