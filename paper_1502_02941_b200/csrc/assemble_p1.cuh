@@ -473,25 +473,14 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_p1_kernel(
 template <int NQV, int NQE, int WARPS>
 struct SmemP1Pipe {
   using SM = SmemP1<NQV, NQE>;
-  // one chunk's records (ints): adj_nb [32] int4, adj_op [32] int4, elements [96], rp [32], rp+1 [32]
-  static constexpr int kNb = 0, kOp = 128, kV = 256, kRp = 352, kRpn = 384, kIdxInts = 416;
-  static constexpr int kIdx = kIdxInts / 2;      // doubles
-  static constexpr int kNode = 32 * 6 * 2;       // doubles: [6][32] double2
+  static constexpr int kNb = ChunkRec::kNb, kOp = ChunkRec::kOp, kV = ChunkRec::kV,
+                       kRp = ChunkRec::kRp, kRpn = ChunkRec::kRpn, kIdxInts = ChunkRec::kIdxInts;
+  static constexpr int kIdx = ChunkRec::kIdx, kNode = ChunkRec::kNode;
   static constexpr int kWarp = kIdx + kNode + SM::kStage;  // RHS stored directly
   static constexpr size_t kBytes = sizeof(double) * (size_t(SM::kTr) + size_t(WARPS) * kWarp);
 };
 
-__device__ __forceinline__ void cp_async16(void* sm, const void* g) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" :: "r"(smem_addr(sm)), "l"(g) : "memory");
-}
-__device__ __forceinline__ void cp_async16_hint(void* sm, const void* g, unsigned long long pol) {
-  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" :: "r"(smem_addr(sm)), "l"(g), "l"(pol) : "memory");
-}
-__device__ __forceinline__ void cp_async4(void* sm, const void* g) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" :: "r"(smem_addr(sm)), "l"(g) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
 
 template <int NQV, int NQE, int WARPS>
 __global__ void __launch_bounds__(WARPS * 32, 1) assemble_p1_pipe_kernel(

@@ -148,6 +148,30 @@ __device__ __forceinline__ void bulk_store(void* g, const void* sm, unsigned byt
   }
   asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
 }
+// Per-lane asynchronous global -> shared copies (LDGSTS): the persistent kernels land the next
+// chunk's records and node coordinates in shared memory without holding registers.
+__device__ __forceinline__ void cp_async16(void* sm, const void* g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" :: "r"(smem_addr(sm)), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async16_hint(void* sm, const void* g, unsigned long long pol) {
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" :: "r"(smem_addr(sm)), "l"(g), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* sm, const void* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" :: "r"(smem_addr(sm)), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
+// One 32-element chunk's bound-mesh records and gathered node coordinates, as landed in shared
+// memory by the persistent kernels: adj_nb [32] int4, adj_op [32] int4, elements [96],
+// row_ptr [32], row_ptr + 1 [32] (ints), then the nodes [6][32] double2 (own vertices 0..2,
+// the neighbours' opposite vertices 3..5).
+struct ChunkRec {
+  static constexpr int kNb = 0, kOp = 128, kV = 256, kRp = 352, kRpn = 384, kIdxInts = 416;
+  static constexpr int kIdx = kIdxInts / 2;      // doubles
+  static constexpr int kNode = 32 * 6 * 2;       // doubles
+};
+
 __device__ __forceinline__ void bulk_wait_read() {
   asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
 }
