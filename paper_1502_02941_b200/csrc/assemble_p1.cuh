@@ -370,7 +370,7 @@ __device__ __forceinline__ void p1_row(const Params2<3, NQV, NQE, false, true>& 
     // srow + head is 16-byte aligned (srow has val's 16-byte phase): pairs load as one LDS.128
     const double2* s2 = reinterpret_cast<const double2*>(srow + head);
     const int npair = (n - head) >> 1;
-#pragma unroll 2
+#pragma unroll 4
     for (int k = lane; k < npair; k += 32) {
       const double2 w = s2[k];
       store_pair(dst + head + 2 * k, w.x, w.y, pol);
