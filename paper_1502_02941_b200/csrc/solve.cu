@@ -31,6 +31,7 @@ using dgb::cuda_check;
 constexpr int kThreads = 256;
 constexpr int kRedBlocks = 296;  // 2 per SM: partial sums of one reduction
 constexpr int kMaxRestart = 200;
+constexpr long long kGraphMaxN = 1 << 18;  // unknowns: below this a GMRES step is launch-bound
 
 // ------------------------------------------------------------------------------ kernels
 // Inverse of block row e's diagonal block (Gauss-Jordan, partial pivoting).  A zero pivot
@@ -417,9 +418,14 @@ struct Reducer {
       : s(st), partial(sizeof(double) * kRedBlocks * (kMaxRestart + 1)),
         out(sizeof(double) * (kMaxRestart + 1)), host(kMaxRestart + 1) {}
   // h[j] = V_j . w for j < k; returns a host pointer (valid until the next call)
+  // partial-sum blocks: 2 per SM, fewer for short vectors (a block per 256 rows at most)
+  static int blocks_for(long long n) {
+    return static_cast<int>(std::min<long long>(kRedBlocks, (n + kThreads - 1) / kThreads));
+  }
   const double* dots(const double* V, long long ldv, int k, const double* w, long long n) {
-    multidot_partial_kernel<<<dim3(kRedBlocks, k), kThreads, 0, s>>>(V, ldv, w, n, partial.as<double>());
-    sum_partials_kernel<<<k, kThreads, 0, s>>>(partial.as<double>(), kRedBlocks, out.as<double>());
+    const int nb = blocks_for(n);
+    multidot_partial_kernel<<<dim3(nb, k), kThreads, 0, s>>>(V, ldv, w, n, partial.as<double>());
+    sum_partials_kernel<<<k, kThreads, 0, s>>>(partial.as<double>(), nb, out.as<double>());
     cuda_check(cudaGetLastError(), "multidot");
     cuda_check(cudaMemcpyAsync(host.p, out.p, sizeof(double) * k, cudaMemcpyDeviceToHost, s), "D2H(dots)");
     cuda_check(cudaStreamSynchronize(s), "cudaStreamSynchronize(dots)");
@@ -428,15 +434,17 @@ struct Reducer {
   double dot(const double* a, const double* b, long long n) { return dots(a, 0, 1, b, n)[0]; }
   // the same, left on the device: out[j] = V_j . w (no host round trip)
   void dots_device(const double* V, long long ldv, int k, const double* w, long long n, double* out) {
-    multidot_partial_kernel<<<dim3(kRedBlocks, k), kThreads, 0, s>>>(V, ldv, w, n, partial.as<double>());
-    sum_partials_kernel<<<k, kThreads, 0, s>>>(partial.as<double>(), kRedBlocks, out);
+    const int nb = blocks_for(n);
+    multidot_partial_kernel<<<dim3(nb, k), kThreads, 0, s>>>(V, ldv, w, n, partial.as<double>());
+    sum_partials_kernel<<<k, kThreads, 0, s>>>(partial.as<double>(), nb, out);
     cuda_check(cudaGetLastError(), "multidot");
   }
   double absmax(const double* x, long long n) {
-    absmax_partial_kernel<<<kRedBlocks, kThreads, 0, s>>>(x, n, partial.as<double>());
+    const int nb = blocks_for(n);
+    absmax_partial_kernel<<<nb, kThreads, 0, s>>>(x, n, partial.as<double>());
     cuda_check(cudaGetLastError(), "absmax");
-    std::vector<double> hp(kRedBlocks);
-    cuda_check(cudaMemcpyAsync(hp.data(), partial.p, sizeof(double) * kRedBlocks, cudaMemcpyDeviceToHost, s), "D2H(absmax)");
+    std::vector<double> hp(nb);
+    cuda_check(cudaMemcpyAsync(hp.data(), partial.p, sizeof(double) * nb, cudaMemcpyDeviceToHost, s), "D2H(absmax)");
     cuda_check(cudaStreamSynchronize(s), "cudaStreamSynchronize(absmax)");
     double m = 0.0;
     for (double v : hp) m = std::max(m, v);
@@ -462,8 +470,22 @@ dgb_solve_options resolve(const dgb_solve_options* opt) {
 
 // GMRES(m), right preconditioning with block Jacobi, classical Gram-Schmidt with one
 // re-orthogonalisation (CGS2).  Returns the contract check on the true residual.
+// A library-owned blocking stream that stands in for the legacy default stream (which cannot
+// be captured into a graph).  Blocking streams are ordered with the legacy stream both ways,
+// so callers on stream 0 see the usual semantics.
+cudaStream_t solve_stream_for(cudaStream_t s) {
+  if (s != nullptr && s != cudaStreamLegacy) return s;
+  static thread_local cudaStream_t own[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return s;
+  if (!own[dev]) cuda_check(cudaStreamCreate(&own[dev]), "cudaStreamCreate(solve)");
+  return own[dev];
+}
+
 void gmres_solve(const dgb_bsr* a, const double* b, double* x, const dgb_solve_options& o,
-                 dgb_solve_info* info, cudaStream_t s) {
+                 dgb_solve_info* info, cudaStream_t s_in) {
+  const cudaStream_t s = solve_stream_for(s_in);
   const int nl = a->block_dim, E = a->n_block_rows;
   const long long n = static_cast<long long>(E) * nl;
   alloc_stream() = s;
@@ -505,38 +527,69 @@ void gmres_solve(const dgb_bsr* a, const double* b, double* x, const dgb_solve_o
   double x_norm = std::sqrt(R.dot(x, x, n));
   std::vector<double> H(static_cast<size_t>(m + 1) * m), g(m + 1), y(m);
   int its = 0, restarts = 0;
+  // Arnoldi step k on the device: Hessenberg column k, rotations and g live in HBM
+  auto arnoldi_step = [&](int k) {
+    double* vk = Vp + static_cast<long long>(k) * n;
+    double* vn = Vp + static_cast<long long>(k + 1) * n;
+    double* hk = Hd.as<double>() + static_cast<long long>(k) * (m + 1);
+    A.precond(dinv.as<double>(), vk, z.as<double>());
+    A.spmv(z.as<double>(), w.as<double>());
+    R.dots_device(Vp, n, k + 1, w.as<double>(), n, hk);                          // CGS pass 1
+    subtract_combo_kernel<<<grid_for(n), kThreads, 0, s>>>(w.as<double>(), Vp, n, hk, k + 1, n);
+    R.dots_device(Vp, n, k + 1, w.as<double>(), n, hdev.as<double>());           // CGS pass 2
+    subtract_combo_kernel<<<grid_for(n), kThreads, 0, s>>>(w.as<double>(), Vp, n, hdev.as<double>(), k + 1, n);
+    add_small_kernel<<<1, kMaxRestart + 1, 0, s>>>(hk, hdev.as<double>(), k + 1);
+    R.dots_device(w.as<double>(), 0, 1, w.as<double>(), n, nrm.as<double>());
+    normalize_kernel<<<grid_for(n), kThreads, 0, s>>>(vn, w.as<double>(), nrm.as<double>(), hk + k + 1, n);
+    givens_kernel<<<1, 1, 0, s>>>(Hd.as<double>(), m + 1, csd.as<double>(), snd.as<double>(),
+                                  gd.as<double>(), k, resd.as<double>());
+    cuda_check(cudaGetLastError(), "arnoldi step");
+  };
+  // CUDA graphs for launch-bound (small) systems, on a capturable (non-legacy) stream
+  const bool use_graph = n <= kGraphMaxN && s != nullptr && s != cudaStreamLegacy;
+  cudaGraph_t cycle_graph = nullptr;
+  cudaGraphExec_t cycle_exec = nullptr;
+  struct GraphGuard {
+    cudaGraph_t* g;
+    cudaGraphExec_t* e;
+    ~GraphGuard() {
+      if (*e) cudaGraphExecDestroy(*e);
+      if (*g) cudaGraphDestroy(*g);
+    }
+  } graph_guard{&cycle_graph, &cycle_exec};
   while (true) {
     const double bound = 1e-10 * (a_fro * x_norm + b_norm);
     const double target = o.tolerance_scale * bound;
     if (beta <= target || its >= o.max_iterations) break;
     scale_kernel<<<grid_for(n), kThreads, 0, s>>>(Vp, r.as<double>(), 1.0 / beta, n);
-    // Arnoldi on the device: Hessenberg columns, rotations and g live in HBM; the host reads
-    // the residual estimate every kCheck steps (extra steps past convergence only lower it)
+    // the host reads the residual estimate every kCheck steps (extra steps past convergence
+    // only lower it)
     cuda_check(cudaMemsetAsync(gd.p, 0, sizeof(double) * (m + 1), s), "memset(g)");
     set_scalar_kernel<<<1, 1, 0, s>>>(gd.as<double>(), beta);
     int k = 0;
     bool done = false;
-    for (; k < m && its < o.max_iterations && !done; ++k) {
-      ++its;
-      double* vk = Vp + static_cast<long long>(k) * n;
-      double* vn = Vp + static_cast<long long>(k + 1) * n;
-      double* hk = Hd.as<double>() + static_cast<long long>(k) * (m + 1);
-      A.precond(dinv.as<double>(), vk, z.as<double>());
-      A.spmv(z.as<double>(), w.as<double>());
-      R.dots_device(Vp, n, k + 1, w.as<double>(), n, hk);                          // CGS pass 1
-      subtract_combo_kernel<<<grid_for(n), kThreads, 0, s>>>(w.as<double>(), Vp, n, hk, k + 1, n);
-      R.dots_device(Vp, n, k + 1, w.as<double>(), n, hdev.as<double>());           // CGS pass 2
-      subtract_combo_kernel<<<grid_for(n), kThreads, 0, s>>>(w.as<double>(), Vp, n, hdev.as<double>(), k + 1, n);
-      add_small_kernel<<<1, kMaxRestart + 1, 0, s>>>(hk, hdev.as<double>(), k + 1);
-      R.dots_device(w.as<double>(), 0, 1, w.as<double>(), n, nrm.as<double>());
-      normalize_kernel<<<grid_for(n), kThreads, 0, s>>>(vn, w.as<double>(), nrm.as<double>(), hk + k + 1, n);
-      givens_kernel<<<1, 1, 0, s>>>(Hd.as<double>(), m + 1, csd.as<double>(), snd.as<double>(),
-                                    gd.as<double>(), k, resd.as<double>());
-      cuda_check(cudaGetLastError(), "arnoldi step");
-      if ((k + 1) % kCheck == 0 || k + 1 == m || its >= o.max_iterations) {
-        cuda_check(cudaMemcpyAsync(est.p, resd.p, sizeof(double), cudaMemcpyDeviceToHost, s), "D2H(res)");
-        cuda_check(cudaStreamSynchronize(s), "cudaStreamSynchronize(res)");
-        done = *est.p <= target;
+    if (use_graph && its + m <= o.max_iterations) {
+      // small system: the m Arnoldi steps (13 launches each) as one CUDA graph, captured on
+      // the first cycle and replayed; the residual estimate is read once per cycle (extra
+      // steps past convergence only lower it)
+      if (!cycle_exec) {
+        cuda_check(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "cudaStreamBeginCapture");
+        for (int kk = 0; kk < m; ++kk) arnoldi_step(kk);
+        cuda_check(cudaStreamEndCapture(s, &cycle_graph), "cudaStreamEndCapture");
+        cuda_check(cudaGraphInstantiate(&cycle_exec, cycle_graph, 0), "cudaGraphInstantiate");
+      }
+      cuda_check(cudaGraphLaunch(cycle_exec, s), "cudaGraphLaunch");
+      k = m;
+      its += m;
+    } else {
+      for (; k < m && its < o.max_iterations && !done; ++k) {
+        ++its;
+        arnoldi_step(k);
+        if ((k + 1) % kCheck == 0 || k + 1 == m || its >= o.max_iterations) {
+          cuda_check(cudaMemcpyAsync(est.p, resd.p, sizeof(double), cudaMemcpyDeviceToHost, s), "D2H(res)");
+          cuda_check(cudaStreamSynchronize(s), "cudaStreamSynchronize(res)");
+          done = *est.p <= target;
+        }
       }
     }
     // y = H(0:k, 0:k)^-1 g (host, one copy per cycle), then x += M^-1 (V y)
