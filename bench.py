@@ -329,7 +329,8 @@ def run_ours(args, world, rank, local):
         pass
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic,
-                "peak_source": peak_kind, "kernel": f"assemble_kernel<{ref.n_local}>",
+                "peak_source": peak_kind,
+                "kernel": kernel_name(ref.n_local, spec.c.advection.kind == capi.VEC_CONSTANT, batched, args),
                 "kernel_ms": round(kern_avg_ms, 4), "bytes_per_launch": bytes_per_launch,
                 "assemblies_per_launch": sets_per_launch,
                 "kernel_share_of_step": round(sum(kern_ms) / total_ms, 3) if world == 1 else None}
@@ -883,6 +884,16 @@ def run_mesh(args, world, rank, local):
         "roofline": None, "cpu_baseline": cpu, "e2e": None, "gpu_launches": None,
         "clocks": clocks.summary(),
     }), flush=True)
+
+
+def kernel_name(nl: int, const_b: bool, batched: bool, args) -> str:
+    """The block-row kernel the library launches for this run (dg_assembly.cu launch_v2)."""
+    bound = not args.no_bind
+    if nl == 3 and const_b:
+        return "assemble_p1_pipe_kernel" if bound and args.p1_pipe != 0 else "assemble_p1_kernel"
+    if nl == 6 and const_b and bound and args.ws != 0 and ((batched and not args.no_fuse) or args.ws > 1):
+        return "assemble_ws_kernel"
+    return f"assemble_kernel<{nl}>"
 
 
 def l2_policy_text(l2: int) -> str:
