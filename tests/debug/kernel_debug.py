@@ -1,5 +1,5 @@
 """Debug aid: where a kernel differs from the oracle (block kind, boundary vs interior),
-toggling per-element fields and the Neumann side.  python tools/kernel_debug.py DEG QO VEL"""
+toggling per-element fields and the Neumann side.  python tests/debug/kernel_debug.py DEG QO VEL"""
 import sys
 sys.path.insert(0, '/root/repo')
 sys.path.insert(0, '/root/repo/tests')

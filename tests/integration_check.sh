@@ -15,6 +15,6 @@ open("gpurun_out/integration/dgfem/gpu.hpp", "w").write(code)
 PY
 REFINC=oracle/_ref/include
 [ -d /root/reference/proj/include ] && REFINC=/root/reference/proj/include
-g++ -std=c++20 -O2 -I$OUT -I$REFINC -Iinclude tools/integration/main.cpp oracle/_ref/obj/*.o \
+g++ -std=c++20 -O2 -I$OUT -I$REFINC -Iinclude tests/integration/main.cpp oracle/_ref/obj/*.o \
     paper_1502_02941_b200/libdgfem_b200.so -fopenmp -o $OUT/integ
 LD_LIBRARY_PATH=paper_1502_02941_b200 $OUT/integ
