@@ -313,9 +313,10 @@ enum dgb_plan_option {
   DGB_OPTION_BATCH_FUSE = 4, /* dgb_assemble_batch on the tensor-core kernels (default 1): sets
                                 with equal penalties share the per-element work and each CTA
                                 writes every set; 0 = one CTA row per set (grid.y = n) */
-  DGB_OPTION_WARP_SPECIALIZED = 5, /* P-form tensor-core kernels on a bound mesh (default 1):
-                                      persistent producer / consumer warps; 0 = the
-                                      monolithic kernel; 4..12 = producer warps of 16 (tuning) */
+  DGB_OPTION_WARP_SPECIALIZED = 5, /* P-form tensor-core kernels on a bound mesh (default 1:
+                                      8 producer + 4 consumer warps for config 2's kernel);
+                                      0 = the monolithic kernel; 4..12 = producer warps of 16,
+                                      100 p + c = p producers and c consumers (tuning) */
   DGB_OPTION_P1_PIPELINE = 6, /* P1 kernels on a bound mesh (default 1): persistent kernel with
                                  the record and node gathers in flight one chunk ahead
                                  (asynchronous copies), 12 warps per SM at 166 registers;

@@ -1366,8 +1366,9 @@ void launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_prob
       const int n_chunks = (out_row_end - out_row_begin + 31) / 32;
       cfg.gridDim = dim3(std::max(1, std::min(plan->sm_count, n_chunks)), 1);
       // producer : consumer warps (16 per CTA): option value 1 = the default per batch kind
-      // measured on config 2 (profiles/NOTES.md): the per-element pass is the longer side
-      const int np = plan->warp_specialized == 1 ? 10 : plan->warp_specialized;
+      // measured on config 2 (profiles/NOTES.md): 8 producers + 4 consumers (12 warps at 146
+      // registers) beats every 16-warp split at 128 registers (best 10 / 6)
+      const int np = plan->warp_specialized == 1 ? 804 : plan->warp_specialized;
       auto launch = [&](auto tag, auto ctag) {
         constexpr int NPW = decltype(tag)::value, NCW = decltype(ctag)::value;
         using WS = dgb::v2::SmemWs<NL, NQV, NQE, NPW, NCW>;
@@ -1389,6 +1390,9 @@ void launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_prob
           case 1105: launch(std::integral_constant<int, 11>{}, std::integral_constant<int, 5>{}); break;
           case 1206: launch(std::integral_constant<int, 12>{}, std::integral_constant<int, 6>{}); break;
           case 1406: launch(std::integral_constant<int, 14>{}, std::integral_constant<int, 6>{}); break;
+          case 804: launch(std::integral_constant<int, 8>{}, std::integral_constant<int, 4>{}); break;
+          case 903: launch(std::integral_constant<int, 9>{}, std::integral_constant<int, 3>{}); break;
+          case 705: launch(std::integral_constant<int, 7>{}, std::integral_constant<int, 5>{}); break;
           default: launch(std::integral_constant<int, 10>{}, std::integral_constant<int, 6>{}); break;
         }
       } else {
