@@ -4,15 +4,19 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C]
     python bench.py --op nonlinear [...]   # H(u), HJ(u) assembly
 
-Workload (default): BASELINE.json configs[1] = config 2 -- the 256x256 unit-square mesh
-(131,072 triangles), P2, assembled with each of SIPG, NIPG and IIPG (sigma = 18).  One step =
-the three assemblies (K = D + C + R in BSR form plus F).  `value` = elements assembled per
-second with mesh, tables and coefficients resident in HBM; `e2e` = the same metric through
-the host-buffer C-ABI call (dgb_assemble_all_host: H2D of the mesh, assembly, D2H of K and F).
+Workload (default): BASELINE.json configs[3] = config 4, the largest single-GPU config -- the
+2048x2048 unit-square mesh (8,388,608 triangles, element numbering Fisher-Yates permuted), P1,
+SIPG (sigma = 6), Gaussian manufactured solution.  One step = one assembly (K = D + C + R in BSR
+form plus F, `assemble_all` + `stiffness()`).  `value` = elements assembled per second with
+mesh, tables and coefficients resident in HBM; `e2e` = the same metric through the host-buffer
+C-ABI call (dgb_assemble_all_host: H2D of the mesh, bind, assembly, D2H of K and F);
+`secondary` = the other configs timed the same way in the same process (config 2 both as the
+fused 3-method batch and as one launch per method).
 
 Under torchrun (N > 1) each rank assembles its own shard (weak scaling; no collective on the
 data path), the step time is the max over ranks.  `--impl reference` times the reference's
 own CPU assembly (oracle/_ref, OpenMP on all host cores) on a bounded sample of the workload.
+Other ops: --op nonlinear | solve | mesh | spmv | c1-throughput (see --help).
 """
 from __future__ import annotations
 
@@ -43,12 +47,20 @@ def parse_args():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", type=int, default=2)
-    ap.add_argument("--op", choices=["assembly", "nonlinear", "solve", "mesh"], default="assembly",
+    ap.add_argument("--config", type=int, default=4,
+                    help="BASELINE.json config (default 4: the largest single-GPU config, "
+                         "8.4M triangles)")
+    ap.add_argument("--secondary", default="2,2s,3,5,1",
+                    help="assembly op, N = 1: also time these configs on the same box "
+                         "(device-resident; 'Cs' = one launch per method instead of the fused "
+                         "batch); '' for none")
+    ap.add_argument("--op", choices=["assembly", "nonlinear", "solve", "mesh", "spmv"],
+                    default="assembly",
                     help="assembly: the headline (assemble_all + stiffness); nonlinear: "
                          "assemble_nonlinear on the config's mesh and degree, r(u) = u^2; "
                          "solve: K x = F of the config's SIPG system (block-Jacobi GMRES); "
-                         "mesh: build_mesh + uniform_refine to level --levels on the device")
+                         "mesh: build_mesh + uniform_refine to level --levels on the device; "
+                         "spmv: config 4's 100 BSR SpMVs")
     ap.add_argument("--levels", type=int, default=10, help="--op mesh: refinement levels")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -166,25 +178,51 @@ def dist_setup(args):
     return world, rank, local
 
 
-def cpu_reference_sample(cfg_index: int, n_sample: int, seconds: float):
-    """Times the reference's own assemble_all + stiffness() (oracle/_ref, OpenMP on every host
-    core) on config `cfg_index`'s coefficients over an n_sample^2 unit-square mesh; falls back
-    to the plain-C restatement when the reference library is absent.  Returns
-    (elements/s, kind, cores, sample description, seconds)."""
+def _cores() -> int:
+    return len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+
+
+_RAW_CACHE: dict = {}
+
+
+def cpu_reference_sample(cfg_index: int, n_sample: int, seconds: float, threads: int = 0):
+    """Times the reference's own assemble_all + stiffness() (oracle/_ref, OpenMP over `threads`
+    host threads, default all) with config `cfg_index`'s coefficients on an n_sample^2
+    unit-square mesh (the config's jitter / permutation / boundary tags), repeating until
+    `seconds` of assembly time have accumulated (at least one assembly per method).  The mesh
+    comes from oracle/meshgen.py (numpy) through the reference's own build_mesh, so this leg
+    never loads the repo's CUDA library.  Falls back to the plain-C restatement when the
+    reference library is absent.  Returns (elements/s, kind, cores, sample description,
+    seconds)."""
+    from oracle import meshgen
     from oracle import oracle as orc
-    from paper_1502_02941_b200 import dgfem, problems
+    from paper_1502_02941_b200 import problems
     cfg = problems.CONFIGS[cfg_index]
-    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
-    mesh = dgfem.unit_square_mesh(n_sample, cfg.jitter, problems.SEED_JITTER, cfg.permute,
-                                  problems.SEED_PERMUTE, cfg.neumann_sides)
-    spec = problems.config_problem(cfg_index, mesh.n_elements)
-    params = [dgfem.config_parameters(cfg, m) for m in cfg.methods]
+    cores = threads if threads > 0 else _cores()
+    key = (cfg_index, n_sample)
+    if key not in _RAW_CACHE:
+        _RAW_CACHE.clear()
+        _RAW_CACHE[key] = {"raw": meshgen.config_raw(cfg, n_sample)}
+    cache = _RAW_CACHE[key]
+    raw = cache["raw"]
+    E = raw["elements"].shape[0]
+    spec = problems.config_problem(cfg_index, E)
     elements = 0
     t_total = 0.0
     try:
         lib = orc.RefLib()
-        raw = mesh.raw()
-        rmesh = lib.build_mesh(raw["nodes"], raw["elements"], raw["dirichlet"], raw["neumann"])
+        if "rmesh" not in cache:   # the reference's build_mesh (untimed, reported separately)
+            t0 = time.perf_counter()
+            cache["rmesh"] = lib.build_mesh(raw["nodes"], raw["elements"], raw["dirichlet"],
+                                            raw["neumann"])
+            cache["build_s"] = time.perf_counter() - t0
+        params = []
+        for m in cfg.methods:
+            p = lib.set_parameters(m, cfg.degree)          # the reference's set_parameters
+            p.sigma_interior, p.sigma_boundary = cfg.sigma, 2.0 * cfg.sigma
+            p.neumann_inflow = cfg.neumann_inflow
+            params.append(p)
+        rmesh = cache["rmesh"]
         rref = lib.reference(cfg.degree, cfg.quad_order)
         kind = "reference"
         clip = cfg.neumann_sides if cfg.neumann_inflow == 1 else 0
@@ -192,11 +230,14 @@ def cpu_reference_sample(cfg_index: int, n_sample: int, seconds: float):
             for p in params:
                 s = lib.assemble(rmesh, rref, spec.c, p, threads=cores, clip_sides=clip)
                 t_total += s.seconds[0] + s.seconds[1]
-                elements += mesh.n_elements
+                elements += E
                 del s
             if t_total >= seconds:
                 break
     except FileNotFoundError:
+        from paper_1502_02941_b200 import dgfem   # fallback only: the port needs mesh arrays
+        mesh = dgfem.build_mesh(raw["nodes"], raw["elements"], raw["dirichlet"], raw["neumann"])
+        params = [dgfem.config_parameters(cfg, m) for m in cfg.methods]
         ol = orc.OracleLib()
         kind = "port"
         arrays, tables = mesh.arrays(), dgfem.ReferenceElement(cfg.degree, cfg.quad_order).tables()
@@ -205,84 +246,59 @@ def cpu_reference_sample(cfg_index: int, n_sample: int, seconds: float):
                 t0 = time.perf_counter()
                 ol.assemble(arrays, tables, spec.c, p, threads=cores)
                 t_total += time.perf_counter() - t0
-                elements += mesh.n_elements
+                elements += E
             if t_total >= seconds:
                 break
-    desc = (f"config {cfg_index} coefficients on a {n_sample}x{n_sample} unit-square mesh "
-            f"({mesh.n_elements} elements), methods {len(params)}, assemble_all + stiffness(), "
-            f"{elements // mesh.n_elements} assemblies in {t_total:.1f} s")
+    full = " = the full config" if n_sample == cfg.n else ""
+    desc = (f"config {cfg_index} on a {n_sample}x{n_sample} mesh ({E} elements{full}), "
+            f"{len(cfg.methods)} method(s), assemble_all + stiffness() on {cores} threads, "
+            f"{elements // E} assemblies in {t_total:.2f} s")
     return elements / t_total, kind, cores, desc, t_total
 
 
-# ----------------------------------------------------------------------------- ours
-def run_ours(args, world, rank, local):
-    import ctypes as C
+def cpu_sample_size(cfg_index: int, budget_s: float, threads: int = 0) -> int:
+    """The largest n (the config's own n, halved until it fits) whose one-assembly-per-method
+    reference time is estimated to fit `budget_s`, from a calibration on a 64 x 64 mesh (the
+    reference's assembly time is linear in the element count)."""
+    from paper_1502_02941_b200 import problems
+    cfg = problems.CONFIGS[cfg_index]
+    rate = cpu_reference_sample(cfg_index, 64, 0.3, threads)[0]   # elements/s
+    n = cfg.n
+    while n > 16 and len(cfg.methods) * 2 * n * n / rate > budget_s:
+        n //= 2
+    return n
 
+
+def config_block(cfg, index: int, world: int, n_local: int) -> dict:
+    """The bench line's `config`: identical for both arms (needs no CUDA library)."""
+    E = 2 * cfg.n * cfg.n
+    return {
+        "workload": f"config {index}: {cfg.n}x{cfg.n} unit square, {E} triangles, P{cfg.degree}, "
+                    "methods " + "/".join(["SIPG", "NIPG", "IIPG"][m] for m in cfg.methods)
+                    + f", sigma={cfg.sigma:g}, quad_order {cfg.quad_order}",
+        "elements_per_step": world * E * len(cfg.methods), "n_local": n_local,
+        "global_mesh": f"{world * cfg.n}x{cfg.n} cells on [0,{world}]x[0,1]" if world > 1 else None,
+        "l2": "flushed between timed steps by a 256 MiB write (outside the timed events)",
+        "parallelism": f"{world} rank(s), element-row shards" if world > 1 else "1 GPU",
+    }
+
+
+def time_steps(run, stream, steps: int, warmup: int, flush, dist=None, clocks=None):
+    """W untimed steps, then `steps` timed steps of a workload.ConfigRun: CUDA events on
+    `stream` around every step and around every block-row kernel launch (recorded by the plan
+    on the launching stream), L2 flushed between steps outside the events.  `clocks` (a
+    ClockSampler) brackets the timed steps.  Returns (step_ms list, kernel_ms list)."""
     import torch
-    from paper_1502_02941_b200 import capi, dgfem, problems
-
-    torch.cuda.set_device(local)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    lib = capi.load()
-    from paper_1502_02941_b200 import shard
-    cfg = problems.CONFIGS[args.config]
-    mesh = dgfem.config_mesh(cfg, strips=world)       # global mesh: world x config size
-    ref = dgfem.ReferenceElement(cfg.degree, cfg.quad_order)
-    spec = problems.config_problem(args.config, mesh.n_elements)
-    params = [dgfem.config_parameters(cfg, m) for m in cfg.methods]
-    begin, end = shard.row_range(mesh.n_elements, rank, world)
-    l2 = args.l2_policy  # -1: the library's per-kernel default (profiles/NOTES.md)
-    shards = [shard.ShardAssembler(mesh, ref, spec, local, begin, end, bind=False)]
-    shards[0].plan.set_option(capi.OPTION_L2_POLICY, l2)
-    if args.l2_carve_mb:  # read at bind time
-        shards[0].plan.set_option(capi.OPTION_L2_CARVEOUT_MB, args.l2_carve_mb)
-    if not args.no_bind:
-        shards[0].plan.bind_mesh(shards[0].dmesh, begin, end)
-    shards += [shard.ShardAssembler(mesh, ref, spec, local, begin, end, share=shards[0])
-               for _ in params[1:]]   # one plan and one device mesh for all methods
-    plan = shards[0].plan
-    if args.minblocks:
-        plan.set_option(capi.OPTION_MIN_BLOCKS, args.minblocks)
-    if args.ablate:
-        plan.set_option(capi.OPTION_PROFILE_ABLATE, args.ablate)
-    if args.no_fuse:
-        plan.set_option(capi.OPTION_BATCH_FUSE, 0)
-    if args.ws >= 0:
-        plan.set_option(capi.OPTION_WARP_SPECIALIZED, args.ws)
-    if args.p1_pipe >= 0:
-        plan.set_option(capi.OPTION_P1_PIPELINE, args.p1_pipe)
-    stream = torch.cuda.current_stream(local)
-    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=f"cuda:{local}")  # 256 MiB > L2
-
-    batched = (not args.no_batch) and len(params) > 1
-
-    def step(kernel_events=None):
-        if batched:  # one dgb_assemble_batch: all methods in one launch when the rows are bound
-            if kernel_events is not None:
-                ks, ke = kernel_events[0]
-                lib.dgb_plan_set_kernel_events(plan._h, C.c_void_p(ks.cuda_event), C.c_void_p(ke.cuda_event))
-            shard.assemble_batch(shards, params, stream=stream, check=False)
-        else:
-            for i, (p, sh) in enumerate(zip(params, shards)):
-                if kernel_events is not None:
-                    ks, ke = kernel_events[i]
-                    lib.dgb_plan_set_kernel_events(plan._h, C.c_void_p(ks.cuda_event), C.c_void_p(ke.cuda_event))
-                sh.assemble(p, stream=stream, check=False)
-        lib.dgb_plan_set_kernel_events(plan._h, None, None)
-
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         flush.fill_(1.0)
-        step()
-    dgfem._check(lib.dgb_plan_status(plan._h, C.c_void_p(stream.cuda_stream)))
+        run.step(stream)
+    run.check_status(stream)
     torch.cuda.synchronize()
-
-    K = args.steps
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    nk = run.launches_per_step()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(steps)]
     kev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-            for _ in params] for _ in range(K)]
+            for _ in range(nk)] for _ in range(steps)]
     for row in kev:  # torch creates the cudaEvent_t lazily: record once so .cuda_event exists
         for a, b in row:
             a.record(stream)
@@ -290,69 +306,137 @@ def run_ours(args, world, rank, local):
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
-    with ClockSampler(local) as clocks:
-        for k in range(K):
-            flush.fill_(float(k))          # L2 flush between timed steps (outside the events)
-            ev[k][0].record(stream)
-            step(kev[k])
-            ev[k][1].record(stream)
-        torch.cuda.synchronize()
+    if clocks is not None:
+        clocks.__enter__()
+    for k in range(steps):
+        flush.fill_(float(k))          # L2 flush between timed steps (outside the events)
+        ev[k][0].record(stream)
+        run.step(stream, kev[k])
+        ev[k][1].record(stream)
+    torch.cuda.synchronize()
+    if clocks is not None:
+        clocks.__exit__(None, None, None)
     if dist:
         dist.barrier()
-    dgfem._check(lib.dgb_plan_status(plan._h, C.c_void_p(stream.cuda_stream)))
-    step_ms = [a.elapsed_time(b) for a, b in ev]
-    kern_ms = [a.elapsed_time(b) for row in kev for a, b in (row[:1] if batched else row)]
+    run.check_status(stream)
+    return ([a.elapsed_time(b) for a, b in ev],
+            [a.elapsed_time(b) for row in kev for a, b in row])
+
+
+def device_summary(run, step_ms, kern_ms, world: int = 1) -> dict:
+    """Throughput and roofline figures of one timed ConfigRun (this rank's rows)."""
+    sets = len(run.params) if run.batched else 1
+    nbytes = algorithmic_bytes(run.mesh, run.ref.n_local, len(run.spec.per_element), sets, world)
+    kms = sum(kern_ms) / len(kern_ms)
+    ms = sum(step_ms) / len(step_ms)
+    peak, _ = peak_hbm()
+    achieved = nbytes / (kms / 1e3) / 1e9
+    return {"value": round(len(run.params) * run.n_rows / (ms / 1e3), 1),
+            "ms_per_step": round(ms, 4), "kernel_ms": round(kms, 4), "bytes_per_launch": nbytes,
+            "achieved_gbs": round(achieved, 1), "frac": round(achieved / peak, 4),
+            "kernel_share_of_step": round(sum(kern_ms) / sum(step_ms), 3)}
+
+
+# ----------------------------------------------------------------------------- ours
+def run_ours(args, world, rank, local):
+    import torch
+    from paper_1502_02941_b200 import capi, problems, workload
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    lib = capi.load()
+    cfg = problems.CONFIGS[args.config]
+    options = {capi.OPTION_L2_POLICY: args.l2_policy,
+               capi.OPTION_L2_CARVEOUT_MB: args.l2_carve_mb or None,
+               capi.OPTION_MIN_BLOCKS: args.minblocks or None,
+               capi.OPTION_PROFILE_ABLATE: args.ablate or None,
+               capi.OPTION_BATCH_FUSE: 0 if args.no_fuse else None,
+               capi.OPTION_WARP_SPECIALIZED: args.ws if args.ws >= 0 else None,
+               capi.OPTION_P1_PIPELINE: args.p1_pipe if args.p1_pipe >= 0 else None}
+    run = workload.ConfigRun(args.config, local, rank, world, batch=not args.no_batch,
+                             bind=not args.no_bind, options=options)
+    mesh, ref, spec = run.mesh, run.ref, run.spec
+    batched = run.batched
+    stream = torch.cuda.current_stream(local)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=f"cuda:{local}")  # 256 MiB > L2
+
+    K = args.steps
+    clocks = ClockSampler(local)
+    step_ms, kern_ms = time_steps(run, stream, K, args.warmup, flush, dist, clocks)
     total_ms = sum(step_ms)
     if dist:
         t = torch.tensor([total_ms], device=f"cuda:{local}", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
     ms_per_step = total_ms / K
-    units_per_step = len(params) * mesh.n_elements   # all ranks together
+    units_per_step = len(run.params) * mesh.n_elements   # all ranks together
     value = units_per_step * K / (total_ms / 1e3)
+    launches = K * run.launches_per_step() * lib.dgb_plan_launch_count(run.plan._h)
+    bind_ms = run.bind_ms
 
-    # roofline of the block-row kernel (dominant launch)
-    per_elem_fields = len(spec.per_element)
-    sets_per_launch = len(params) if batched else 1
-    bytes_per_launch = algorithmic_bytes(mesh, ref.n_local, per_elem_fields, sets_per_launch, world)
-    kern_avg_ms = sum(kern_ms) / len(kern_ms)
-    achieved = bytes_per_launch / (kern_avg_ms / 1e3) / 1e9
+    # roofline of the block-row kernel (the dominant, and per step the only, launch)
+    summ = device_summary(run, step_ms, kern_ms, world)
     peak, peak_kind = peak_hbm()
     traffic = None
     try:
         with open(PROFILE_SUMMARY) as f:
-            prof = json.load(f)
-        entry = prof.get(f"config{args.config}")
+            entry = json.load(f).get(f"config{args.config}")
         if entry:
             traffic = entry.get("dram_bytes_per_launch")
     except Exception:
         pass
-    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(achieved / peak, 4), "traffic": traffic,
-                "peak_source": peak_kind,
-                "kernel": kernel_name(ref.n_local, spec.c.advection.kind == capi.VEC_CONSTANT, batched, args),
-                "kernel_ms": round(kern_avg_ms, 4), "bytes_per_launch": bytes_per_launch,
-                "assemblies_per_launch": sets_per_launch,
-                "kernel_share_of_step": round(sum(kern_ms) / total_ms, 3) if world == 1 else None}
+    roofline = {"bound": "hbm", "achieved": summ["achieved_gbs"], "peak": peak, "unit": "GB/s",
+                "frac": summ["frac"], "traffic": traffic, "peak_source": peak_kind,
+                "kernel": kernel_name(ref.n_local, spec.c.advection.kind == capi.VEC_CONSTANT,
+                                      batched, args),
+                "kernel_ms": summ["kernel_ms"], "bytes_per_launch": summ["bytes_per_launch"],
+                "assemblies_per_launch": len(run.params) if batched else 1,
+                "kernel_share_of_step": summ["kernel_share_of_step"] if world == 1 else None}
 
     # e2e through the host-buffer C-ABI entry point (pinned host memory in and out)
     e2e = None
     if not args.no_e2e:
+        from paper_1502_02941_b200 import dgfem
         local_mesh = mesh if world == 1 else dgfem.config_mesh(cfg)
         local_spec = spec if world == 1 else problems.config_problem(args.config, local_mesh.n_elements)
-        e2e = run_e2e(args, local_mesh, ref, local_spec, params, local)
+        e2e = run_e2e(args, local_mesh, ref, local_spec, run.params, local)
         if dist:
             t = torch.tensor([e2e["seconds"]], device=f"cuda:{local}", dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e["value"] = world * e2e["elements"] / float(t.item())
         e2e = {"value": round(e2e["value"], 1), "unit": "elements/s",
                "h2d_bytes_per_step": e2e["h2d"], "d2h_bytes_per_step": e2e["d2h"],
-               "steps": e2e["steps"], "api": "dgb_assemble_all_host"}
+               "steps": e2e["steps"], "api": "dgb_assemble_all_host",
+               "per_call": "H2D of mesh + coefficients, bind, assembly, D2H of K and F"}
+    del run, mesh
+    torch.cuda.empty_cache()
+
+    # the other BASELINE configs on the same box, device-resident (N = 1 only)
+    secondary = None
+    if world == 1 and args.secondary:
+        secondary = []
+        for item in args.secondary.split(","):
+            idx, batch = int(item.rstrip("s")), not item.endswith("s")   # "2s": one launch per method
+            r2 = workload.ConfigRun(idx, local, batch=batch)
+            s_ms, k_ms = time_steps(r2, stream, max(5, K // 2), 3, flush)
+            d = {"config": idx, **device_summary(r2, s_ms, k_ms),
+                 "launch": (f"one fused dgb_assemble_batch of {len(r2.params)} methods"
+                            if r2.batched else f"one launch per method ({len(r2.params)})"),
+                 "kernel": kernel_name(r2.ref.n_local,
+                                       r2.spec.c.advection.kind == capi.VEC_CONSTANT,
+                                       r2.batched, args),
+                 "bind_ms": round(r2.bind_ms, 4)}
+            secondary.append(d)
+            del r2
+            torch.cuda.empty_cache()
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        n_sample = {1: 32, 2: 96, 3: 32, 4: 128, 5: 24}[args.config]
-        v, kind, cores, desc, secs = cpu_reference_sample(args.config, n_sample, args.cpu_seconds)
+        n_sample = {1: 32, 2: 128, 3: 64, 4: 256, 5: 32}[args.config]
+        v, kind, cores, desc, _ = cpu_reference_sample(args.config, n_sample, args.cpu_seconds)
         cpu = {"value": round(v, 1), "unit": "elements/s", "cores": cores, "kind": kind,
                "sample": desc}
 
@@ -360,32 +444,29 @@ def run_ours(args, world, rank, local):
         dist.destroy_process_group()
     if rank != 0:
         return
+    conf = config_block(cfg, args.config, world, ref.n_local)
+    conf.update({
+        "nq_vol": ref.nq_vol, "nq_edge": ref.nq_edge,
+        "l2_policy": l2_policy_text(args.l2_policy),
+        "pattern": ("recomputed in every assembly (count + scan)" if args.no_bind else
+                    "bound once per mesh (dgb_plan_bind_mesh: count + scan + adjacency; "
+                    "untimed setup, see bind_ms); every assembly still writes row_ptr, block "
+                    "columns, values and RHS"),
+        "launch": ("one fused dgb_assemble_batch of the methods per step" if batched else
+                   "one launch per method"),
+    })
     line = {
         "metric": METRIC, "value": round(value, 1), "unit": "elements/s", "n_gpus": world,
         "steps": K, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded BASELINE.json config inputs; no dataset involved)",
-        "config": {
-            "workload": f"config {args.config}: {cfg.n}x{cfg.n} unit square, {mesh.n_elements} "
-                        f"triangles, P{cfg.degree}, methods "
-                        + "/".join(["SIPG", "NIPG", "IIPG"][m] for m in cfg.methods)
-                        + f", sigma={cfg.sigma:g}",
-            "elements_per_step": units_per_step, "n_local": ref.n_local,
-            "global_mesh": f"{world * cfg.n}x{cfg.n} cells on [0,{world}]x[0,1]" if world > 1 else None,
-            "nq_vol": ref.nq_vol, "nq_edge": ref.nq_edge,
-            "l2": "flushed between timed steps by a 256 MiB write (outside the timed events)",
-            "l2_policy": l2_policy_text(l2),
-            "pattern": ("recomputed in every assembly (count + scan)" if args.no_bind else
-                        "bound once per mesh (dgb_plan_bind_mesh, untimed setup); every assembly "
-                        "still writes row_ptr, block columns, values and RHS"),
-            "parallelism": f"{world} rank(s), element-row shards" if world > 1 else "1 GPU",
-            "launch": ("one dgb_assemble_batch per step (the methods as grid.y of one launch when "
-                       "the P2 tensor-core kernel applies)" if batched else "one launch per method"),
-        },
+        "config": conf,
+        "bind_ms": round(bind_ms, 4) if bind_ms is not None else None,
         "roofline": roofline,
         "cpu_baseline": cpu,
         "e2e": e2e,
-        "gpu_launches": K * (1 if batched else len(params)) * lib.dgb_plan_launch_count(plan._h),
+        "secondary": secondary,
+        "gpu_launches": launches,
         "clocks": clocks.summary(),
     }
     print(json.dumps(line), flush=True)
@@ -445,33 +526,41 @@ def run_e2e(args, mesh, ref, spec, params, device):
             "h2d": h2d * len(params), "d2h": d2h * len(params)}
 
 
+
 # ----------------------------------------------------------------------------- reference arm
 def run_reference(args, world, rank):
+    """The reference's own CPU assembly (oracle/_ref: assemble_all + stiffness(), OpenMP on
+    every host core) on the same config, metric and unit as our arm.  Each step is one bounded
+    sample: the config's own mesh when one assembly per method fits the per-step budget,
+    otherwise the largest halving of it that does (the metric is per element, and the
+    reference's time is linear in the element count).  Rank 0 only; the repo's CUDA library is
+    never loaded (oracle/meshgen.py feeds the reference's build_mesh)."""
     if rank != 0:
         return
     from paper_1502_02941_b200 import problems
     cfg = problems.CONFIGS[args.config]
-    n_sample = {1: 32, 2: 64, 3: 24, 4: 96, 5: 16}[args.config]
-    per_step = max(0.5, min(10.0, 120.0 / max(1, args.steps + args.warmup)))
+    per_step = max(0.5, min(10.0, 150.0 / max(1, args.steps + args.warmup)))
+    n_sample = cpu_sample_size(args.config, per_step)
     for _ in range(args.warmup):
         cpu_reference_sample(args.config, n_sample, 0.0)
     vals, secs_total = [], 0.0
     kind = cores = desc = None
-    for _ in range(args.steps):
-        v, kind, cores, desc, secs = cpu_reference_sample(args.config, n_sample, per_step)
+    for _ in range(args.steps):   # small samples repeat to ~1/4 of the step budget
+        v, kind, cores, desc, secs = cpu_reference_sample(args.config, n_sample, 0.25 * per_step)
         vals.append(v)
         secs_total += secs
-    value = statistics.fmean(vals)
+    value = len(vals) / sum(1.0 / v for v in vals)     # elements over total time
+    conf = config_block(cfg, args.config, world, (cfg.degree + 1) * (cfg.degree + 2) // 2)
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 1), "unit": "elements/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(1e3 * secs_total / args.steps, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded BASELINE.json config inputs)",
-        "config": {"workload": f"config {args.config} (bounded CPU sample: {desc})",
-                   "parallelism": f"OpenMP, {cores} host threads"},
+        "data": "synthetic (seeded BASELINE.json config inputs; no dataset involved)",
+        "config": conf,
+        "sample": desc,
         "cpu_baseline": {"value": round(value, 1), "unit": "elements/s", "cores": cores,
-                         "kind": kind, "sample": desc},
+                         "kind": kind, "sample": f"per step: {desc}"},
         "e2e": {"value": round(value, 1), "unit": "elements/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -818,6 +907,125 @@ def run_solve(args, world, rank, local):
     }), flush=True)
 
 
+# ----------------------------------------------------------------------------- spmv op
+METRIC_SPMV = ("BSR SpMV y = K x of the assembled config-4 system (fp64, 1 B200): block rows/sec "
+               "and achieved HBM GB/s vs roofline")
+
+
+def spmv_cpu_sample(n_sample: int, seconds: float):
+    """The reference's own matvec (sparse.cpp:116-129: serial CSR loop over stiffness()) on
+    config 4's system over an n_sample^2 mesh (oracle/_ref via ref_shim, which adds a copy of x
+    in and y out per call); the C restatement's OpenMP product when the reference is absent.
+    Returns (block rows/s, kind, cores, description)."""
+    from oracle import meshgen
+    from oracle import oracle as orc
+    from paper_1502_02941_b200 import capi, problems
+    cfg = problems.CONFIGS[4]
+    raw = meshgen.config_raw(cfg, n_sample)
+    E = raw["elements"].shape[0]
+    x = 2.0 * problems.uniform01(problems.SEED_SPMV_X, 3 * E) - 1.0
+    y = np.zeros(3 * E)
+    lib = orc.RefLib()
+    p = lib.set_parameters(capi.SIPG, 1)
+    p.sigma_interior, p.sigma_boundary = cfg.sigma, 2.0 * cfg.sigma
+    rmesh = lib.build_mesh(raw["nodes"], raw["elements"], raw["dirichlet"], raw["neumann"])
+    system = lib.assemble(rmesh, lib.reference(1, cfg.quad_order), problems.config_problem(4).c, p)
+    reps, t = 0, 0.0
+    while t < seconds:
+        t0 = time.perf_counter()
+        system.matvec(x, y)
+        t += time.perf_counter() - t0
+        reps += 1
+    desc = (f"the reference's matvec on config 4's SIPG system over a {n_sample}x{n_sample} mesh "
+            f"({E} block rows), {reps} products in {t:.2f} s, serial")
+    return E * reps / t, "reference", 1, desc
+
+
+def run_spmv(args, world, rank, local):
+    """Config 4's 100 BSR SpMVs (BASELINE.json configs[3]) on the matrix the bench's assembly
+    produces.  One step = the 100 products y = K x with x seeded U[-1, 1]; the matrix (2.4 GB)
+    and x (201 MB) exceed L2, so no flush is needed between products.  `value` = block rows
+    multiplied per second; roofline per product = SURVEY.md §8(d)'s 2,985,721,860 B."""
+    import torch
+    from paper_1502_02941_b200 import workload
+    torch.cuda.set_device(local)
+    sp = workload.SpmvRun(4, local)
+    stream = torch.cuda.current_stream(local)
+    n_prod = 100
+    for _ in range(args.warmup):
+        for _ in range(n_prod):
+            sp.step(stream)
+    torch.cuda.synchronize()
+    K = args.steps
+    ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(n_prod)] for _ in range(K)]
+    clocks = ClockSampler(local)
+    with clocks:
+        for k in range(K):
+            for j in range(n_prod):
+                ev[k][j][0].record(stream)
+                sp.step(stream)
+                ev[k][j][1].record(stream)
+        torch.cuda.synchronize()
+    prod_ms = [a.elapsed_time(b) for row in ev for a, b in row]
+    step_ms = [sum(a.elapsed_time(b) for a, b in row) for row in ev]
+    E = sp.run.n_rows
+    ms = sum(step_ms) / K
+    value = n_prod * E / (ms / 1e3)
+    nbytes = sp.bytes_per_product()
+    avg = sum(prod_ms) / len(prod_ms)
+    peak, peak_kind = peak_hbm()
+    traffic = None
+    try:
+        with open(PROFILE_SUMMARY) as f:
+            traffic = json.load(f).get("spmv_config4", {}).get("dram_bytes_per_launch")
+    except Exception:
+        pass
+    e2e = None
+    if not args.no_e2e:   # host x in, host y out, per product, through the C-ABI product
+        hx = sp.x.cpu().pin_memory()
+        hy = torch.empty_like(hx).pin_memory()
+        dx, dy = torch.empty_like(sp.x), torch.empty_like(sp.y)
+        torch.cuda.synchronize()
+        reps = 10
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            dx.copy_(hx, non_blocking=True)
+            sp.x, x_keep = dx, sp.x
+            sp.step(stream, dy)
+            sp.x = x_keep
+            hy.copy_(dy, non_blocking=True)
+            torch.cuda.synchronize()
+        secs = time.perf_counter() - t0
+        e2e = {"value": round(reps * E / secs, 1), "unit": "block rows/s",
+               "h2d_bytes_per_step": hx.numel() * 8, "d2h_bytes_per_step": hy.numel() * 8,
+               "note": "per product: H2D of x, dgb_spmv, D2H of y (K resident)"}
+    cpu = None
+    if not args.no_cpu_baseline:
+        try:
+            v, kind, cores, desc = spmv_cpu_sample(512, min(args.cpu_seconds, 10.0))
+            cpu = {"value": round(v, 1), "unit": "block rows/s", "cores": cores, "kind": kind,
+                   "sample": desc}
+        except FileNotFoundError:
+            cpu = None
+    print(json.dumps({
+        "metric": METRIC_SPMV, "value": round(value, 1), "unit": "block rows/s", "n_gpus": 1,
+        "steps": K, "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (config 4's assembled system, x seeded U[-1,1])",
+        "config": {"workload": f"config 4: {n_prod} BSR SpMVs per step on the 2048x2048 P1 SIPG "
+                               f"matrix ({E} block rows, {sp.system.col.shape[0]} 3x3 blocks)",
+                   "l2": "matrix 2.4 GB and x 201 MB exceed L2 (no flush needed)"},
+        "roofline": {"bound": "hbm", "achieved": round(nbytes / (avg / 1e3) / 1e9, 1), "peak": peak,
+                     "unit": "GB/s", "frac": round(nbytes / (avg / 1e3) / 1e9 / peak, 4),
+                     "traffic": traffic, "peak_source": peak_kind,
+                     "kernel": "bsr_spmv_kernel<3,256>", "kernel_ms": round(avg, 4),
+                     "bytes_per_launch": nbytes, "kernel_share_of_step": 1.0},
+        "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": K * n_prod,
+        "clocks": clocks.summary(),
+    }), flush=True)
+
+
 # ----------------------------------------------------------------------------- mesh op
 METRIC_MESH = ("mesh topology build (build_mesh + uniform_refine chain to the C4 size): "
                "elements/sec (1 B200)")
@@ -915,6 +1123,10 @@ def main():
         return
     if args.op == "solve":
         run_solve(args, world, rank, local)
+        return
+    if args.op == "spmv":
+        if rank == 0:
+            run_spmv(args, world, rank, local)
         return
     if args.op == "nonlinear":
         if args.impl == "reference":

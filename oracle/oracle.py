@@ -282,9 +282,12 @@ class RefSystem:
         self.lib.lib.dgref_system_rhs(self.h, _ptr(F))
         return F
 
-    def matvec(self, x: np.ndarray) -> np.ndarray:
+    def matvec(self, x: np.ndarray, out: np.ndarray | None = None) -> np.ndarray:
+        """The reference's own matvec (sparse.cpp:116-129) of stiffness() with x."""
         x = np.ascontiguousarray(x, dtype=np.float64)
-        y = np.zeros((row_ptr.shape[0] - 1) * nl)  # rows of the (possibly sharded) BSR
+        nnz, n = C.c_longlong(), C.c_int()
+        self.lib.lib.dgref_system_nnz(self.h, 0, C.byref(nnz), C.byref(n))
+        y = np.zeros(n.value) if out is None else out
         self.lib._check(self.lib.lib.dgref_matvec(self.h, _ptr(x), _ptr(y)))
         return y
 

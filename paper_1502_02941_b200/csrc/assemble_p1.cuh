@@ -140,7 +140,7 @@ __device__ __forceinline__ void p1_row(const Params2<3, NQV, NQE, false, true>& 
   const double G00 = B11 * rdet, G01 = -B10 * rdet;
   const double G10 = -B01 * rdet, G11 = B00 * rdet;
   const double eps = scalar_element(P.prob.diffusion, ee);
-  if (P.ablate & 32) {  // (profiling ablation: gathers and own geometry only)
+  if (DGB_ABLATE(32)) {  // (profiling ablation: gathers and own geometry only)
     if (active) o_rhs[ee - P.row_begin] = det + po[0].x + po[1].x + po[2].x;
     return;
   }
@@ -151,7 +151,7 @@ __device__ __forceinline__ void p1_row(const Params2<3, NQV, NQE, false, true>& 
   for (int i = 0; i < NL; ++i) F[i] = 0.0;
   {
     source_points<NQV, false>(
-        P.prob.source, ee, P.ablate & 2,
+        P.prob.source, ee, DGB_ABLATE(2),
         [&](int q, double& px, double& py) {
           // volume points only evaluate coefficients (no term selection): fused
           px = fma(B01, P.t.x[L::VY + q], fma(B00, P.t.x[L::VX + q], pv[0].x));
@@ -231,7 +231,7 @@ __device__ __forceinline__ void p1_row(const Params2<3, NQV, NQE, false, true>& 
       cp = sh * (h * eps_e) - up;
       const double cx = up - sh * (h * eps_e);
       // K_ef = sum_p phi^l_p (x) b1_p + a2_p (x) phi^lf_(n-1-p)
-      if (!(P.ablate & 4)) {  // (profiling ablation: skip the neighbour block)
+      if (!(DGB_ABLATE(4))) {  // (profiling ablation: skip the neighbour block)
       const double* trm = tr + lf * (NQE * 3 * NL);
       // P1: the reference gradients are constant, so the neighbour's w d phi at its points are
       // the same for every edge: read them from the constant bank (edge 0) with the
@@ -387,7 +387,7 @@ __device__ __forceinline__ void p1_row(const Params2<3, NQV, NQE, false, true>& 
     double* dst = o_val + static_cast<long long>(rp_first) * N2;
     const int head = rp_first & 1;
     const int body = (n - head) & ~1;
-    if (lane == 0 && body > 0 && !(P.ablate & 1)) bulk_store(dst + head, srow + head, body * sizeof(double), P.evict_first);
+    if (lane == 0 && body > 0 && !(DGB_ABLATE(1))) bulk_store(dst + head, srow + head, body * sizeof(double), P.evict_first);
     // (a warp past the last row has no range: n <= 0, nothing to write)
     if (lane == 1 && head && n > 0) dst[0] = srow[0];
     if (lane == 2 && n > 0 && head + body < n) dst[n - 1] = srow[n - 1];
@@ -431,7 +431,7 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_p1_kernel(
     rp = __ldg(P.row_ptr_src + (ee - P.row_begin));
     rp_next = __ldg(P.row_ptr_src + (ee - P.row_begin + 1));
   }
-  if (P.ablate & 64) {  // (profiling ablation: index records only)
+  if (DGB_ABLATE(64)) {  // (profiling ablation: index records only)
     if (active) o_rhs[ee - P.row_begin] = double(v[0] + v[1] + v[2] + anb.x + anb.w + aop.x + aop.z + rp + rp_next);
     return;
   }
@@ -445,7 +445,7 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_p1_kernel(
     po[1] = hints ? ld_hint(nodes2 + max(aop.y, 0), pol_g) : __ldg(nodes2 + max(aop.y, 0));
     po[2] = hints ? ld_hint(nodes2 + max(aop.z, 0), pol_g) : __ldg(nodes2 + max(aop.z, 0));
   }
-  p1_row<NQV, NQE, BOUND>(P, tr, mset, stw, P.ablate & 128 ? srhs : nullptr, lane, blockIdx.x * blockDim.x + warp * 32, ee,
+  p1_row<NQV, NQE, BOUND>(P, tr, mset, stw, DGB_ABLATE(128) ? srhs : nullptr, lane, blockIdx.x * blockDim.x + warp * 32, ee,
                           active, v, anb, aop, rp, rp_next, pv, po, false, [] {});
   if (lane == 0) bulk_wait_all();
 }

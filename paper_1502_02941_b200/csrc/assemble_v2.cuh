@@ -17,6 +17,15 @@
 //    in shared memory and writes it back with coalesced stores at the block's sorted slot.
 #pragma once
 
+// Profiling ablations (dgb_plan_set_option(DGB_OPTION_PROFILE_ABLATE), results WRONG while
+// set) exist only in a tuning build (-DDGB_TUNING, see tools/README.md); in the shipped library
+// every ablation test is the constant 0 and compiles away.
+#ifdef DGB_TUNING
+#define DGB_ABLATE(bits) (P.ablate & (bits))
+#else
+#define DGB_ABLATE(bits) 0
+#endif
+
 namespace dgb {
 namespace v2 {
 
@@ -506,7 +515,7 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
                      : (c == 1 ? -g1 : g0 - g1);
   }
   __syncthreads();
-  if (P.ablate & 16) return;
+  if (DGB_ABLATE(16)) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   // this CTA's parameter set (grid.y) and its outputs
   // split form (fused P-form batch): shared products, kappa applied per set at the store
@@ -579,7 +588,7 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
   const double G00 = B11 * rdet, G01 = -B10 * rdet;
   const double G10 = -B01 * rdet, G11 = B00 * rdet;
   const double eps = scalar_element(P.prob.diffusion, ee);
-  if (P.ablate & 32) {
+  if (DGB_ABLATE(32)) {
     if (active) o_rhs[ee - P.row_begin] = det;
     return;
   }
@@ -590,7 +599,7 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
   for (int i = 0; i < NL; ++i) F[i] = 0.0;
   {
     source_points<NQV, TRIG>(
-        P.prob.source, ee, P.ablate & 2,
+        P.prob.source, ee, DGB_ABLATE(2),
         [&](int q, double& px, double& py) {
           // volume points only evaluate coefficients (no term selection): fused
           px = fma(B01, P.t.x[L::VY + q], fma(B00, P.t.x[L::VX + q], pv[0].x));
@@ -903,19 +912,19 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
       __syncwarp();
       const int g = lane >> 2, t = lane & 3;
       if constexpr (kSplit) {
-        if (!(P.ablate & 8)) {
+        if (!(DGB_ABLATE(8))) {
           mma_block_store_split<SM::kKS, SM::kNT, N2>(
               [&](int m, int ks) { return sk[(4 * ks + t) * SM::kCT + 8 * m + g]; }, o_bfrag,
-              (active && !(P.ablate & 1)) ? static_cast<long long>(rp + diag_slot) * N2 : -1LL,
+              (active && !(DGB_ABLATE(1))) ? static_cast<long long>(rp + diag_slot) * N2 : -1LL,
               P.bt + mset, n_sets, lane, pol);
         }
-      } else if (!(P.ablate & 8)) {
+      } else if (!(DGB_ABLATE(8))) {
 #pragma unroll 1
         for (int s = 0; s < n_sets; ++s) {
           mma_block_store<SM::kKS, SM::kNT, N2>(
               [&](int m, int ks) { return sk[(4 * ks + t) * SM::kCT + 8 * m + g]; },
               P.bt[mset + s].bfrag,
-              (active && !(P.ablate & 1)) ? static_cast<long long>(rp + diag_slot) * N2 : -1LL,
+              (active && !(DGB_ABLATE(1))) ? static_cast<long long>(rp + diag_slot) * N2 : -1LL,
               P.bt[mset + s].val, lane, pol);
         }
       }
@@ -1024,7 +1033,7 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
     if (!__any_sync(0xffffffffu, has)) continue;
     const int lf = (meta >> 2) & 3, slot = meta >> 4;
     if constexpr (SM::kMma) {
-      if (P.ablate & 4) continue;
+      if (DGB_ABLATE(4)) continue;
       // neighbour terms X, Y0, Y1, Z0, Z1 of edge l.  The B operand depends on the
       // neighbour's local edge lf, so the warp's elements are regrouped into 8-row m-tiles of
       // equal lf (rows are independent in D = C . B): ceil(n_lf / 8) tiles per lf value, each
@@ -1099,7 +1108,7 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
               dmma_8x8x4(d0, d1, c0, bv[0][nt]);
               dmma_8x8x4(z0, z1, c1, bv[1][nt]);
               const int n0 = 8 * nt + 2 * t;
-              if (cb >= 0 && !(P.ablate & 1)) {
+              if (cb >= 0 && !(DGB_ABLATE(1))) {
 #pragma unroll
                 for (int s = 0; s < kMaxBatch; ++s) {
                   if (s < n_sets) {
@@ -1148,7 +1157,7 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
 #pragma unroll
               for (int ks = 0; ks < KO; ++ks) dmma_8x8x4(d0, d1, ca[ks], bv[ks][nt]);
               const int n0 = 8 * nt + 2 * t;
-              if (cb >= 0 && !(P.ablate & 1)) store_entries<N2>(o_val + cb, n0, d0, d1, pol);
+              if (cb >= 0 && !(DGB_ABLATE(1))) store_entries<N2>(o_val + cb, n0, d0, d1, pol);
             }
           }
         } else {
@@ -1192,7 +1201,7 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
                 double d0 = 0.0, d1 = 0.0;
 #pragma unroll
                 for (int ks = 0; ks < KO; ++ks) dmma_8x8x4(d0, d1, at[u][ks], bk[ks]);
-                if (bt_[u] >= 0 && !(P.ablate & 1)) store_entries<N2>(o_val + bt_[u], n0, d0, d1, pol);
+                if (bt_[u] >= 0 && !(DGB_ABLATE(1))) store_entries<N2>(o_val + bt_[u], n0, d0, d1, pol);
               }
             }
           }

@@ -93,7 +93,7 @@ __device__ __forceinline__ void ws_produce(const Params2<NL, NQV, NQE, false, fu
   for (int i = 0; i < NL; ++i) F[i] = 0.0;
   {
     source_points<NQV, false>(
-        P.prob.source, ee, P.ablate & 2,
+        P.prob.source, ee, DGB_ABLATE(2),
         [&](int q, double& px, double& py) {
           // volume points only evaluate coefficients (no term selection): fused
           px = fma(B01, P.t.x[L::VY + q], fma(B00, P.t.x[L::VX + q], pv[0].x));
@@ -373,8 +373,8 @@ __device__ __forceinline__ void ws_consume(const Params2<NL, NQV, NQE, false, fu
   const unsigned long long pol = output_policy(P.evict_first);
   const double* frag = P.bt[0].bfrag;
 
-  if (!(P.ablate & 8)) {
-    const long long base = (active && !(P.ablate & 1)) ? static_cast<long long>(rp + diag_slot) * N2 : -1LL;
+  if (!(DGB_ABLATE(8))) {
+    const long long base = (active && !(DGB_ABLATE(1))) ? static_cast<long long>(rp + diag_slot) * N2 : -1LL;
     auto a_at = [&](int m, int ks) { return sk[(4 * ks + t) * CT + 8 * m + g]; };
     ws_diag<SM::kKS, NT, N2, FUSE>(a_at, frag, base, P.bt, n_sets, lane, pol);
   }
@@ -385,7 +385,7 @@ __device__ __forceinline__ void ws_consume(const Params2<NL, NQV, NQE, false, fu
     const int meta = mk[l * 32 + lane];
     const bool has = (meta & 3) == DGB_EDGE_INTERIOR;
     if (!__any_sync(0xffffffffu, has)) continue;
-    if (P.ablate & 4) continue;
+    if (DGB_ABLATE(4)) continue;
     const int lf = (meta >> 2) & 3, bslot = meta >> 4;
     const unsigned lt = (1u << lane) - 1u;
     const unsigned m0 = __ballot_sync(0xffffffffu, has && lf == 0);
@@ -451,7 +451,7 @@ __device__ __forceinline__ void ws_consume(const Params2<NL, NQV, NQE, false, fu
             dmma_8x8x4(d[nt][0], d[nt][1], c1, bv[1][nt]);
           }
         }
-        if (cb >= 0 && !(P.ablate & 1)) {
+        if (cb >= 0 && !(DGB_ABLATE(1))) {
           if constexpr (FUSE) {
 #pragma unroll
             for (int s = 0; s < kMaxBatch; ++s) {
@@ -492,7 +492,7 @@ __global__ void __launch_bounds__(SmemWs<NL, NQV, NQE, NPROD, NCONS>::kThreads, 
   double* rhs_st = slots + NS * W::kSlot;
   if (threadIdx.x < W::kBars) mbar_init(bars + threadIdx.x, 32);
   __syncthreads();
-  if (P.ablate & 16) return;
+  if (DGB_ABLATE(16)) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool producer = warp < NP;
   const int n_sets = FUSE ? P.n_batch : 1;

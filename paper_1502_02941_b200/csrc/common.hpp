@@ -31,6 +31,11 @@ int record_error(int status, const std::string& message, long long detail);
 // Clears the thread's last error (successful calls).
 void clear_error();
 
+#ifdef __CUDACC__
+// y = K x over a BSR on `s` (spmv.cu): the one SpMV of the library (dgb_spmv and the solve).
+void launch_bsr_spmv(const dgb_bsr* a, const double* x, double* y, cudaStream_t s);
+#endif
+
 // Runs fn, translating exceptions into status codes.
 template <typename Fn>
 int guarded(Fn&& fn) {

@@ -26,6 +26,7 @@
 #include <mutex>
 #include <string>
 #include <limits>
+#include <map>
 #include <type_traits>
 #include <vector>
 
@@ -760,30 +761,6 @@ __global__ void __launch_bounds__(256) assemble_kernel(const __grid_constant__ K
 }
 
 // ------------------------------------------------------------------------------------------
-// BSR SpMV: y = K x (one thread per scalar row)
-// ------------------------------------------------------------------------------------------
-template <int NL>
-__global__ void __launch_bounds__(256) spmv_kernel(int32_t n_rows,
-                                                   const int32_t* __restrict__ row_ptr,
-                                                   const int32_t* __restrict__ col,
-                                                   const double* __restrict__ val,
-                                                   const double* __restrict__ x,
-                                                   double* __restrict__ y) {
-  const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (t >= static_cast<long long>(n_rows) * NL) return;
-  const int e = static_cast<int>(t / NL), i = static_cast<int>(t - static_cast<long long>(e) * NL);
-  const int b0 = __ldg(row_ptr + e), b1 = __ldg(row_ptr + e + 1);
-  double s = 0.0;
-  for (int b = b0; b < b1; ++b) {
-    const double* blkrow = val + (static_cast<long long>(b) * NL + i) * NL;
-    const double* xs = x + static_cast<long long>(__ldg(col + b)) * NL;
-#pragma unroll
-    for (int j = 0; j < NL; ++j) s = fma(__ldg(blkrow + j), __ldg(xs + j), s);
-  }
-  y[t] = s;
-}
-
-// ------------------------------------------------------------------------------------------
 // host: tensors from reference tables
 // ------------------------------------------------------------------------------------------
 Layout make_layout(int nl, int nqv, int nqe) {
@@ -925,13 +902,68 @@ void cuda_check(cudaError_t err, const char* what) {
 
 int tile_for(int nl) { return nl <= 6 ? 64 : 32; }
 
+// The dynamic shared-memory limit is an attribute of a kernel in one device context: raise it
+// once per (kernel, device) pair, under a lock (a process-wide flag would skip a second device,
+// and concurrent first calls would race on it).
+void ensure_dynamic_smem(const void* fn, size_t bytes, const char* what) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> done;
+  int dev = 0;
+  cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& have = done[{fn, dev}];
+  if (bytes > have) {
+    cuda_check(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(bytes)), what);
+    have = bytes;
+  }
+}
+
 }  // namespace dgb
 
 // ------------------------------------------------------------------------------------------
 // plan + C-ABI
 // ------------------------------------------------------------------------------------------
-// the persisting-L2 carve-out (process-wide device limit) was set by a plan of this library
-static bool g_carve_out_is_ours = false;
+// The persisting-L2 carve-out (cudaLimitPersistingL2CacheSize) is one limit per device,
+// shared by everything in the process.  Plans that want one hold a reference on their device:
+// the first reference saves the caller's limit, the limit is only ever raised while references
+// are held, and the last release restores the saved value.
+namespace {
+struct CarveOut {
+  int refs = 0;
+  size_t saved = 0;
+};
+std::mutex g_carve_mu;
+std::map<int, CarveOut> g_carve;
+
+// Takes (or keeps) a reference on `device`'s carve-out and raises it to at least `want`;
+// returns the limit now in force.
+size_t carve_acquire(int device, size_t want, bool held) {
+  std::lock_guard<std::mutex> lock(g_carve_mu);
+  CarveOut& c = g_carve[device];
+  size_t cur = 0;
+  cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+  if (!held) {
+    if (c.refs == 0) c.saved = cur;
+    ++c.refs;
+  }
+  if (cur < want) {
+    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
+    cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+  }
+  cudaGetLastError();
+  return cur;
+}
+
+void carve_release(int device) {
+  std::lock_guard<std::mutex> lock(g_carve_mu);
+  CarveOut& c = g_carve[device];
+  if (c.refs > 0 && --c.refs == 0) {
+    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, c.saved);
+    cudaGetLastError();
+  }
+}
+}  // namespace
 
 struct dgb_plan {
   int device = 0;
@@ -943,6 +975,10 @@ struct dgb_plan {
   // offending edge wins and no per-assembly reset is needed
   unsigned long long* d_err = nullptr;
   unsigned long long epoch = 0;
+  // dgb_plan_status reports an InflowOnNeumann raised by any launch of the latest call, i.e.
+  // an error word with epoch in [status_from, epoch] (a per-set batch spans several epochs)
+  unsigned long long status_from = 0;
+  bool in_batch = false;
   void* d_scan = nullptr;
   size_t scan_bytes = 0;
   int32_t scan_n = 0;
@@ -966,6 +1002,7 @@ struct dgb_plan {
   const void* bound_edge_elements = nullptr;
   int32_t last_launches = 0;
   size_t l2_persist_bytes = 0;  // persisting-L2 carve-out available to the node window
+  bool carve_held = false;      // this plan holds a reference on its device's carve-out
   size_t l2_window_max = 0;     // cudaDevAttrMaxAccessPolicyWindowSize
   size_t l2_persist_max = 0;    // cudaDevAttrMaxPersistingL2CacheSize
   int l2_policy = -1;           // bit 0: persist nodes in L2, bit 1: evict-first output; -1 auto
@@ -999,21 +1036,9 @@ struct DeviceGuard {
 
 template <int NL>
 void launch_assemble(const dgb::KParams& P, int n_tiles, size_t smem, cudaStream_t s) {
-  static bool configured = false;
-  if (!configured) {
-    cuda_check(cudaFuncSetAttribute(dgb::assemble_kernel<NL>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024),
-               "cudaFuncSetAttribute");
-    configured = true;
-  }
+  dgb::ensure_dynamic_smem(reinterpret_cast<const void*>(dgb::assemble_kernel<NL>), 200 * 1024,
+                           "cudaFuncSetAttribute");
   dgb::assemble_kernel<NL><<<n_tiles, 256, smem, s>>>(P);
-}
-
-template <int NL>
-void launch_spmv(const dgb_bsr* a, const double* x, double* y, cudaStream_t s) {
-  const long long rows = static_cast<long long>(a->n_block_rows) * NL;
-  const int grid = static_cast<int>((rows + 255) / 256);
-  if (grid > 0) dgb::spmv_kernel<NL><<<grid, 256, 0, s>>>(a->n_block_rows, a->row_ptr, a->col, a->val, x, y);
 }
 
 void validate_tables(const dgb_reference_tables* t) {
@@ -1307,26 +1332,21 @@ void launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_prob
       smem_bytes = sizeof(double) * (SP::kTr + (THREADS / 32) * SP::kWarp);
     }
   }
-  static size_t configured = 0;
-  if (std::max(smem_bytes, smem) > configured) {  // every kernel this instantiation may launch
-    const int bytes = static_cast<int>(std::max(smem_bytes, smem));
-    cuda_check(cudaFuncSetAttribute(dgb::v2::assemble_kernel<NL, NQV, NQE, BK, THREADS, MINB>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, bytes),
-               "cudaFuncSetAttribute(v2)");
+  {  // every kernel this instantiation may launch
+    const size_t bytes = std::max(smem_bytes, smem);
+    dgb::ensure_dynamic_smem(reinterpret_cast<const void*>(dgb::v2::assemble_kernel<NL, NQV, NQE, BK, THREADS, MINB>),
+                             bytes, "cudaFuncSetAttribute(v2)");
     if constexpr (SM::kMma) {
-      cuda_check(cudaFuncSetAttribute(dgb::v2::assemble_kernel<NL, NQV, NQE, BK, THREADS, MINB, true>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, bytes),
-                 "cudaFuncSetAttribute(v2 fused)");
+      dgb::ensure_dynamic_smem(
+          reinterpret_cast<const void*>(dgb::v2::assemble_kernel<NL, NQV, NQE, BK, THREADS, MINB, true>), bytes,
+          "cudaFuncSetAttribute(v2 fused)");
     }
     if constexpr (NL == 3 && BK == 0) {
-      cuda_check(cudaFuncSetAttribute(dgb::v2::assemble_p1_kernel<NQV, NQE, THREADS, MINB, true>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, bytes),
-                 "cudaFuncSetAttribute(p1)");
-      cuda_check(cudaFuncSetAttribute(dgb::v2::assemble_p1_kernel<NQV, NQE, THREADS, MINB, false>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, bytes),
-                 "cudaFuncSetAttribute(p1)");
+      dgb::ensure_dynamic_smem(reinterpret_cast<const void*>(dgb::v2::assemble_p1_kernel<NQV, NQE, THREADS, MINB, true>),
+                               bytes, "cudaFuncSetAttribute(p1)");
+      dgb::ensure_dynamic_smem(reinterpret_cast<const void*>(dgb::v2::assemble_p1_kernel<NQV, NQE, THREADS, MINB, false>),
+                               bytes, "cudaFuncSetAttribute(p1)");
     }
-    configured = std::max(smem_bytes, smem);
   }
   const int grid = (out_row_end - out_row_begin + THREADS - 1) / THREADS;
   // Keep the node coordinates (gathered by every element and its neighbours, in random order
@@ -1374,12 +1394,12 @@ void launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_prob
         using WS = dgb::v2::SmemWs<NL, NQV, NQE, NPW, NCW>;
         auto wk = fuse ? dgb::v2::assemble_ws_kernel<NL, NQV, NQE, true, NPW, NCW>
                        : dgb::v2::assemble_ws_kernel<NL, NQV, NQE, false, NPW, NCW>;
-        cuda_check(cudaFuncSetAttribute(wk, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        int(WS::kBytes)), "cudaFuncSetAttribute(ws)");
+        dgb::ensure_dynamic_smem(reinterpret_cast<const void*>(wk), WS::kBytes, "cudaFuncSetAttribute(ws)");
         cfg.blockDim = dim3(WS::kThreads);
         cfg.dynamicSmemBytes = WS::kBytes;
         cuda_check(cudaLaunchKernelEx(&cfg, wk, P), "cudaLaunchKernelEx(ws)");
       };
+#ifdef DGB_TUNING
       if constexpr (NL == 6 && NQV == 7) {  // config 2's kernel: producer share tunable
         // n (4..12): n producers of 16 warps; 100 p + c: p producers, c consumers
         switch (np) {
@@ -1398,6 +1418,16 @@ void launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_prob
       } else {
         launch(std::integral_constant<int, 8>{}, std::integral_constant<int, 8>{});
       }
+#else
+      // the shipped split (profiles/NOTES.md): 8 producer + 4 consumer warps for config 2's
+      // kernel, 8 + 8 for the other P-form shapes
+      (void)np;
+      if constexpr (NL == 6 && NQV == 7) {
+        launch(std::integral_constant<int, 8>{}, std::integral_constant<int, 4>{});
+      } else {
+        launch(std::integral_constant<int, 8>{}, std::integral_constant<int, 8>{});
+      }
+#endif
       return;
     }
   }
@@ -1414,8 +1444,7 @@ void launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_prob
         constexpr int W = decltype(tag)::value;
         using PS = dgb::v2::SmemP1Pipe<NQV, NQE, W>;
         auto pk = dgb::v2::assemble_p1_pipe_kernel<NQV, NQE, W>;
-        cuda_check(cudaFuncSetAttribute(pk, cudaFuncAttributeMaxDynamicSharedMemorySize, int(PS::kBytes)),
-                   "cudaFuncSetAttribute(p1 pipe)");
+        dgb::ensure_dynamic_smem(reinterpret_cast<const void*>(pk), PS::kBytes, "cudaFuncSetAttribute(p1 pipe)");
         const int n_chunks = (out_row_end - out_row_begin + 31) / 32;
         cfg.gridDim = dim3(std::max(1, std::min(plan->sm_count, (n_chunks + W - 1) / W)), nb);
         cfg.blockDim = dim3(32 * W);
@@ -1447,6 +1476,7 @@ bool try_launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_
     launch_v2<NL_, NQV_, NQE_, BK_, T_, MB_>(plan, mesh, problem, params, out, rhs, nb, s, rb, re, src); \
     return true;                                                                           \
   }
+#ifdef DGB_TUNING
   if (mb == 3) {  // tuning variants of the headline kernels: smaller CTAs (shorter tail)
     DGB_V2(6, 7, 3, 0, 64, 6)
     DGB_V2(3, 6, 2, 0, 64, 8)
@@ -1459,6 +1489,7 @@ bool try_launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_
     DGB_V2(6, 7, 3, 0, 128, 6)
     DGB_V2(3, 6, 2, 0, 128, 6)
   }
+#endif
   DGB_V2(3, 6, 2, 0, 128, 4)
   DGB_V2(3, 6, 2, 1, 128, 4)
   DGB_V2(3, 6, 2, 2, 128, 4)
@@ -1605,13 +1636,8 @@ void launch_nonlinear(const dgb::nlr::NlParams& P, cudaStream_t s) {
   const size_t smem = sizeof(double) * (((P.nq * NL + 1) & ~1) + ((P.nq + 1) & ~1) +
                                         (kThreads / 32) * (4 * P.ks * dgb::nlr::kCT + 32 * NL));
   auto kernel = dgb::nlr::nonlinear_kernel<NL>;
-  static size_t configured = 0;
-  if (smem > configured) {  // raise the dynamic shared-memory limit once per size class
-    cuda_check(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(std::max<size_t>(smem, 48 * 1024))),
-               "cudaFuncSetAttribute(nonlinear)");
-    configured = std::max<size_t>(smem, 48 * 1024);
-  }
+  dgb::ensure_dynamic_smem(reinterpret_cast<const void*>(kernel), std::max<size_t>(smem, 48 * 1024),
+                           "cudaFuncSetAttribute(nonlinear)");
   const int grid = (P.n_elements + kThreads - 1) / kThreads;
   kernel<<<grid, kThreads, smem, s>>>(P);
   cuda_check(cudaGetLastError(), "nonlinear_kernel");
@@ -1667,19 +1693,14 @@ int dgb_plan_bind_mesh(dgb_plan* plan, const dgb_mesh_arrays* mesh, int32_t row_
       if (p1_auto) want = std::min(want, size_t(56) << 20);
       if (want > 0 && plan->l2_carve_mb > 0) want = std::min(want, size_t(plan->l2_carve_mb) << 20);
       plan->l2_persist_bytes = 0;
-      if (want == 0 && g_carve_out_is_ours) {
-        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);
-        g_carve_out_is_ours = false;
-        cudaGetLastError();
+      if (want == 0 && plan->carve_held) {
+        carve_release(plan->device);
+        plan->carve_held = false;
       }
       if (want > 0) {
-        g_carve_out_is_ours = true;
-        size_t cur = 0;
-        cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
-        if (cur != want) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
-        cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
-        plan->l2_persist_bytes = cur;
-        cudaGetLastError();
+        const size_t cur = carve_acquire(plan->device, want, plan->carve_held);
+        plan->carve_held = true;
+        plan->l2_persist_bytes = std::min(cur, want);
       }
     }
     plan->bound_ee = mesh->element_edges;
@@ -1767,11 +1788,7 @@ void dgb_plan_destroy(dgb_plan* p) {
   int prev = -1;
   cudaGetDevice(&prev);
   cudaSetDevice(p->device);
-  if (p->l2_persist_bytes > 0 && g_carve_out_is_ours) {  // the carve-out this plan set up
-    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);
-    g_carve_out_is_ours = false;
-    cudaGetLastError();
-  }
+  if (p->carve_held) carve_release(p->device);  // restores the caller's limit with the last one
   cudaFree(p->d_tens);
   cudaFree(p->d_err);
   cudaFree(p->d_scan);
@@ -1827,7 +1844,7 @@ int dgb_assemble_batch(dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_pr
       DeviceGuard guard(plan->device);
       cudaStream_t s = static_cast<cudaStream_t>(stream);
       plan->last_status = DGB_OK;
-      ++plan->epoch;
+      plan->status_from = ++plan->epoch;
       plan->last_launches = 1;
       if (plan->ev_start) cuda_check(cudaEventRecord(plan->ev_start, s), "cudaEventRecord");
       if (!try_launch_v2(plan, mesh, problem, params, outs, rhs, n, s, row_begin, row_end,
@@ -1839,12 +1856,19 @@ int dgb_assemble_batch(dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_pr
     if (st != DGB_STATUS_UNSUPPORTED_DEGREE) return st;  // else: the per-set path below
   }
   int launches = 0;
+  const unsigned long long from = plan->epoch + 1;
+  plan->in_batch = true;
   for (int i = 0; i < n; ++i) {
     const int st = dgb_assemble_rows(plan, mesh, problem, params + i, row_begin, row_end, outs + i,
                                      rhs[i], stream);
-    if (st != DGB_OK) return st;
+    if (st != DGB_OK) {
+      plan->in_batch = false;
+      return st;
+    }
     launches += plan->last_launches;
   }
+  plan->in_batch = false;
+  plan->status_from = std::min(from, plan->epoch);
   plan->last_launches = launches;
   return DGB_OK;
 }
@@ -1883,6 +1907,7 @@ int dgb_assemble_rows(dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_pro
       return;
     }
     ++plan->epoch;
+    if (!plan->in_batch) plan->status_from = plan->epoch;
     const bool bound = plan->d_pattern && plan->bound_ee == mesh->element_edges &&
                        plan->bound_elements == mesh->elements &&
                        plan->bound_edge_elements == mesh->edge_elements &&
@@ -1988,7 +2013,14 @@ int dgb_plan_set_option(dgb_plan* plan, int32_t option, int32_t value) {
     case DGB_OPTION_P1_PIPELINE: plan->p1_pipe = value; return DGB_OK;
     case DGB_OPTION_L2_CARVEOUT_MB: plan->l2_carve_mb = value; return DGB_OK;
     // profiling diagnostics (results are WRONG while set): see the header
-    case DGB_OPTION_PROFILE_ABLATE: plan->ablate = value; return DGB_OK;
+    case DGB_OPTION_PROFILE_ABLATE:
+#ifdef DGB_TUNING
+      plan->ablate = value;
+      return DGB_OK;
+#else
+      return dgb::record_error(DGB_STATUS_INVALID_ARGUMENT,
+                               "profiling ablations need a tuning build (-DDGB_TUNING)", option);
+#endif
     default: return DGB_STATUS_INVALID_ARGUMENT;
   }
 }
@@ -2001,7 +2033,9 @@ int dgb_plan_status(dgb_plan* plan, void* stream) {
     cuda_check(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)), "cudaStreamSynchronize");
     unsigned long long w = 0;
     cuda_check(cudaMemcpy(&w, plan->d_err, sizeof w, cudaMemcpyDeviceToHost), "cudaMemcpy(err)");
-    if ((w >> 32) == (plan->epoch & 0xFFFFFFFFull) && plan->epoch != 0) {
+    const unsigned long long we = w >> 32;
+    if (plan->epoch != 0 && we >= (plan->status_from & 0xFFFFFFFFull) &&
+        we <= (plan->epoch & 0xFFFFFFFFull)) {
       throw dgb::Error(DGB_STATUS_INFLOW_ON_NEUMANN,
                        "inflow across a Neumann edge: no boundary data to upwind from",
                        static_cast<long long>(0xFFFFFFFFull - (w & 0xFFFFFFFFull)));
@@ -2012,15 +2046,8 @@ int dgb_plan_status(dgb_plan* plan, void* stream) {
 int dgb_spmv(const dgb_bsr* a, const double* x, double* y, void* stream) {
   return dgb::guarded([&] {
     if (!a || !x || !y) throw dgb::Error(DGB_STATUS_INVALID_ARGUMENT, "null argument");
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    switch (a->block_dim) {
-      case 3: launch_spmv<3>(a, x, y, s); break;
-      case 6: launch_spmv<6>(a, x, y, s); break;
-      case 10: launch_spmv<10>(a, x, y, s); break;
-      case 15: launch_spmv<15>(a, x, y, s); break;
-      default: throw dgb::Error(DGB_STATUS_UNSUPPORTED_DEGREE, "unsupported block size", a->block_dim);
-    }
-    cuda_check(cudaGetLastError(), "spmv_kernel");
+    if (a->n_block_rows < 0 || a->nnzb < 0) throw dgb::Error(DGB_STATUS_INVALID_ARGUMENT, "negative size");
+    dgb::launch_bsr_spmv(a, x, y, static_cast<cudaStream_t>(stream));  // spmv.cu
   });
 }
 
@@ -2083,6 +2110,13 @@ int dgb_assemble_all_host(const dgb_mesh_arrays* mesh, const dgb_reference_table
     cuda_check(cudaMemcpyAsync(out->val, d.val, sizeof(double) * nnzb * nl * nl, cudaMemcpyDeviceToHost, s), "D2H");
     cuda_check(cudaMemcpyAsync(rhs, d_rhs, sizeof(double) * E * nl, cudaMemcpyDeviceToHost, s), "D2H");
     cuda_check(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+    // the cached plan outlives the call: give the persisting-L2 carve-out back at once, so a
+    // host-buffer call never leaves L2 set aside in the caller's process
+    if (plan->carve_held) {
+      carve_release(plan->device);
+      plan->carve_held = false;
+      plan->l2_persist_bytes = 0;
+    }
   });
 }
 

@@ -16,6 +16,8 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <mutex>
+#include <set>
 #include <vector>
 
 #include "common.hpp"
@@ -111,24 +113,6 @@ __global__ void block_apply_kernel(const double* __restrict__ d, const double* _
   double s = 0.0;
 #pragma unroll
   for (int j = 0; j < NL; ++j) s = fma(row[j], xs[j], s);
-  y[r] = s;
-}
-
-// y = K x over a BSR (one thread per scalar row, sorted block columns).
-template <int NL>
-__global__ void bsr_spmv_kernel(const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
-                                const double* __restrict__ val, const double* __restrict__ x,
-                                double* __restrict__ y, long long n) {
-  const long long r = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (r >= n) return;
-  const int e = static_cast<int>(r / NL), i = static_cast<int>(r - static_cast<long long>(e) * NL);
-  double s = 0.0;
-  for (int b = row_ptr[e]; b < row_ptr[e + 1]; ++b) {
-    const double* blk = val + static_cast<long long>(b) * NL * NL + i * NL;
-    const double* xs = x + static_cast<long long>(col[b]) * NL;
-#pragma unroll
-    for (int j = 0; j < NL; ++j) s = fma(blk[j], xs[j], s);
-  }
   y[r] = s;
 }
 
@@ -301,17 +285,18 @@ cudaStream_t& alloc_stream() {
   return st;
 }
 
-void keep_pool_cached() {
-  static bool done = false;
-  if (done) return;
+void keep_pool_cached() {  // per device (each has its own default pool)
+  static std::mutex mu;
+  static std::set<int> done;
   int dev = 0;
   cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  if (!done.insert(dev).second) return;
   cudaMemPool_t pool;
   if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
     unsigned long long keep = ~0ull;
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
   }
-  done = true;
 }
 
 struct DevBuf {
@@ -375,16 +360,7 @@ struct BsrOps {
   long long n;
   cudaStream_t s;
 
-  void spmv(const double* x, double* y) const {
-    switch (nl) {
-      case 3: bsr_spmv_kernel<3><<<grid_for(n), kThreads, 0, s>>>(a->row_ptr, a->col, a->val, x, y, n); break;
-      case 6: bsr_spmv_kernel<6><<<grid_for(n), kThreads, 0, s>>>(a->row_ptr, a->col, a->val, x, y, n); break;
-      case 10: bsr_spmv_kernel<10><<<grid_for(n), kThreads, 0, s>>>(a->row_ptr, a->col, a->val, x, y, n); break;
-      case 15: bsr_spmv_kernel<15><<<grid_for(n), kThreads, 0, s>>>(a->row_ptr, a->col, a->val, x, y, n); break;
-      default: throw dgb::Error(DGB_STATUS_UNSUPPORTED_DEGREE, "unsupported block size", nl);
-    }
-    cuda_check(cudaGetLastError(), "bsr_spmv_kernel");
-  }
+  void spmv(const double* x, double* y) const { dgb::launch_bsr_spmv(a, x, y, s); }
   void precond(const double* dinv, const double* x, double* y) const {
     switch (nl) {
       case 3: block_apply_kernel<3><<<grid_for(n), kThreads, 0, s>>>(dinv, x, y, n); break;

@@ -45,3 +45,47 @@ def gather_rows(rp, col, val, rhs, rows):
     out_rp[1:] = np.cumsum(counts)
     idx = np.concatenate([np.arange(rp[r], rp[r + 1]) for r in rows]) if rows.size else np.zeros(0, int)
     return out_rp, col[idx], val[idx], rhs[rows]
+
+
+def expected_pattern(mesh: dict):
+    """The reference's K pattern (SURVEY.md §8 "K pattern": the diagonal block plus both
+    off-diagonal blocks of every interior edge, block columns sorted ascending, as
+    `stiffness()`'s CSR has them, sparse.cpp:46-51) computed in numpy from the mesh arrays
+    alone: (row_ptr [E+1], col [E+2I]).  Size-independent, so it checks the GPU pattern of a
+    full-size config bit for bit."""
+    ee = mesh["element_edges"].astype(np.int64)                  # [E, 3]
+    lr = mesh["edge_elements"][ee]                               # [E, 3, 2]
+    E = ee.shape[0]
+    me = np.arange(E, dtype=np.int64)[:, None]
+    nb = np.where(lr[..., 0] == me, lr[..., 1], lr[..., 0]).astype(np.int64)
+    big = np.iinfo(np.int64).max
+    nb = np.where(nb < 0, big, nb)
+    cols = np.sort(np.concatenate([me, nb], axis=1), axis=1)     # [E, 4]
+    keep = cols != big
+    row_ptr = np.zeros(E + 1, np.int32)
+    row_ptr[1:] = np.cumsum(keep.sum(axis=1))
+    return row_ptr, cols[keep].astype(np.int32)
+
+
+def sample_rows(n_rows: int, seed: int, n_sample: int = 4000, edge: int = 64) -> np.ndarray:
+    """A seeded sample of block rows plus the first and last `edge` rows (sorted, unique)."""
+    rng = np.random.default_rng(seed)
+    return np.unique(np.concatenate([
+        rng.choice(n_rows, size=min(n_rows, n_sample), replace=False),
+        np.arange(min(edge, n_rows)), np.arange(max(0, n_rows - edge), n_rows)]))
+
+
+def gather_rows_device(out, rows):
+    """Block rows `rows` of a device BsrSystem, gathered on the device and copied back in the
+    oracle's subset layout (avoids copying a multi-GB full matrix to the host)."""
+    import torch
+    rows = np.asarray(rows)
+    rp = out.row_ptr.cpu().numpy()
+    counts = rp[rows + 1] - rp[rows]
+    out_rp = np.zeros(rows.size + 1, np.int32)
+    out_rp[1:] = np.cumsum(counts)
+    idx = np.concatenate([np.arange(rp[r], rp[r + 1]) for r in rows])
+    it = torch.from_numpy(idx).to(out.val.device)
+    ir = torch.from_numpy(rows.astype(np.int64)).to(out.val.device)
+    return (out_rp, out.col[it].cpu().numpy(), out.val[it].cpu().numpy(),
+            out.rhs[ir].cpu().numpy())

@@ -19,32 +19,6 @@ def to_np(s):
     return (s.row_ptr.cpu().numpy(), s.col.cpu().numpy(), s.val.cpu().numpy(), s.rhs.cpu().numpy())
 
 
-def test_spmv_matches_oracle_config4_size(oracle):
-    """Config 4 (2048^2 x 2, P1, permuted) K x for seeded U[-1,1] x: |dy_i| <= 1e-12 sum_j |K_ij x_j|
-    (SURVEY.md §8(c)); 100 products reuse the same K (bench --config 4 times them)."""
-    import torch
-    cfg = problems.CONFIGS[4]
-    mesh = dgfem.config_mesh(cfg)
-    ref = dgfem.ReferenceElement(cfg.degree, cfg.quad_order)
-    spec = problems.config_problem(4)
-    params = dgfem.config_parameters(cfg, capi.SIPG)
-    plan = dgfem.Plan(ref.view)
-    dm, dp = dgfem.DeviceMesh(mesh), dgfem.DeviceProblem(spec)
-    out = plan.assemble(dm, dp, params, plan.allocate(dm))
-    n = mesh.n_elements * ref.n_local
-    x = torch.from_numpy(2.0 * problems.uniform01(problems.SEED_SPMV_X, n) - 1.0).cuda()
-    y = torch.empty_like(x)
-    for _ in range(3):
-        plan.spmv(out, x, y)
-    torch.cuda.synchronize()
-    rp, col, val, _ = to_np(out)
-    xs = x.cpu().numpy()
-    y_ref = oracle.spmv(rp, col, val, xs)
-    absx = np.abs(xs)
-    scale = oracle.spmv(rp, col, np.abs(val), absx)
-    assert np.all(np.abs(y.cpu().numpy() - y_ref) <= 1e-12 * scale + 1e-300)
-
-
 def test_inflow_on_neumann_reports_lowest_edge(oracle):
     """test_assembly.cpp:371-381, test_parallel_consistency.cpp:152-182."""
     mesh = dgfem.unit_square_mesh(6, 0.0, 0, False, 0, 15)   # all Neumann
@@ -62,6 +36,71 @@ def test_inflow_on_neumann_reports_lowest_edge(oracle):
     params.neumann_inflow = capi.INFLOW_DROP
     g = dgfem.assemble_all(mesh, ref, spec, params)
     compare_system(to_np(g), oracle.assemble(mesh.arrays(), ref.tables(), spec.c, params))
+
+
+def test_batch_reports_error_of_an_earlier_set(oracle):
+    """dgb_assemble_batch over sets that differ in the Neumann policy (per-set launches): an
+    InflowOnNeumann raised by the first set (ERROR) is still reported after a later set (DROP)
+    assembled cleanly, with the reference's lowest-edge detail."""
+    mesh = dgfem.unit_square_mesh(6, 0.0, 0, False, 0, 15)   # all Neumann
+    ref = dgfem.ReferenceElement(1)
+    spec = problems.registry_get("smooth-sine")
+    p_err = dgfem.set_parameters(capi.SIPG, 1, capi.INFLOW_ERROR)
+    p_drop = dgfem.set_parameters(capi.SIPG, 1, capi.INFLOW_DROP)
+    a = shard.ShardAssembler(mesh, ref, spec, 0, 0, mesh.n_elements)
+    b = shard.ShardAssembler(mesh, ref, spec, 0, 0, mesh.n_elements, share=a)
+    with pytest.raises(dgfem.Error) as e:
+        shard.assemble_batch([a, b], [p_err, p_drop])
+    assert e.value.code == "InflowOnNeumann"
+    from oracle.oracle import ReferenceError_
+    with pytest.raises(ReferenceError_) as r:
+        oracle.assemble(mesh.arrays(), ref.tables(), spec.c, p_err)
+    assert e.value.detail == r.value.detail
+    # a clean call afterwards reports no stale error
+    shard.assemble_batch([a, b], [p_drop, p_drop])
+
+
+def _l2_limit() -> int:
+    from cuda.bindings import runtime as rt
+    err, v = rt.cudaDeviceGetLimit(rt.cudaLimit.cudaLimitPersistingL2CacheSize)
+    assert err == rt.cudaError_t.cudaSuccess
+    return int(v)
+
+
+def _set_l2_limit(v: int) -> None:
+    from cuda.bindings import runtime as rt
+    (err,) = rt.cudaDeviceSetLimit(rt.cudaLimit.cudaLimitPersistingL2CacheSize, v)
+    assert err == rt.cudaError_t.cudaSuccess
+
+
+def test_l2_carve_out_is_restored():
+    """The P1 plans' persisting-L2 carve-out is per device and reference counted: a bound plan
+    raises the limit, the host-buffer entry (a cached plan) gives it back at the end of the
+    call, and destroying the last plan restores the caller's own value."""
+    import torch
+    torch.cuda.init()
+    cfg = problems.CONFIGS[4]
+    mesh = dgfem.unit_square_mesh(64, 0.0, 0, True, 3, 0)
+    ref = dgfem.ReferenceElement(cfg.degree, cfg.quad_order)
+    spec = problems.config_problem(4)
+    params = dgfem.config_parameters(cfg, capi.SIPG)
+    _set_l2_limit(1 << 20)          # the caller's own carve-out
+    start = _l2_limit()
+    dgfem.assemble_all_host(mesh, ref.view, spec, params)
+    assert _l2_limit() == start
+    a = shard.ShardAssembler(mesh, ref, spec, 0, 0, mesh.n_elements, bind=True)
+    b = shard.ShardAssembler(mesh, ref, spec, 0, 0, mesh.n_elements, bind=True)
+    a.assemble(params)
+    assert _l2_limit() >= start
+    del a
+    import gc
+    gc.collect()
+    assert _l2_limit() >= start    # b still holds its reference
+    b.assemble(params)
+    del b
+    gc.collect()
+    assert _l2_limit() == start
+    _set_l2_limit(0)
 
 
 @pytest.mark.parametrize("index", [2, 3])
