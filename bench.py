@@ -54,13 +54,16 @@ def parse_args():
                     help="assembly op, N = 1: also time these configs on the same box "
                          "(device-resident; 'Cs' = one launch per method instead of the fused "
                          "batch); '' for none")
-    ap.add_argument("--op", choices=["assembly", "nonlinear", "solve", "mesh", "spmv"],
+    ap.add_argument("--op", choices=["assembly", "nonlinear", "solve", "mesh", "spmv",
+                                     "c1-throughput"],
                     default="assembly",
                     help="assembly: the headline (assemble_all + stiffness); nonlinear: "
                          "assemble_nonlinear on the config's mesh and degree, r(u) = u^2; "
                          "solve: K x = F of the config's SIPG system (block-Jacobi GMRES); "
                          "mesh: build_mesh + uniform_refine to level --levels on the device; "
-                         "spmv: config 4's 100 BSR SpMVs")
+                         "spmv: config 4's 100 BSR SpMVs; c1-throughput: config 1 single "
+                         "launch, CUDA-graph replay and --copies systems per launch")
+    ap.add_argument("--copies", type=int, default=512, help="--op c1-throughput: systems per launch")
     ap.add_argument("--levels", type=int, default=10, help="--op mesh: refinement levels")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -1019,9 +1022,73 @@ def run_spmv(args, world, rank, local):
         "roofline": {"bound": "hbm", "achieved": round(nbytes / (avg / 1e3) / 1e9, 1), "peak": peak,
                      "unit": "GB/s", "frac": round(nbytes / (avg / 1e3) / 1e9 / peak, 4),
                      "traffic": traffic, "peak_source": peak_kind,
-                     "kernel": "bsr_spmv_kernel<3,256>", "kernel_ms": round(avg, 4),
+                     "kernel": "bsr_spmv_kernel<3,128,3>", "kernel_ms": round(avg, 4),
                      "bytes_per_launch": nbytes, "kernel_share_of_step": 1.0},
         "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": K * n_prod,
+        "clocks": clocks.summary(),
+    }), flush=True)
+
+
+# ----------------------------------------------------------------------------- small-config throughput
+def run_c1_throughput(args, world, rank, local):
+    """Config 1's throughput figures (BASELINE.md §2 note 1): config 1 (2,048 triangles, 0.77 MB
+    of output) cannot approach its roofline in one launch, so beside the single launch this
+    reports (a) a CUDA graph replaying G single assemblies back to back and (b) B = --copies
+    independent config-1 systems in ONE launch of the bound block-row kernel (the disjoint
+    union of B copies of the mesh; workload.BatchedSystemsRun).  `value` = (b)'s elements/s."""
+    import torch
+    from paper_1502_02941_b200 import workload
+    torch.cuda.set_device(local)
+    stream = torch.cuda.current_stream(local)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=f"cuda:{local}")
+    K = args.steps
+    single = workload.ConfigRun(1, local)
+    s_ms, k_ms = time_steps(single, stream, K, args.warmup, flush)
+    single_sum = device_summary(single, s_ms, k_ms)
+    G = 100
+    graph = workload.capture_graph(single, G)
+    for _ in range(args.warmup):
+        graph.replay()
+    torch.cuda.synchronize()
+    gev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    for k in range(K):
+        flush.fill_(float(k))
+        gev[k][0].record(stream)
+        graph.replay()
+        gev[k][1].record(stream)
+    torch.cuda.synchronize()
+    g_ms = sum(a.elapsed_time(b) for a, b in gev) / K
+    E1 = single.n_rows
+    del graph, single
+    torch.cuda.empty_cache()
+    batch = workload.BatchedSystemsRun(1, args.copies, local)
+    clocks = ClockSampler(local)
+    b_ms, bk_ms = time_steps(batch, stream, K, args.warmup, flush, clocks=clocks)
+    summ = device_summary(batch, b_ms, bk_ms)
+    peak, peak_kind = peak_hbm()
+    print(json.dumps({
+        "metric": METRIC + " -- config 1 throughput (many systems)", "value": summ["value"],
+        "unit": "elements/s", "n_gpus": 1, "steps": K, "warmup": args.warmup,
+        "ms_per_step": summ["ms_per_step"], "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (config 1's seeded inputs, replicated)",
+        "config": {"workload": f"{args.copies} independent config-1 systems (32x32 unit square, "
+                               f"2048 triangles, P1, SIPG) per launch: the bound block-row kernel "
+                               f"over their disjoint union ({batch.n_rows} block rows)",
+                   "l2": "flushed between timed steps by a 256 MiB write (outside the timed events)"},
+        "roofline": {"bound": "hbm", "achieved": summ["achieved_gbs"], "peak": peak, "unit": "GB/s",
+                     "frac": summ["frac"], "traffic": None, "peak_source": peak_kind,
+                     "kernel": "assemble_p1_pipe_kernel", "kernel_ms": summ["kernel_ms"],
+                     "bytes_per_launch": summ["bytes_per_launch"],
+                     "kernel_share_of_step": summ["kernel_share_of_step"]},
+        "single_launch": {"value": single_sum["value"], "kernel_ms": single_sum["kernel_ms"],
+                          "ms_per_step": single_sum["ms_per_step"], "frac": single_sum["frac"]},
+        "graph_replay": {"assemblies_per_replay": G, "ms_per_replay": round(g_ms, 4),
+                         "us_per_assembly": round(1e3 * g_ms / G, 2),
+                         "value": round(G * E1 / (g_ms / 1e3), 1)},
+        "bind_ms": round(batch.bind_ms, 4),
+        "cpu_baseline": None, "e2e": None,
+        "gpu_launches": K * batch.launches_per_step(),
         "clocks": clocks.summary(),
     }), flush=True)
 
@@ -1127,6 +1194,10 @@ def main():
     if args.op == "spmv":
         if rank == 0:
             run_spmv(args, world, rank, local)
+        return
+    if args.op == "c1-throughput":
+        if rank == 0:
+            run_c1_throughput(args, world, rank, local)
         return
     if args.op == "nonlinear":
         if args.impl == "reference":

@@ -118,3 +118,58 @@ class SpmvRun:
         nl, E = self.run.ref.n_local, self.run.n_rows
         nnzb = self.system.col.shape[0]
         return 8 * nl * nl * nnzb + 4 * nnzb + 4 * (E + 1) + 16 * nl * E
+
+
+def replicated_raw(raw: dict, copies: int) -> dict:
+    """The disjoint union of `copies` copies of a raw mesh (nodes, elements, boundary pairs):
+    copy b's node and element indices are offset by b n_nodes and b n_elements, so no edge is
+    shared between copies and the assembled union is block diagonal -- copy b's system is block
+    rows [b E, (b+1) E) with block columns offset by b E."""
+    import numpy as np
+    nn = raw["nodes"].shape[0]
+    off = (np.arange(copies, dtype=np.int64) * nn)[:, None, None]
+    rep = lambda a: (a[None].astype(np.int64) + off).reshape(-1, a.shape[1]).astype(np.int32)  # noqa: E731
+    return {"nodes": np.tile(raw["nodes"], (copies, 1)), "elements": rep(raw["elements"]),
+            "dirichlet": rep(raw["dirichlet"]), "neumann": rep(raw["neumann"])}
+
+
+class BatchedSystemsRun(ConfigRun):
+    """`copies` independent systems of config `index` in ONE launch: the bound block-row kernel
+    over the disjoint union of the config's mesh repeated `copies` times (BASELINE.md §2 note 1:
+    a small config's throughput figure).  System b is block rows [b E, (b+1) E) of the output,
+    its block columns offset by b E and its row_ptr by b nnzb; `system(b)` returns it with both
+    offsets removed (the reference's per-call DgSystem of that copy)."""
+
+    def __init__(self, index: int = 1, copies: int = 512, device: int = 0):
+        cfg = problems.CONFIGS[index]
+        single = dgfem.config_mesh(cfg)
+        self.copies, self.E_sys = copies, single.n_elements
+        self.nnzb_sys = single.n_elements + 2 * single.n_interior_edges
+        r = replicated_raw(single.raw(), copies)
+        union = dgfem.build_mesh(r["nodes"], r["elements"], r["dirichlet"], r["neumann"])
+        super().__init__(index, device, mesh=union)
+
+    def system(self, b: int):
+        out = self.outputs()[0]
+        E, nb = self.E_sys, self.nnzb_sys
+        rp = out.row_ptr[b * E:(b + 1) * E + 1] - b * nb
+        return dgfem.BsrSystem(rp, out.col[b * nb:(b + 1) * nb] - b * E,
+                               out.val[b * nb:(b + 1) * nb], out.rhs[b * E:(b + 1) * E],
+                               out.block_dim)
+
+
+def capture_graph(run: ConfigRun, n: int):
+    """A CUDA graph of `n` consecutive steps of `run` (its launches captured on a side stream;
+    replay() re-issues them with one launch call).  The plan must already be bound."""
+    import torch
+    side = torch.cuda.Stream(run.device)
+    side.wait_stream(torch.cuda.current_stream(run.device))
+    with torch.cuda.stream(side):
+        run.step(side)          # warm (first-launch attribute setup happens outside capture)
+    torch.cuda.current_stream(run.device).wait_stream(side)
+    torch.cuda.synchronize(run.device)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=side):
+        for _ in range(n):
+            run.step(side)
+    return g

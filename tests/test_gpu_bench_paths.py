@@ -75,3 +75,42 @@ def test_config2_single_assembly_path(oracle):
     run = workload.ConfigRun(2, batch=False)
     assert not run.batched
     _check_run(oracle, run, 2102)
+
+
+def test_batched_c1_systems_equal_single_assembly(oracle):
+    """bench.py --op c1-throughput: 512 copies of config 1 in one launch.  Every copy's system
+    equals the single config-1 assembly bit for bit (offsets removed), and that one matches
+    the oracle in full."""
+    import torch
+    single = workload.ConfigRun(1)
+    stream = torch.cuda.current_stream(0)
+    single.step(stream)
+    batch = workload.BatchedSystemsRun(1, copies=512)
+    batch.step(stream)
+    torch.cuda.synchronize()
+    batch.check_status(stream)
+    s = single.outputs()[0]
+    for b in (0, 1, 255, 511):
+        sb = batch.system(b)
+        for x, y in zip((s.row_ptr, s.col, s.val, s.rhs), (sb.row_ptr, sb.col, sb.val, sb.rhs)):
+            assert torch.equal(x, y)
+    o = oracle.assemble(single.mesh.arrays(), single.ref.tables(), single.spec.c, single.params[0])
+    compare_system((s.row_ptr.cpu().numpy(), s.col.cpu().numpy(), s.val.cpu().numpy(),
+                    s.rhs.cpu().numpy()), o)
+
+
+def test_c1_graph_replay_equals_single_launch():
+    """The CUDA-graph replay of config 1's launch (bench.py --op c1-throughput) writes the same
+    bits as the eager launch."""
+    import torch
+    run = workload.ConfigRun(1)
+    stream = torch.cuda.current_stream(0)
+    run.step(stream)
+    torch.cuda.synchronize()
+    ref = [t.clone() for t in (run.outputs()[0].val, run.outputs()[0].rhs)]
+    run.outputs()[0].val.fill_(0.0)
+    g = workload.capture_graph(run, 4)
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(ref[0], run.outputs()[0].val)
+    assert torch.equal(ref[1], run.outputs()[0].rhs)
