@@ -177,7 +177,10 @@ enum dgb_function_mode {
   DGB_MODE_VALUE = 0,   /* u                                                                 */
   DGB_MODE_SOURCE = 1,  /* q0 u - q1 lap(u) + q2 du/dx + q3 du/dy  (manufactured source with
                            constant alpha = q0, eps = q1, b = (q2, q3))                      */
-  DGB_MODE_FLUX_X = 2   /* q1 du/dx  (conormal flux through x = const sides)                 */
+  DGB_MODE_FLUX_X = 2,  /* q1 du/dx  (conormal flux through x = const sides)                 */
+  DGB_MODE_SOURCE_SQUARE = 3 /* the SOURCE value + u^2: the manufactured source of a problem
+                           with the nonlinear reaction r(u) = u^2 (the reference's
+                           "paper-boundary-layer", problems.cpp:113-118)                     */
 };
 typedef struct dgb_scalar_field {
   int32_t kind;               /* dgb_field_kind  */

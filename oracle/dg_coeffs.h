@@ -81,6 +81,8 @@ static inline double dgc_scalar_point(const dgb_scalar_field* f, double x, doubl
       return u;
     case DGB_MODE_SOURCE:
       return f->q[0] * u - f->q[1] * lap + f->q[2] * ux + f->q[3] * uy;
+    case DGB_MODE_SOURCE_SQUARE: /* problems.cpp:113-118: f += val * val */
+      return (f->q[0] * u - f->q[1] * lap + f->q[2] * ux + f->q[3] * uy) + u * u;
     case DGB_MODE_FLUX_X:
       return f->q[1] * ux;
     default:

@@ -15,7 +15,7 @@ LIB_PATH = os.path.join(_HERE, "libdgfem_b200.so")
 EDGE_INTERIOR, EDGE_DIRICHLET, EDGE_NEUMANN = 0, 1, 2
 FIELD_CONSTANT, FIELD_PER_ELEMENT, FIELD_FUNCTION = 0, 1, 2
 FN_SIN_SIN, FN_TANH_LAYER, FN_GAUSSIAN, FN_AFFINE, FN_STEP_Y = 1, 2, 3, 4, 5
-MODE_VALUE, MODE_SOURCE, MODE_FLUX_X = 0, 1, 2
+MODE_VALUE, MODE_SOURCE, MODE_FLUX_X, MODE_SOURCE_SQUARE = 0, 1, 2, 3
 VEC_CONSTANT, VEC_AFFINE, VEC_TRIG = 0, 1, 2
 SIPG, NIPG, IIPG = 0, 1, 2
 INFLOW_ERROR, INFLOW_DROP = 0, 1

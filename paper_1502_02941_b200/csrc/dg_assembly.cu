@@ -180,6 +180,7 @@ __device__ __noinline__ double scalar_function(int fn, int mode, double p0, doub
   switch (mode) {
     case DGB_MODE_VALUE: return u;
     case DGB_MODE_SOURCE: return q0 * u - q1 * lap + q2 * ux + q3 * uy;
+    case DGB_MODE_SOURCE_SQUARE: return (q0 * u - q1 * lap + q2 * ux + q3 * uy) + u * u;
     case DGB_MODE_FLUX_X: return q1 * ux;
     default: return nan("");
   }
@@ -199,6 +200,7 @@ __device__ __forceinline__ double scalar_point_inline(const dgb_scalar_field& f,
   switch (f.mode) {
     case DGB_MODE_VALUE: return u;
     case DGB_MODE_SOURCE: return f.q[0] * u - f.q[1] * lap + f.q[2] * ux + f.q[3] * uy;
+    case DGB_MODE_SOURCE_SQUARE: return (f.q[0] * u - f.q[1] * lap + f.q[2] * ux + f.q[3] * uy) + u * u;
     case DGB_MODE_FLUX_X: return f.q[1] * ux;
     default: return nan("");
   }

@@ -79,6 +79,7 @@ class ProblemSpec:
     per_element: dict = field(default_factory=dict)  # field name -> np.ndarray [n_elements]
     neumann_sides: int = 0  # unit-square sides tagged Neumann (mesh.hpp:74 neumann_on)
     exact: tuple | None = None  # (fn, p) of the exact solution, when known
+    reaction: int | None = None  # nonlinear reaction r(u) (capi.REACTION_*), when the problem has one
 
     def set_per_element(self, name: str, values: np.ndarray) -> None:
         values = np.ascontiguousarray(values, dtype=np.float64)
@@ -126,6 +127,17 @@ def registry_get(name: str) -> ProblemSpec:
         return make_problem(name, eps, vec_constant(b1, b2), 1.0,
                             source_of(*u, alpha=1.0, eps=eps, bx=b1, by=b2), function(*u),
                             exact=u)
+    if name == "paper-boundary-layer":
+        # problems.cpp:78-134 (nonlinear = true): the layer above with r(u) = u^2 (r' = 2u) and
+        # f += u^2; the reaction is applied by the Newton driver (ProblemSpec.reaction)
+        eps = 1e-6
+        b1, b2 = 1.0 / math.sqrt(5.0), 2.0 / math.sqrt(5.0)
+        u = (capi.FN_TANH_LAYER, (2.0, -1.0, -0.25, math.sqrt(5.0 * eps)))
+        spec = make_problem(name, eps, vec_constant(b1, b2), 1.0,
+                            function(*u, mode=capi.MODE_SOURCE_SQUARE, q=(1.0, eps, b1, b2)),
+                            function(*u), exact=u)
+        spec.reaction = capi.REACTION_SQUARE
+        return spec
     if name == "pure-advection-patch":
         # problems.cpp:182-193
         return make_problem(name, 1e-10, vec_constant(1.0, 0.0), 0.0, constant(0.0),

@@ -10,6 +10,7 @@ from paper_1502_02941_b200 import capi, dgfem, problems
 pytestmark = pytest.mark.gpu
 
 REGISTRY = ["smooth-sine", "smooth-sine-mixed", "poly-exact", "paper-boundary-layer-linear",
+            "paper-boundary-layer",
             "pure-advection-patch"]
 
 
@@ -133,3 +134,25 @@ def test_every_kernel_per_element_fields(oracle, degree, quad_order, vel):
         g = run_gpu(mesh, ref, spec, params)
         o = oracle.assemble(mesh.arrays(), ref.tables(), spec.c, params)
         compare_system(g, o)
+
+
+@pytest.mark.parametrize("level,degree", [(3, 1), (3, 2), (4, 1)])
+def test_reference_benchmark_cases(oracle, level, degree):
+    """The reference's own assembly benchmark (bench/assembly_bench.cpp:31-48, configure :79-93):
+    unit_square_mesh refined `level` times, build_reference(k), paper-boundary-layer (with its
+    f += u^2 source), SIPG -- the mesh built and refined on the device, the assembly through the
+    GPU path, compared with the oracle on the same arrays."""
+    import torch
+    from test_solve_oracle import UNIT_SQUARE
+    raw = UNIT_SQUARE
+    m = dgfem.device_build_mesh(raw["nodes"], raw["elements"], raw["dirichlet"], raw["neumann"])
+    for _ in range(level):
+        m = m.refine()
+    spec = problems.registry_get("paper-boundary-layer")
+    ref = dgfem.ReferenceElement(degree)
+    params = dgfem.set_parameters(capi.SIPG, degree)
+    plan = dgfem.Plan(ref.view)
+    out = plan.assemble(m, dgfem.DeviceProblem(spec), params, plan.allocate(m))
+    torch.cuda.synchronize()
+    g = (out.row_ptr.cpu().numpy(), out.col.cpu().numpy(), out.val.cpu().numpy(), out.rhs.cpu().numpy())
+    compare_system(g, oracle.assemble(m.arrays(), ref.tables(), spec.c, params))
