@@ -98,6 +98,7 @@ struct Params2 {
   int32_t evict_first;           // L2 evict-first hint on the output stream
   int32_t ablate;                // profiling diagnostics only (wrong results): see dg_assembly.cu
   int32_t load_hints;            // L2 hints on loads: gathers evict-last, streamed records evict-first
+  const double* tr_src;          // the plan's neighbour trace table (the kernel's `tr`), or null
   int32_t n_batch;
   MethodOut bt[kMaxBatch];
   dgb_problem prob;
@@ -504,6 +505,9 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
   constexpr int SS = SM::SS, NF = SM::NF;
   extern __shared__ double smem[];
   double* tr = smem;  // [3][NQE][3][NL]: phi, w d0 phi, w d1 phi of each local edge's points
+  if (P.tr_src) {     // built once per plan (dgb_plan_create), the same values as below
+    for (int i = threadIdx.x; i < 3 * NQE * 3 * NL; i += blockDim.x) tr[i] = __ldg(P.tr_src + i);
+  } else
   for (int i = threadIdx.x; i < 3 * NQE * 3 * NL; i += blockDim.x) {
     const int j = i % NL, c = (i / NL) % 3, p = (i / (3 * NL)) % NQE, l = i / (3 * NL * NQE);
     // gradients rotated to the neighbour's (opposite, b, a) vertex order (p1_tables)
@@ -1173,26 +1177,23 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
             for (int ks = 0; ks < KO; ++ks) at[u][ks] = 0.0;
             if (tb + u < te) tile_rows(tb + u, at[u], bt_[u]);
           }
-          constexpr int PF = 3;
+          // a ring of PF register buffers, the n-tile loop fully unrolled so the ring needs no
+          // moves: the L2 latency of a fragment is covered by PF n-tiles of products
+          constexpr int PF = 8;
           double bq[PF][KO];
 #pragma unroll
           for (int u = 0; u < PF; ++u) {
 #pragma unroll
             for (int ks = 0; ks < KO; ++ks) bq[u][ks] = __ldg(fr + (ks * SM::kNT + u) * 32);
           }
-#pragma unroll 1
+#pragma unroll
           for (int nt = 0; nt < SM::kNT; ++nt) {
             double bk[KO];
 #pragma unroll
-            for (int ks = 0; ks < KO; ++ks) bk[ks] = bq[0][ks];
-#pragma unroll
-            for (int u = 0; u + 1 < PF; ++u) {
-#pragma unroll
-              for (int ks = 0; ks < KO; ++ks) bq[u][ks] = bq[u + 1][ks];
-            }
+            for (int ks = 0; ks < KO; ++ks) bk[ks] = bq[nt % PF][ks];
             if (nt + PF < SM::kNT) {
 #pragma unroll
-              for (int ks = 0; ks < KO; ++ks) bq[PF - 1][ks] = __ldg(fr + (ks * SM::kNT + nt + PF) * 32);
+              for (int ks = 0; ks < KO; ++ks) bq[nt % PF][ks] = __ldg(fr + (ks * SM::kNT + nt + PF) * 32);
             }
             const int n0 = 8 * nt + 2 * t;
 #pragma unroll

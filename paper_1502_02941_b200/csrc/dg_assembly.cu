@@ -1034,6 +1034,10 @@ struct dgb_plan {
   // nonlinear reaction Jacobian: Phi_q,(i,j) = phi_qj phi_qi as DMMA B fragments [ks][nt][lane]
   double* d_nlfrag = nullptr;
   int nl_ks = 0;
+  // neighbour trace table of the block-row kernels (phi, w d0 phi, w d1 phi of each local
+  // edge's points, gradients rotated to the neighbour's (opposite, b, a) order), built once
+  // per plan instead of by every CTA
+  double* d_trace = nullptr;
 };
 
 namespace {
@@ -1128,6 +1132,9 @@ void launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_prob
   P.n_elements = mesh->n_elements;
   P.row_begin = out_row_begin;
   P.row_end = out_row_end;
+  // P4 only: measured -1.5% on config 5, but +25% on config 3 (whose CTAs start faster from the
+  // constant bank than from an L2 round trip)
+  P.tr_src = NL == 15 ? plan->d_trace : nullptr;
   P.drop_neumann = params->neumann_inflow == DGB_INFLOW_DROP;
   // auto (-1): evict-first output for odd N2 only (measured, profiles/NOTES.md: P4's 8-byte
   // fragment stores gain 33%; P2's 16-byte fragment stores lose 5%: the L2 must hold a block
@@ -1782,6 +1789,25 @@ int dgb_plan_create(const dgb_reference_tables* tables, int32_t device, dgb_plan
       cuda_check(cudaMalloc(&p->d_tens, h.size() * sizeof(double)), "cudaMalloc(tensors)");
       cuda_check(cudaMemcpy(p->d_tens, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice),
                  "cudaMemcpy(tensors)");
+      {
+        const int nl = p->nl, ne = p->nqe, n = 3 * ne * 3 * nl;
+        const dgb::Layout& V = p->L;
+        std::vector<double> trh(n);
+        for (int i = 0; i < n; ++i) {
+          const int j = i % nl, c = (i / nl) % 3, q = (i / (3 * nl)) % ne, l = i / (3 * nl * ne);
+          const int lp = l * ne + q;
+          const double w = h[V.EW + q];
+          const double g0 = w * h[V.EDPHI + (lp * 2) * nl + j];
+          const double g1 = w * h[V.EDPHI + (lp * 2 + 1) * nl + j];
+          trh[i] = c == 0 ? h[V.EPHI + lp * nl + j]
+                   : l == 0 ? (c == 1 ? g0 : g1)
+                   : l == 1 ? (c == 1 ? g1 - g0 : -g0)
+                            : (c == 1 ? -g1 : g0 - g1);
+        }
+        cuda_check(cudaMalloc(&p->d_trace, n * sizeof(double)), "cudaMalloc(trace)");
+        cuda_check(cudaMemcpy(p->d_trace, trh.data(), n * sizeof(double), cudaMemcpyHostToDevice),
+                   "cudaMemcpy(trace)");
+      }
       cuda_check(cudaMalloc(&p->d_err, sizeof(unsigned long long)), "cudaMalloc(err)");
       {
         int max_persist = 0, max_window = 0;
@@ -1813,6 +1839,7 @@ void dgb_plan_destroy(dgb_plan* p) {
   cudaFree(p->d_adj);
   for (auto& c : p->bfrag_cache) cudaFree(c.second);
   cudaFree(p->d_nlfrag);
+  cudaFree(p->d_trace);
   if (prev >= 0) cudaSetDevice(prev);
   delete p;
 }
