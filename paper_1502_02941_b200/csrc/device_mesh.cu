@@ -18,6 +18,8 @@
 #include <algorithm>
 #include <cstdint>
 #include <memory>
+#include <mutex>
+#include <set>
 #include <vector>
 
 #include <cub/device/device_radix_sort.cuh>
@@ -230,17 +232,42 @@ __global__ void refine_boundary_kernel(const uint8_t* __restrict__ kind, const i
   pairs[2 * slot + 3] = edges[2 * u + 1];
 }
 
+// Stream-ordered allocations from the device's default pool, kept cached (release threshold
+// raised once per device): a refine chain allocates and frees per level, and plain
+// cudaMalloc / cudaFree made its wall time vary 47 ms .. 0.39 s from run to run.
+void keep_mesh_pool_cached() {
+  static std::mutex mu;
+  static std::set<int> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  if (!done.insert(dev).second) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    unsigned long long keep = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+}
+template <typename T>
+void pool_alloc(T** x, size_t bytes, cudaStream_t s) {
+  keep_mesh_pool_cached();
+  cuda_check(cudaMallocAsync(reinterpret_cast<void**>(x), std::max<size_t>(bytes, 1), s),
+             "cudaMallocAsync(mesh)");
+}
+
 struct Tmp {
+  cudaStream_t s;
   std::vector<void*> p;
+  explicit Tmp(cudaStream_t st) : s(st) {}
   ~Tmp() {
-    for (void* x : p) cudaFree(x);
+    for (void* x : p) cudaFreeAsync(x, s);
   }
   template <typename T>
   T* alloc(size_t n) {
-    void* x = nullptr;
-    cuda_check(cudaMalloc(&x, std::max<size_t>(n, 1) * sizeof(T)), "cudaMalloc(mesh)");
+    T* x = nullptr;
+    pool_alloc(&x, n * sizeof(T), s);
     p.push_back(x);
-    return static_cast<T*>(x);
+    return x;
   }
 };
 
@@ -253,7 +280,7 @@ T read1(const T* d, cudaStream_t s) {
 }
 
 // Builds from DEVICE arrays (nodes [2n], elements [3E], pairs: dirichlet then neumann [2(nd+nn)]).
-// Takes ownership of `nodes` (a cudaMalloc'd copy).
+// Takes ownership of `nodes` (a pool allocation on `s`).
 dgb_device_mesh* build(double* nodes, int n_nodes, const int32_t* elements, int E,
                        const int32_t* pairs, int n_dir, int n_neu, int device, cudaStream_t s) {
   std::unique_ptr<dgb_device_mesh, void (*)(dgb_device_mesh*)> owner(new dgb_device_mesh(),
@@ -267,11 +294,11 @@ dgb_device_mesh* build(double* nodes, int n_nodes, const int32_t* elements, int 
     throw dgb::Error(status, msg, detail);
   };
   {
-    Tmp t;
+    Tmp t(s);
     unsigned long long* words = t.alloc<unsigned long long>(8);
     cuda_check(cudaMemsetAsync(words, 0xFF, 8 * sizeof(unsigned long long), s), "memset");
     cuda_check(cudaMemsetAsync(words + 7, 0, sizeof(unsigned long long), s), "memset");
-    cuda_check(cudaMalloc(&m->elements, std::max<size_t>(3ull * E, 1) * sizeof(int32_t)), "cudaMalloc");
+    pool_alloc(&m->elements, std::max<size_t>(3ull * E, 1) * sizeof(int32_t), s);
     if (E > 0) {
       validate_orient_kernel<<<blocks(E), kT, 0, s>>>(nodes, elements, E, n_nodes, m->elements, words);
       cuda_check(cudaGetLastError(), "validate_orient_kernel");
@@ -302,10 +329,10 @@ dgb_device_mesh* build(double* nodes, int n_nodes, const int32_t* elements, int 
       m->n_edges = read1(uid + M - 1, s);
     }
     const int NE = m->n_edges;
-    cuda_check(cudaMalloc(&m->edges, std::max<size_t>(2ull * NE, 1) * sizeof(int32_t)), "cudaMalloc");
-    cuda_check(cudaMalloc(&m->edge_elements, std::max<size_t>(2ull * NE, 1) * sizeof(int32_t)), "cudaMalloc");
-    cuda_check(cudaMalloc(&m->element_edges, std::max<size_t>(3ull * E, 1) * sizeof(int32_t)), "cudaMalloc");
-    cuda_check(cudaMalloc(&m->edge_kind, std::max<size_t>(NE, 1)), "cudaMalloc");
+    pool_alloc(&m->edges, std::max<size_t>(2ull * NE, 1) * sizeof(int32_t), s);
+    pool_alloc(&m->edge_elements, std::max<size_t>(2ull * NE, 1) * sizeof(int32_t), s);
+    pool_alloc(&m->element_edges, std::max<size_t>(3ull * E, 1) * sizeof(int32_t), s);
+    pool_alloc(&m->edge_kind, std::max<size_t>(NE, 1), s);
     cuda_check(cudaMemsetAsync(m->edge_kind, DGB_EDGE_INTERIOR, std::max<size_t>(NE, 1), s), "memset");
     unsigned long long* ukeys = t.alloc<unsigned long long>(NE);
     if (M > 0) {
@@ -383,9 +410,9 @@ int dgb_device_mesh_build(const double* nodes_xy, int32_t n_nodes, const int32_t
     Guard g(device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     double* nodes = nullptr;
-    cuda_check(cudaMalloc(&nodes, std::max<size_t>(2ull * n_nodes, 1) * sizeof(double)), "cudaMalloc");
+    pool_alloc(&nodes, std::max<size_t>(2ull * n_nodes, 1) * sizeof(double), s);
     cuda_check(cudaMemcpyAsync(nodes, nodes_xy, 2ull * n_nodes * sizeof(double), cudaMemcpyDefault, s), "copy(nodes)");
-    Tmp t;
+    Tmp t(s);
     int32_t* pairs = t.alloc<int32_t>(2ull * (n_dirichlet + n_neumann));
     if (n_dirichlet) cuda_check(cudaMemcpyAsync(pairs, dirichlet_pairs, 8ull * n_dirichlet, cudaMemcpyDefault, s), "copy");
     if (n_neumann) cuda_check(cudaMemcpyAsync(pairs + 2 * n_dirichlet, neumann_pairs, 8ull * n_neumann, cudaMemcpyDefault, s), "copy");
@@ -406,10 +433,10 @@ int dgb_device_mesh_refine(const dgb_device_mesh* in, dgb_device_mesh** out, voi
       throw dgb::Error(DGB_STATUS_INVALID_ARGUMENT, "refined mesh exceeds 32-bit indices");
     }
     double* nodes = nullptr;
-    cuda_check(cudaMalloc(&nodes, std::max<size_t>(2ull * (NN + NE), 1) * sizeof(double)), "cudaMalloc");
+    pool_alloc(&nodes, std::max<size_t>(2ull * (NN + NE), 1) * sizeof(double), s);
     const long long nmax = std::max<long long>(2LL * NN, NE);
     if (nmax > 0) refine_nodes_kernel<<<blocks(nmax), kT, 0, s>>>(in->nodes, NN, in->edges, NE, nodes);
-    Tmp t;
+    Tmp t(s);
     int32_t* el = t.alloc<int32_t>(12ull * E);
     if (E > 0) refine_elements_kernel<<<blocks(E), kT, 0, s>>>(in->elements, in->element_edges, E, NN, el);
     int32_t* fd = t.alloc<int32_t>(NE + 1);

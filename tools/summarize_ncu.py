@@ -2,10 +2,12 @@
 
     python tools/summarize_ncu.py [round_tag]
 
-Reads gpurun_out/prof_c{2,3,4}.ncu-rep (ncu --set full of the block-row kernel) and
-gpurun_out/launches_c2.csv (per-launch gpu__time_duration list), writes
-profiles/ncu_summary.json (bench.py reads dram_bytes_per_launch for roofline.traffic),
-profiles/ncu_<tag>_c<cfg>.txt and profiles/launches_<tag>_c2.csv.
+Reads gpurun_out/<tag>_c{1..5}.ncu-rep (ncu --set full of the block-row kernel; round 1 named
+them prof_c*), gpurun_out/<tag>_spmv.ncu-rep (the BSR SpMV on config 4) and
+gpurun_out/launches_<tag>_c<L>.csv (per-launch gpu__time_duration list of the headline command,
+L = $LAUNCH_CFG, default 4), writes profiles/ncu_summary.json (bench.py reads
+dram_bytes_per_launch for roofline.traffic), profiles/ncu_<tag>_c<cfg>.txt,
+profiles/ncu_<tag>_spmv.txt and profiles/launches_<tag>_c<L>.csv.
 """
 from __future__ import annotations
 
@@ -100,6 +102,8 @@ def launch_shares(path: str) -> dict:
         name = r[ki]
         short = ("assemble_kernel" if "assemble_" in name else
                  "count_blocks_kernel" if "count_blocks" in name else
+                 "adjacency_kernel" if "adjacency" in name else
+                 "l2_flush_fill (outside the timed events)" if "FillFunctor" in name else
                  "cub_scan" if "cub" in name.lower() or "Scan" in name else name[:40])
         try:
             v = float(r[vi].replace(",", ""))
@@ -117,7 +121,9 @@ def main():
     summary_path = os.path.join(PROF, "ncu_summary.json")
     summary = json.load(open(summary_path)) if os.path.exists(summary_path) else {}
     for cfg in (1, 2, 3, 4, 5):
-        rep = os.path.join(OUT, f"prof_c{cfg}.ncu-rep")
+        rep = os.path.join(OUT, f"{tag}_c{cfg}.ncu-rep")
+        if not os.path.exists(rep):
+            rep = os.path.join(OUT, f"prof_c{cfg}.ncu-rep")
         if not os.path.exists(rep):
             continue
         s = summarize(rep, cfg)
@@ -125,10 +131,23 @@ def main():
         summary[f"config{cfg}"] = s
         with open(os.path.join(PROF, f"ncu_{tag}_c{cfg}.txt"), "w") as f:
             f.write(json.dumps(s, indent=2) + "\n")
-    lc = os.path.join(OUT, "launches_c2.csv")
+    rep = os.path.join(OUT, f"{tag}_spmv.ncu-rep")
+    if os.path.exists(rep):
+        s = summarize(rep, 4)
+        s["kernel"] = "BSR SpMV (config 4 matrix)"
+        s["assemblies_per_launch"] = None
+        s["warp_instructions_per_row"] = s.pop("warp_instructions_per_element")
+        s["round"] = tag
+        summary["spmv_config4"] = s
+        with open(os.path.join(PROF, f"ncu_{tag}_spmv.txt"), "w") as f:
+            f.write(json.dumps(s, indent=2) + "\n")
+    lcfg = int(os.environ.get("LAUNCH_CFG", "4"))
+    lc = os.path.join(OUT, f"launches_{tag}_c{lcfg}.csv")
+    if not os.path.exists(lc):
+        lc = os.path.join(OUT, f"launches_c{lcfg}.csv")
     if os.path.exists(lc):
-        shutil.copy(lc, os.path.join(PROF, f"launches_{tag}_c2.csv"))
-        summary["launch_shares_c2"] = launch_shares(lc)
+        shutil.copy(lc, os.path.join(PROF, f"launches_{tag}_c{lcfg}.csv"))
+        summary[f"launch_shares_c{lcfg}"] = launch_shares(lc)
     with open(summary_path, "w") as f:
         json.dump(summary, f, indent=2)
     print(json.dumps({k: (v.get("dram_bytes_per_launch"), v.get("warp_instructions_per_element"),
