@@ -276,6 +276,19 @@ void dgb_plan_destroy(dgb_plan* plan);
 int dgb_assemble(dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_problem* problem,
                  const dgb_params* params, dgb_bsr* out, double* rhs, void* stream);
 
+/* Per-term assembly: the reference's assemble_diffusion / assemble_convection /
+ * assemble_reaction (assembly.hpp:72-95, assembly.cpp:512-641) as matrices.  `terms` is a mask
+ * of dgb_term; K gets exactly the selected terms' sum in K's full pattern: the coefficients of
+ * the other terms are zeroed (eps = 0 removes every diffusion volume and face term, b = 0 every
+ * transport and upwind term, alpha = 0 the reaction), so their entries are exact zeros and, e.g.,
+ * DGB_TERM_DIFFUSION gives the reference's D on its own pattern.  F is the load vector of that
+ * modified problem (not the reference's per-term F_D / F_C, which assemble_all discards).
+ * Otherwise as dgb_assemble. */
+enum dgb_term { DGB_TERM_DIFFUSION = 1, DGB_TERM_CONVECTION = 2, DGB_TERM_REACTION = 4, DGB_TERM_ALL = 7 };
+int dgb_assemble_terms(dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_problem* problem,
+                       const dgb_params* params, int32_t terms, dgb_bsr* out, double* rhs,
+                       void* stream);
+
 /* Shard form of dgb_assemble: block rows [row_begin, row_end) only.  `out`
  * holds those rows (row_ptr relative to the shard, starting at 0; block columns global) and
  * rhs their F slices; out->nnzb from dgb_count_blocks_host.  The mesh arrays are the full mesh

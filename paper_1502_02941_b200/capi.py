@@ -91,6 +91,7 @@ class Reaction(C.Structure):
 
 
 REACTION_ZERO, REACTION_LINEAR, REACTION_SQUARE, REACTION_CUBIC = 0, 1, 2, 3
+TERM_DIFFUSION, TERM_CONVECTION, TERM_REACTION, TERM_ALL = 1, 2, 4, 7
 
 
 class SolveOptions(C.Structure):
@@ -141,6 +142,8 @@ def _declare(lib: C.CDLL) -> C.CDLL:
         "dgb_plan_create": (C.c_int, [P(ReferenceTables), C.c_int32, P(vp)]),
         "dgb_plan_destroy": (None, [vp]),
         "dgb_assemble": (C.c_int, [vp, P(MeshArrays), P(Problem), P(Params), P(Bsr), vp, vp]),
+        "dgb_assemble_terms": (C.c_int, [vp, P(MeshArrays), P(Problem), P(Params), C.c_int32, P(Bsr),
+                                         vp, vp]),
         "dgb_plan_status": (C.c_int, [vp, vp]),
         "dgb_plan_set_kernel_events": (C.c_int, [vp, vp, vp]),
         "dgb_plan_bind_mesh": (C.c_int, [vp, P(MeshArrays), C.c_int32, C.c_int32, vp]),
@@ -187,7 +190,7 @@ EXPORTED_SYMBOLS = [
     "dgb_mesh_build", "dgb_mesh_unit_square", "dgb_mesh_view", "dgb_mesh_raw",
     "dgb_mesh_free", "dgb_reference_create", "dgb_reference_view", "dgb_reference_free",
     "dgb_set_parameters", "dgb_bsr_nnzb", "dgb_plan_create", "dgb_plan_destroy",
-    "dgb_assemble", "dgb_plan_status", "dgb_plan_set_kernel_events",
+    "dgb_assemble", "dgb_assemble_terms", "dgb_plan_status", "dgb_plan_set_kernel_events",
     "dgb_plan_bind_mesh", "dgb_plan_unbind_mesh", "dgb_plan_launch_count", "dgb_plan_set_option", "dgb_spmv", "dgb_assemble_all_host",
     "dgb_mesh_rectangle", "dgb_assemble_rows", "dgb_count_blocks_host",
     "dgb_assemble_nonlinear", "dgb_assemble_nonlinear_host",

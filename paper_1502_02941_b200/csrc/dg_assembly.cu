@@ -2027,6 +2027,28 @@ int dgb_assemble(dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_problem*
                            stream);
 }
 
+int dgb_assemble_terms(dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_problem* problem,
+                       const dgb_params* params, int32_t terms, dgb_bsr* out, double* rhs,
+                       void* stream) {
+  if (!problem) return dgb::record_error(DGB_STATUS_INVALID_ARGUMENT, "null argument", -1);
+  if (terms < 0 || terms > DGB_TERM_ALL) {
+    return dgb::record_error(DGB_STATUS_INVALID_ARGUMENT, "InvalidArgument: unknown term mask", terms);
+  }
+  dgb_problem p = *problem;
+  auto zero_scalar = [](dgb_scalar_field& f) {
+    std::memset(&f, 0, sizeof f);
+    f.kind = DGB_FIELD_CONSTANT;
+    f.value = 0.0;
+  };
+  if (!(terms & DGB_TERM_DIFFUSION)) zero_scalar(p.diffusion);
+  if (!(terms & DGB_TERM_REACTION)) zero_scalar(p.linear_reaction);
+  if (!(terms & DGB_TERM_CONVECTION)) {
+    std::memset(&p.advection, 0, sizeof p.advection);
+    p.advection.kind = DGB_VEC_CONSTANT;
+  }
+  return dgb_assemble(plan, mesh, &p, params, out, rhs, stream);
+}
+
 int64_t dgb_count_blocks_host(const dgb_mesh_arrays* mesh, int32_t row_begin, int32_t row_end) {
   if (!mesh || row_begin < 0 || row_end > mesh->n_elements || row_begin > row_end) return -1;
   int64_t n = 0;

@@ -307,6 +307,22 @@ class Plan:
             _check(self._lib.dgb_plan_status(self._h, C.c_void_p(handle)))
         return out
 
+    def assemble_terms(self, dmesh: DeviceMesh, dproblem: DeviceProblem, params: Params,
+                       terms: int, out: BsrSystem, stream=None, check: bool = True) -> BsrSystem:
+        """dgb_assemble_terms: K of the selected terms only (capi.TERM_* mask), e.g. the
+        reference's `assemble_diffusion(...).D` for capi.TERM_DIFFUSION."""
+        import torch
+        if stream is None:
+            stream = torch.cuda.current_stream(self.device)
+        handle = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+        b = out.struct()
+        _check(self._lib.dgb_assemble_terms(self._h, C.byref(dmesh.view), C.byref(dproblem.c),
+                                            C.byref(params), terms, C.byref(b),
+                                            out.rhs.data_ptr(), C.c_void_p(handle)))
+        if check:
+            _check(self._lib.dgb_plan_status(self._h, C.c_void_p(handle)))
+        return out
+
     def assemble_nonlinear(self, dmesh: DeviceMesh, coef, reaction: int, h=None, hj=None,
                            stream=None):
         """dgb_assemble_nonlinear on device tensors: H [E, nl] and the block-diagonal HJ
