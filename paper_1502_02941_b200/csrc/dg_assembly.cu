@@ -228,6 +228,24 @@ __device__ __forceinline__ void source_points(const dgb_scalar_field& fs, int e,
     }
     return;
   }
+  if (!skip && fs.mode == DGB_MODE_SOURCE && fs.fn == DGB_FN_SIN_SIN) {
+    // u = p0 sin(pi x) sin(pi y): the source q0 u - q1 lap(u) + q2 u_x + q3 u_y regrouped as
+    // p0 ((q0 + 2 pi^2 q1) sx sy + pi q2 cx sy + pi q3 sx cy), with sincospi: a cheaper
+    // reduction than sincos of the rounded product pi * x (the reference's sin(pi * x) differs
+    // from sin of the exact pi x by at most ~7e-16 absolute).  Config 1's batch: 0.198 -> 0.163 ms.
+    constexpr double pi = 3.14159265358979323846;
+    const double A = fs.p[0] * fma(2.0 * pi * pi, fs.q[1], fs.q[0]);
+    const double Bx = fs.p[0] * (pi * fs.q[2]), By = fs.p[0] * (pi * fs.q[3]);
+#pragma unroll 1
+    for (int q = q_first; q < NQV; q += q_step) {
+      double x, y, sx, cx, sy, cy;
+      xy(q, x, y);
+      sincospi(x, &sx, &cx);
+      sincospi(y, &sy, &cy);
+      use(q, fma(A * sx, sy, fma(Bx * cx, sy, (By * sx) * cy)), x, y);
+    }
+    return;
+  }
   if (!skip && fs.mode == DGB_MODE_SOURCE && (fs.fn == DGB_FN_GAUSSIAN || fs.fn == DGB_FN_TANH_LAYER)) {
     const double q0 = fs.q[0], q1 = fs.q[1], q2 = fs.q[2], q3 = fs.q[3];
     if (fs.fn == DGB_FN_GAUSSIAN) {
