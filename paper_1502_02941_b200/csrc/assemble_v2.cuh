@@ -615,8 +615,12 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_kernel(
 #pragma unroll
           for (int i = 0; i < NL; ++i) F[i] = fma(c, P.t.x[L::PHI + q * NL + i], F[i]);
           if constexpr (TRIG) {
-            double bx, by;
-            velocity_k<BK>(bf, px, py, bx, by);
+            // volume points only scale the transport terms (no upwind decision is taken here):
+            // b = (cos(w0 y), sin(w1 x)) through cospi / sinpi of (w / pi) y -- a cheaper
+            // reduction than cos / sin of the rounded product w y, equal to ~1e-15 absolute.
+            // Edge points keep the reference's expressions (they decide the upwind side).
+            constexpr double kInvPi = 0.318309886183790671538;
+            const double bx = cospi((bf.p[0] * kInvPi) * py), by = sinpi((bf.p[1] * kInvPi) * px);
             if constexpr (SM::kMma) {  // T-form: the transport coefficients are A-operand rows
               sk[(4 + 2 * q) * SM::kCT + lane] = dw * (G00 * bx + G10 * by);
               sk[(4 + 2 * q + 1) * SM::kCT + lane] = dw * (G01 * bx + G11 * by);
