@@ -47,9 +47,9 @@ def parse_args():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", type=int, default=4,
+    ap.add_argument("--config", type=int, default=None,
                     help="BASELINE.json config (default 4: the largest single-GPU config, "
-                         "8.4M triangles)")
+                         "8.4M triangles; --op solve defaults to config 1)")
     ap.add_argument("--secondary", default="2,2s,3,5,1",
                     help="assembly op, N = 1: also time these configs on the same box "
                          "(device-resident; 'Cs' = one launch per method instead of the fused "
@@ -1183,6 +1183,8 @@ def l2_policy_text(l2: int) -> str:
 
 def main():
     args = parse_args()
+    if args.config is None:
+        args.config = 1 if args.op == "solve" else 4
     world, rank, local = dist_setup(args)
     if args.op == "mesh":
         if rank == 0:
