@@ -158,3 +158,14 @@ def test_orthonormal_basis_mass_is_identity():
         phi = t["phi"].reshape(-1, nl)
         M = (phi * t["vol_w"][:, None]).T @ phi
         assert np.abs(M - np.eye(nl)).max() < 1e-13
+
+
+def test_assemble_terms_rejects_bad_mask_before_any_device_work():
+    """dgb_assemble_terms validates its term mask on the host (no GPU needed)."""
+    from paper_1502_02941_b200 import problems
+    lib = capi.load()
+    spec = problems.registry_get("smooth-sine")
+    params = capi.Params()
+    st = lib.dgb_assemble_terms(None, None, C.byref(spec.c), C.byref(params), 9, None, None, None)
+    assert capi.STATUS_NAMES[st] == "InvalidArgument"
+    assert b"term mask" in lib.dgb_last_error_message()
