@@ -434,7 +434,13 @@ typedef struct dgb_solve_options {
   double tolerance_scale;  /* stop at tolerance_scale * the contract bound (default 0.1)   */
   int32_t max_iterations;  /* total Krylov iterations (default 20000)                     */
   int32_t restart;         /* GMRES(m) restart length m (default 30, <= 200)              */
+  int32_t preconditioner;  /* DGB_PRECOND_*: right preconditioner (default: block SGS)        */
+  int32_t pad_;
 } dgb_solve_options;
+/* Right preconditioners of dgb_solve: block Jacobi (the inverses of the diagonal blocks), or one
+ * symmetric block Gauss-Seidel sweep in a multicolour order of the block rows (a greedy colouring
+ * of the BSR graph: rows of one colour are independent, so each colour is one parallel step). */
+enum dgb_preconditioner { DGB_PRECOND_BLOCK_JACOBI = 0, DGB_PRECOND_BLOCK_SGS = 1 };
 
 typedef struct dgb_solve_info { /* SolveInfo (sparse.hpp:55-59) + the Krylov counters      */
   double defect_norm2;

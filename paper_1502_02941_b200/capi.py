@@ -92,11 +92,12 @@ class Reaction(C.Structure):
 
 REACTION_ZERO, REACTION_LINEAR, REACTION_SQUARE, REACTION_CUBIC = 0, 1, 2, 3
 TERM_DIFFUSION, TERM_CONVECTION, TERM_REACTION, TERM_ALL = 1, 2, 4, 7
+PRECOND_BLOCK_JACOBI, PRECOND_BLOCK_SGS = 0, 1
 
 
 class SolveOptions(C.Structure):
     _fields_ = [("tolerance_scale", C.c_double), ("max_iterations", C.c_int32),
-                ("restart", C.c_int32)]
+                ("restart", C.c_int32), ("preconditioner", C.c_int32), ("pad_", C.c_int32)]
 
 
 class SolveInfo(C.Structure):

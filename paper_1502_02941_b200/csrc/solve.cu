@@ -116,6 +116,51 @@ __global__ void block_apply_kernel(const double* __restrict__ d, const double* _
   y[r] = s;
 }
 
+// One colour of the symmetric block Gauss-Seidel sweep (right preconditioner y = M^-1 x with
+// M = (D + L) D^-1 (D + U), L / U the blocks whose column has an earlier / later colour).
+// FORWARD: t_e = D_e^-1 (x_e - sum_{colour(j) < c} K_ej t_j); BACKWARD (colours descending):
+// y_e = t_e - D_e^-1 sum_{colour(j) > c} K_ej y_j.  Rows of one colour share no block, so every
+// row of the colour is updated in parallel (one thread per block row).
+template <int NL, bool FORWARD>
+__global__ void sgs_colour_kernel(const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
+                                  const double* __restrict__ val, const double* __restrict__ dinv,
+                                  const int32_t* __restrict__ colour, const int32_t* __restrict__ order,
+                                  int begin, int end, int c, const double* __restrict__ x,
+                                  const double* __restrict__ t, double* __restrict__ out) {
+  const int idx = begin + blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= end) return;
+  const int e = order[idx];
+  double acc[NL];
+#pragma unroll
+  for (int i = 0; i < NL; ++i) acc[i] = 0.0;
+  for (int b = row_ptr[e]; b < row_ptr[e + 1]; ++b) {
+    const int j = col[b];
+    const int cj = colour[j];
+    if (FORWARD ? cj >= c : cj <= c) continue;  // the diagonal block (cj == c) included
+    const double* blk = val + static_cast<long long>(b) * NL * NL;
+    const double* vj = out + static_cast<long long>(j) * NL;  // t (forward) / y (backward)
+#pragma unroll
+    for (int i = 0; i < NL; ++i) {
+      double sacc = 0.0;
+#pragma unroll
+      for (int k = 0; k < NL; ++k) sacc = fma(blk[i * NL + k], vj[k], sacc);
+      acc[i] += sacc;
+    }
+  }
+  const double* d = dinv + static_cast<long long>(e) * NL * NL;
+  const long long o = static_cast<long long>(e) * NL;
+#pragma unroll
+  for (int i = 0; i < NL; ++i) {
+    double r = 0.0;
+#pragma unroll
+    for (int k = 0; k < NL; ++k) {
+      const double rhs = FORWARD ? x[o + k] - acc[k] : acc[k];
+      r = fma(d[i * NL + k], rhs, r);
+    }
+    out[o + i] = FORWARD ? r : t[o + i] - r;
+  }
+}
+
 __device__ __forceinline__ double block_sum(double v, double* sh) {
   sh[threadIdx.x] = v;
   __syncthreads();
@@ -361,6 +406,34 @@ struct BsrOps {
   cudaStream_t s;
 
   void spmv(const double* x, double* y) const { dgb::launch_bsr_spmv(a, x, y, s); }
+  // symmetric block Gauss-Seidel in colour order: forward colours 0..C-1 into t, backward
+  // colours C-1..0 into y
+  template <int NL>
+  void sgs_t(const double* dinv, const int32_t* colour, const int32_t* order,
+             const std::vector<int>& cstart, const double* x, double* t, double* y) const {
+    const int C = static_cast<int>(cstart.size()) - 1;
+    for (int c = 0; c < C; ++c) {
+      const int cnt = cstart[c + 1] - cstart[c];
+      if (cnt > 0) sgs_colour_kernel<NL, true><<<(cnt + 127) / 128, 128, 0, s>>>(
+          a->row_ptr, a->col, a->val, dinv, colour, order, cstart[c], cstart[c + 1], c, x, nullptr, t);
+    }
+    for (int c = C - 1; c >= 0; --c) {
+      const int cnt = cstart[c + 1] - cstart[c];
+      if (cnt > 0) sgs_colour_kernel<NL, false><<<(cnt + 127) / 128, 128, 0, s>>>(
+          a->row_ptr, a->col, a->val, dinv, colour, order, cstart[c], cstart[c + 1], c, nullptr, t, y);
+    }
+  }
+  void sgs(const double* dinv, const int32_t* colour, const int32_t* order,
+           const std::vector<int>& cstart, const double* x, double* t, double* y) const {
+    switch (nl) {
+      case 3: sgs_t<3>(dinv, colour, order, cstart, x, t, y); break;
+      case 6: sgs_t<6>(dinv, colour, order, cstart, x, t, y); break;
+      case 10: sgs_t<10>(dinv, colour, order, cstart, x, t, y); break;
+      case 15: sgs_t<15>(dinv, colour, order, cstart, x, t, y); break;
+      default: throw dgb::Error(DGB_STATUS_UNSUPPORTED_DEGREE, "unsupported block size", nl);
+    }
+    cuda_check(cudaGetLastError(), "sgs_colour_kernel");
+  }
   void precond(const double* dinv, const double* x, double* y) const {
     switch (nl) {
       case 3: block_apply_kernel<3><<<grid_for(n), kThreads, 0, s>>>(dinv, x, y, n); break;
@@ -440,12 +513,15 @@ dgb_solve_options resolve(const dgb_solve_options* opt) {
     if (opt->tolerance_scale > 0) o.tolerance_scale = opt->tolerance_scale;
     if (opt->max_iterations > 0) o.max_iterations = opt->max_iterations;
     if (opt->restart > 0) o.restart = std::min(opt->restart, kMaxRestart);
+    if (opt->preconditioner == DGB_PRECOND_BLOCK_JACOBI || opt->preconditioner == DGB_PRECOND_BLOCK_SGS) {
+      o.preconditioner = opt->preconditioner;
+    }
   }
   return o;
 }
 
-// GMRES(m), right preconditioning with block Jacobi, classical Gram-Schmidt with one
-// re-orthogonalisation (CGS2).  Returns the contract check on the true residual.
+// GMRES(m), right preconditioning (block Jacobi, or one symmetric block Gauss-Seidel sweep in
+// multicolour order), classical Gram-Schmidt with one re-orthogonalisation (CGS2).  Returns the contract check on the true residual.
 // A library-owned blocking stream that stands in for the legacy default stream (which cannot
 // be captured into a graph).  Blocking streams are ordered with the legacy stream both ways,
 // so callers on stream 0 see the usual semantics.
@@ -489,6 +565,46 @@ void gmres_solve(const dgb_bsr* a, const double* b, double* x, const dgb_solve_o
     throw dgb::Error(DGB_STATUS_SINGULAR_MATRIX, "block-Jacobi factorization failed: zero pivot in a diagonal block",
                      static_cast<long long>(bad));
   }
+  // multicolour order for the block SGS preconditioner: a greedy colouring of the BSR graph on
+  // the host (the block columns of row e are its neighbours; <= 4 colours on a triangle mesh)
+  const bool sgs = o.preconditioner == DGB_PRECOND_BLOCK_SGS;
+  std::vector<int> cstart;
+  DevBuf colour_d(sgs ? sizeof(int32_t) * E : 1), order_d(sgs ? sizeof(int32_t) * E : 1),
+      tbuf(sgs ? sizeof(double) * n : 1);
+  if (sgs) {
+    std::vector<int32_t> rp(E + 1), cl(static_cast<size_t>(a->nnzb)), colour(E, -1), order(E);
+    cuda_check(cudaMemcpyAsync(rp.data(), a->row_ptr, sizeof(int32_t) * (E + 1), cudaMemcpyDeviceToHost, s), "D2H(rp)");
+    cuda_check(cudaMemcpyAsync(cl.data(), a->col, sizeof(int32_t) * a->nnzb, cudaMemcpyDeviceToHost, s), "D2H(col)");
+    cuda_check(cudaStreamSynchronize(s), "cudaStreamSynchronize(pattern)");
+    int n_col = 0;
+    for (int e = 0; e < E; ++e) {
+      unsigned used = 0;  // colours of already-coloured neighbours (< 32)
+      for (int b = rp[e]; b < rp[e + 1]; ++b) {
+        const int j = cl[b];
+        if (j != e && j >= 0 && j < E && colour[j] >= 0 && colour[j] < 32) used |= 1u << colour[j];
+      }
+      int c = 0;
+      while (c < 31 && (used >> c & 1u)) ++c;
+      colour[e] = c;
+      n_col = std::max(n_col, c + 1);
+    }
+    cstart.assign(n_col + 1, 0);
+    for (int e = 0; e < E; ++e) ++cstart[colour[e] + 1];
+    for (int c = 0; c < n_col; ++c) cstart[c + 1] += cstart[c];
+    std::vector<int> fill(cstart.begin(), cstart.end() - 1);
+    for (int e = 0; e < E; ++e) order[fill[colour[e]]++] = e;
+    cuda_check(cudaMemcpyAsync(colour_d.p, colour.data(), sizeof(int32_t) * E, cudaMemcpyHostToDevice, s), "H2D(colour)");
+    cuda_check(cudaMemcpyAsync(order_d.p, order.data(), sizeof(int32_t) * E, cudaMemcpyHostToDevice, s), "H2D(order)");
+    cuda_check(cudaStreamSynchronize(s), "cudaStreamSynchronize(colour)");
+  }
+  auto precond = [&](const double* xin, double* yout) {
+    if (sgs) {
+      A.sgs(dinv.as<double>(), colour_d.as<int32_t>(), order_d.as<int32_t>(), cstart, xin,
+            tbuf.as<double>(), yout);
+    } else {
+      A.precond(dinv.as<double>(), xin, yout);
+    }
+  };
   const long long nvals = a->nnzb * static_cast<long long>(nl) * nl;
   const double a_fro = std::sqrt(R.dot(a->val, a->val, nvals));
   const double b_norm = std::sqrt(R.dot(b, b, n));
@@ -508,7 +624,7 @@ void gmres_solve(const dgb_bsr* a, const double* b, double* x, const dgb_solve_o
     double* vk = Vp + static_cast<long long>(k) * n;
     double* vn = Vp + static_cast<long long>(k + 1) * n;
     double* hk = Hd.as<double>() + static_cast<long long>(k) * (m + 1);
-    A.precond(dinv.as<double>(), vk, z.as<double>());
+    precond(vk, z.as<double>());
     A.spmv(z.as<double>(), w.as<double>());
     R.dots_device(Vp, n, k + 1, w.as<double>(), n, hk);                          // CGS pass 1
     subtract_combo_kernel<<<grid_for(n), kThreads, 0, s>>>(w.as<double>(), Vp, n, hk, k + 1, n);
@@ -580,7 +696,7 @@ void gmres_solve(const dgb_bsr* a, const double* b, double* x, const dgb_solve_o
     }
     cuda_check(cudaMemcpyAsync(hdev.p, y.data(), sizeof(double) * k, cudaMemcpyHostToDevice, s), "H2D(y)");
     combo_kernel<<<grid_for(n), kThreads, 0, s>>>(w.as<double>(), Vp, n, hdev.as<double>(), k, n);
-    A.precond(dinv.as<double>(), w.as<double>(), z.as<double>());
+    precond(w.as<double>(), z.as<double>());
     axpy_kernel<<<grid_for(n), kThreads, 0, s>>>(x, 1.0, z.as<double>(), n);
     cuda_check(cudaGetLastError(), "gmres update");
     ++restarts;
@@ -610,6 +726,8 @@ void dgb_solve_options_default(dgb_solve_options* opt) {
   opt->tolerance_scale = 0.1;
   opt->max_iterations = 20000;
   opt->restart = 30;
+  opt->preconditioner = DGB_PRECOND_BLOCK_SGS;
+  opt->pad_ = 0;
 }
 
 void dgb_newton_config_default(dgb_newton_config* cfg) {

@@ -425,9 +425,11 @@ def _stream_handle(device: int, stream=None) -> int:
 
 
 def solve_options(tolerance_scale: float | None = None, max_iterations: int | None = None,
-                  restart: int | None = None) -> "capi.SolveOptions":
+                  restart: int | None = None, preconditioner: int | None = None) -> "capi.SolveOptions":
     o = capi.SolveOptions()
     capi.load().dgb_solve_options_default(C.byref(o))
+    if preconditioner is not None:
+        o.preconditioner = preconditioner
     if tolerance_scale is not None:
         o.tolerance_scale = tolerance_scale
     if max_iterations is not None:

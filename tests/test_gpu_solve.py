@@ -1,4 +1,4 @@
-"""GPU: dgb_solve (block-Jacobi GMRES under direct_solve's accuracy contract, sparse.cpp:154-217)
+"""GPU: dgb_solve (block-Jacobi / multicolour block-SGS GMRES under direct_solve's accuracy contract, sparse.cpp:154-217)
 and dgb_newton_solve (nonlinear.cpp:109-176) against the numpy/SuperLU restatement
 (oracle/newton.py) and the reference's own tests of this layer.  SURVEY.md §8(f) rank 2."""
 import numpy as np
@@ -29,8 +29,9 @@ def host_csr(out):
     return bsr_to_csr(rp, col, val), out.rhs.cpu().numpy().reshape(-1)
 
 
+@pytest.mark.parametrize("precond", [capi.PRECOND_BLOCK_SGS, capi.PRECOND_BLOCK_JACOBI])
 @pytest.mark.parametrize("case", ["config1", "config2_small", "smooth-sine_k3", "layer_k2"])
-def test_solve_matches_direct_solution(case):
+def test_solve_matches_direct_solution(case, precond):
     if case == "config1":
         cfg = problems.CONFIGS[1]
         mesh = dgfem.config_mesh(cfg)
@@ -55,10 +56,11 @@ def test_solve_matches_direct_solution(case):
         degree, qo = 2, 0
     ref, plan, dm, out = device_system(mesh, degree, spec, params, qo)
     # the reference's acceptance contract with the default (production) tolerance
-    x, info = dgfem.solve(out, out.rhs.reshape(-1))
+    x, info = dgfem.solve(out, out.rhs.reshape(-1), options=dgfem.solve_options(preconditioner=precond))
     assert info["defect_norm2"] <= info["bound"]
     # tightened: converges to the direct solution
-    x2, info2 = dgfem.solve(out, out.rhs.reshape(-1), options=dgfem.solve_options(tolerance_scale=1e-4))
+    x2, info2 = dgfem.solve(out, out.rhs.reshape(-1),
+                            options=dgfem.solve_options(tolerance_scale=1e-4, preconditioner=precond))
     (ro, ci, va), F = host_csr(out)
     xr, _ = onewton.direct_solve(ro, ci, va, F)
     err = np.abs(x2.cpu().numpy() - xr).max() / max(1.0, np.abs(xr).max())
@@ -74,6 +76,21 @@ def test_solve_is_deterministic():
     a, _ = dgfem.solve(out, out.rhs.reshape(-1))
     b, _ = dgfem.solve(out, out.rhs.reshape(-1))
     assert bool((a == b).all())
+
+
+@pytest.mark.parametrize("cfg_index", [1, 2])
+def test_sgs_needs_fewer_iterations_than_jacobi(cfg_index):
+    """The multicolour SGS sweep is the default because it cuts the Krylov iterations on the
+    benchmark systems (each SGS apply costs about two SpMVs' worth of K reads)."""
+    cfg = problems.CONFIGS[cfg_index]
+    mesh = dgfem.config_mesh(cfg) if cfg_index == 1 else dgfem.unit_square_mesh(64)
+    ref, plan, dm, out = device_system(mesh, cfg.degree, problems.config_problem(cfg_index, mesh.n_elements),
+                                       dgfem.config_parameters(cfg, capi.SIPG), cfg.quad_order)
+    _, ij = dgfem.solve(out, out.rhs.reshape(-1),
+                        options=dgfem.solve_options(preconditioner=capi.PRECOND_BLOCK_JACOBI))
+    xs, isg = dgfem.solve(out, out.rhs.reshape(-1))
+    assert isg["defect_norm2"] <= isg["bound"]
+    assert isg["iterations"] < ij["iterations"], (isg, ij)
 
 
 def test_singular_block_raises():
