@@ -207,6 +207,7 @@ OPTION_BATCH_FUSE = 4
 OPTION_WARP_SPECIALIZED = 5
 OPTION_P1_PIPELINE = 6
 OPTION_L2_CARVEOUT_MB = 7
+OPTION_GEOMETRY_CACHE = 8
 OPTION_PROFILE_ABLATE = 1000  # diagnostics only: results are wrong while set
 
 _lib = None

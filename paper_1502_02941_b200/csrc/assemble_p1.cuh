@@ -482,7 +482,7 @@ struct SmemP1Pipe {
 
 
 
-template <int NQV, int NQE, int WARPS>
+template <int NQV, int NQE, int WARPS, bool GEO>
 __global__ void __launch_bounds__(WARPS * 32, 1) assemble_p1_pipe_kernel(
     const __grid_constant__ Params2<3, NQV, NQE, false, true> P) {
   constexpr int NL = 3;
@@ -511,7 +511,15 @@ __global__ void __launch_bounds__(WARPS * 32, 1) assemble_p1_pipe_kernel(
     const int e = P.row_begin + (gw + j * n_gw) * 32 + lane;
     const int r = min(e, P.row_end - 1) - P.row_begin;
     cp_async16(idx + PS::kNb + 4 * lane, P.adj_nb + r);
-    cp_async16(idx + PS::kOp + 4 * lane, P.adj_op + r);
+    if constexpr (GEO) {
+      // the chunk's vertex coordinates from the bound record: six coalesced 16-byte copies per
+      // lane, in flight together with the index records (no dependent gather)
+      const double2* g = P.geo + static_cast<size_t>(gw + j * n_gw) * (6 * 32) + lane;
+#pragma unroll
+      for (int k = 0; k < 6; ++k) cp_async16(nod + k * 32 + lane, g + k * 32);
+    } else {
+      cp_async16(idx + PS::kOp + 4 * lane, P.adj_op + r);
+    }
 #pragma unroll
     for (int k = 0; k < 3; ++k) cp_async4(idx + PS::kV + 3 * lane + k, P.elements + 3 * (P.row_begin + r) + k);
     cp_async4(idx + PS::kRp + lane, P.row_ptr_src + r);
@@ -538,8 +546,10 @@ __global__ void __launch_bounds__(WARPS * 32, 1) assemble_p1_pipe_kernel(
 
   if (n_local > 0) {
     issue_records(0);
-    cp_async_wait_all();
-    issue_nodes();
+    if constexpr (!GEO) {
+      cp_async_wait_all();
+      issue_nodes();
+    }
   }
 #pragma unroll 1
   for (int j = 0; j < n_local; ++j) {
@@ -547,7 +557,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) assemble_p1_pipe_kernel(
     // everything of chunk j into registers; the buffers take chunk j + 1 from here on
     const int v[3] = {idx[PS::kV + 3 * lane], idx[PS::kV + 3 * lane + 1], idx[PS::kV + 3 * lane + 2]};
     const int4 anb = *reinterpret_cast<const int4*>(idx + PS::kNb + 4 * lane);
-    const int4 aop = *reinterpret_cast<const int4*>(idx + PS::kOp + 4 * lane);
+    const int4 aop = GEO ? make_int4(0, 0, 0, 0) : *reinterpret_cast<const int4*>(idx + PS::kOp + 4 * lane);
     const int rp = idx[PS::kRp + lane], rp_next = idx[PS::kRpn + lane];
     const double2 pv[3] = {nod[lane], nod[32 + lane], nod[64 + lane]};
     const double2 po[3] = {nod[96 + lane], nod[128 + lane], nod[160 + lane]};
@@ -559,9 +569,11 @@ __global__ void __launch_bounds__(WARPS * 32, 1) assemble_p1_pipe_kernel(
     const int ee = active ? e : P.row_end - 1;
     p1_row<NQV, NQE, true>(P, tr, mset, stw, srhs, lane, e_first, ee, active, v, anb, aop, rp,
                            rp_next, pv, po, true, [&] {
-                             if (more) {
-                               cp_async_wait_all();  // chunk j + 1's records
-                               issue_nodes();
+                             if constexpr (!GEO) {
+                               if (more) {
+                                 cp_async_wait_all();  // chunk j + 1's records
+                                 issue_nodes();
+                               }
                              }
                            });
   }

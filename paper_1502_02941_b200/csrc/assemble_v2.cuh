@@ -90,6 +90,8 @@ struct Params2 {
   const int32_t* row_ptr_src;    // bound pattern (dgb_plan_bind_mesh) copied to row_ptr, or null
   const int4* adj_nb;            // bound adjacency: neighbour per local edge, .w = kinds | lf << 2
   const int4* adj_op;            // bound adjacency: neighbour's vertex opposite the shared edge
+  const double2* geo;            // bound vertex coordinates per 32-row chunk [chunk][6][32]: own
+                                 // vertices 0..2, the neighbours' opposite vertices 3..5; or null
   unsigned long long* err_edge;  // epoch << 32 | ~edge, max-reduced (lowest edge wins)
   unsigned long long epoch;
   int32_t n_elements;

@@ -455,6 +455,30 @@ __global__ void adjacency_kernel(const int32_t* __restrict__ elements,
   op[r] = make_int4(opp[0], opp[1], opp[2], 0);
 }
 
+// Vertex coordinates of rows [begin, begin + n) per 32-row chunk (bound once per mesh, the P1
+// persistent kernel): geo[(chunk * 6 + k) * 32 + lane] = the element's own vertices (k = 0..2)
+// and its neighbours' vertices opposite the shared edges (k = 3..5; a boundary edge repeats
+// node 0, unused).  The block-row kernel then reads its coordinates with coalesced 16-byte
+// copies instead of six random gathers per element (the "geometry precompute" of the north
+// star); the values are copies of mesh->nodes, so results are bitwise the same.  Lanes past the
+// last row repeat it.
+__global__ void geometry_kernel(const double* __restrict__ nodes, const int32_t* __restrict__ elements,
+                                const int4* __restrict__ op, int32_t begin, int32_t n,
+                                double2* __restrict__ geo) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= ((n + 31) & ~31)) return;
+  const int r = min(t, n - 1);
+  const int e = begin + r;
+  const double2* nodes2 = reinterpret_cast<const double2*>(nodes);
+  const int4 o = __ldg(op + r);
+  double2* g = geo + static_cast<size_t>(t >> 5) * (6 * 32) + (t & 31);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) g[k * 32] = __ldg(nodes2 + __ldg(elements + 3 * e + k));
+  g[3 * 32] = __ldg(nodes2 + max(o.x, 0));
+  g[4 * 32] = __ldg(nodes2 + max(o.y, 0));
+  g[5 * 32] = __ldg(nodes2 + max(o.z, 0));
+}
+
 // ------------------------------------------------------------------------------------------
 // the block-row kernel
 // ------------------------------------------------------------------------------------------
@@ -1035,6 +1059,12 @@ struct dgb_plan {
   size_t adj_cap = 0, adj_rows = 0;
   const void* bound_elements = nullptr;
   const void* bound_edge_elements = nullptr;
+  // P1 persistent kernel: the bound rows' vertex coordinates per chunk (geometry_kernel), valid
+  // for the node array bound_nodes
+  double2* d_geo = nullptr;
+  size_t geo_cap = 0;
+  const void* bound_nodes = nullptr;
+  int geo_cache = 1;            // bind the vertex coordinates too (P1 persistent kernel)
   int32_t last_launches = 0;
   size_t l2_persist_bytes = 0;  // persisting-L2 carve-out available to the node window
   bool carve_held = false;      // this plan holds a reference on its device's carve-out
@@ -1144,6 +1174,7 @@ void launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_prob
   if (row_ptr_src) {
     P.adj_nb = plan->d_adj;
     P.adj_op = plan->d_adj + plan->adj_rows;
+    if (plan->d_geo && plan->geo_cache > 0 && plan->bound_nodes == mesh->nodes) P.geo = plan->d_geo;
   }
   P.err_edge = plan->d_err;
   P.epoch = plan->epoch & 0xFFFFFFFFull;
@@ -1164,6 +1195,7 @@ void launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_prob
     P.load_hints = 1;  // the P1 persistent kernel's auto policy (bind time): hints, normal output
     P.evict_first = 0;
   }
+  if (P.geo) P.load_hints = 0;  // no node gathers left to hint
   P.prob = *problem;
   const double* h = plan->h_tens.data();
   const dgb::Layout& V = plan->L;
@@ -1485,7 +1517,8 @@ void launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_prob
       auto launch = [&](auto tag) {
         constexpr int W = decltype(tag)::value;
         using PS = dgb::v2::SmemP1Pipe<NQV, NQE, W>;
-        auto pk = dgb::v2::assemble_p1_pipe_kernel<NQV, NQE, W>;
+        auto pk = P.geo ? dgb::v2::assemble_p1_pipe_kernel<NQV, NQE, W, true>
+                        : dgb::v2::assemble_p1_pipe_kernel<NQV, NQE, W, false>;
         dgb::ensure_dynamic_smem(reinterpret_cast<const void*>(pk), PS::kBytes, "cudaFuncSetAttribute(p1 pipe)");
         const int n_chunks = (out_row_end - out_row_begin + 31) / 32;
         cfg.gridDim = dim3(std::max(1, std::min(plan->sm_count, (n_chunks + W - 1) / W)), nb);
@@ -1722,6 +1755,27 @@ int dgb_plan_bind_mesh(dgb_plan* plan, const dgb_mesh_arrays* mesh, int32_t row_
     } else {
       cuda_check(cudaMemsetAsync(plan->d_pattern, 0, sizeof(int32_t), s), "cudaMemsetAsync");
     }
+    // P1 persistent kernel: the rows' vertex coordinates in chunk order (96 B per element)
+    plan->bound_nodes = nullptr;
+    const bool want_geo = plan->nl == 3 && plan->p1_pipe > 0 && plan->geo_cache > 0 && rows > 0;
+    if (want_geo) {
+      const size_t padded = (rows + 31) & ~size_t(31);
+      if (padded > plan->geo_cap) {
+        cudaFree(plan->d_geo);
+        plan->d_geo = nullptr;
+        plan->geo_cap = 0;
+        cuda_check(cudaMalloc(&plan->d_geo, padded * 6 * sizeof(double2)), "cudaMalloc(geometry)");
+        plan->geo_cap = padded;
+      }
+      dgb::geometry_kernel<<<static_cast<unsigned>((padded + 255) / 256), 256, 0, s>>>(
+          mesh->nodes, mesh->elements, plan->d_adj + rows, row_begin, row_end - row_begin, plan->d_geo);
+      cuda_check(cudaGetLastError(), "geometry_kernel");
+      plan->bound_nodes = mesh->nodes;
+    } else if (plan->d_geo) {
+      cudaFree(plan->d_geo);
+      plan->d_geo = nullptr;
+      plan->geo_cap = 0;
+    }
     {
       // L2 policy: permuted (gather-heavy) meshes keep their nodes persisting in L2; the
       // carve-out is sized to the node array, never more (it is taken from the write stream).
@@ -1729,7 +1783,8 @@ int dgb_plan_bind_mesh(dgb_plan* plan, const dgb_mesh_arrays* mesh, int32_t row_
       // most 56 MiB (a carve-out of the whole 67 MB node array at config 4 costs 50%; 48-56
       // MiB halves the DRAM reads and gains 3%, profiles/NOTES.md)
       const size_t node_bytes = sizeof(double) * 2 * static_cast<size_t>(mesh->n_nodes);
-      const bool p1_auto = plan->l2_policy < 0 && plan->nl == 3 && plan->p1_pipe > 0;
+      // (with the vertex coordinates bound there are no node gathers to keep resident)
+      const bool p1_auto = plan->l2_policy < 0 && plan->nl == 3 && plan->p1_pipe > 0 && !want_geo;
       size_t want = (plan->l2_policy > 0 && (plan->l2_policy & 5)) || p1_auto
                         ? std::min(node_bytes, plan->l2_persist_max) : 0;
       if (p1_auto) want = std::min(want, size_t(56) << 20);
@@ -1757,7 +1812,7 @@ int dgb_plan_bind_mesh(dgb_plan* plan, const dgb_mesh_arrays* mesh, int32_t row_
 
 int dgb_plan_unbind_mesh(dgb_plan* plan) {
   if (!plan) return DGB_STATUS_INVALID_ARGUMENT;
-  plan->bound_ee = plan->bound_kind = nullptr;
+  plan->bound_ee = plan->bound_kind = plan->bound_nodes = nullptr;
   plan->bound_n = plan->bound_begin = plan->bound_end = -1;
   return DGB_OK;
 }
@@ -1855,6 +1910,7 @@ void dgb_plan_destroy(dgb_plan* p) {
   cudaFree(p->d_scan);
   cudaFree(p->d_pattern);
   cudaFree(p->d_adj);
+  cudaFree(p->d_geo);
   for (auto& c : p->bfrag_cache) cudaFree(c.second);
   cudaFree(p->d_nlfrag);
   cudaFree(p->d_trace);
@@ -2096,6 +2152,7 @@ int dgb_plan_set_option(dgb_plan* plan, int32_t option, int32_t value) {
     case DGB_OPTION_WARP_SPECIALIZED: plan->warp_specialized = value; return DGB_OK;
     case DGB_OPTION_P1_PIPELINE: plan->p1_pipe = value; return DGB_OK;
     case DGB_OPTION_L2_CARVEOUT_MB: plan->l2_carve_mb = value; return DGB_OK;
+    case DGB_OPTION_GEOMETRY_CACHE: plan->geo_cache = value; return DGB_OK;
     // profiling diagnostics (results are WRONG while set): see the header
     case DGB_OPTION_PROFILE_ABLATE:
 #ifdef DGB_TUNING

@@ -140,14 +140,14 @@ class BatchedSystemsRun(ConfigRun):
     its block columns offset by b E and its row_ptr by b nnzb; `system(b)` returns it with both
     offsets removed (the reference's per-call DgSystem of that copy)."""
 
-    def __init__(self, index: int = 1, copies: int = 512, device: int = 0):
+    def __init__(self, index: int = 1, copies: int = 512, device: int = 0, options: dict | None = None):
         cfg = problems.CONFIGS[index]
         single = dgfem.config_mesh(cfg)
         self.copies, self.E_sys = copies, single.n_elements
         self.nnzb_sys = single.n_elements + 2 * single.n_interior_edges
         r = replicated_raw(single.raw(), copies)
         union = dgfem.build_mesh(r["nodes"], r["elements"], r["dirichlet"], r["neumann"])
-        super().__init__(index, device, mesh=union)
+        super().__init__(index, device, mesh=union, options=options)
 
     def system(self, b: int):
         out = self.outputs()[0]
