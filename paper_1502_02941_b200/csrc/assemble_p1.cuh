@@ -11,6 +11,12 @@
 // warp (the warp's row range is contiguous in the BSR).
 #pragma once
 
+// Persistent kernel's copy-out: 1 = one bulk asynchronous copy per chunk whose read of the
+// staging is awaited a volume phase later; 0 = the warp copies its range itself.
+#ifndef DGB_P1_BULK_OUT
+#define DGB_P1_BULK_OUT 1
+#endif
+
 namespace dgb {
 namespace v2 {
 
@@ -52,18 +58,70 @@ __device__ __forceinline__ void p1_tables(const Params2<3, NQV, NQE, false, true
   }
 }
 
+// make_side / edge_geometry of local edge l (assembly.cpp:125-126, mesh.cpp:232-257) from the
+// element's vertices: direction in the sorted-pair orientation o (0: a < b), length and its
+// reciprocal from one rsqrt, unit outward normal.  Shared by the block-row kernel and the
+// bind-time geometry kernel (dg_assembly.cu), so a bound record holds the kernel's own values.
+// The outward normal does not depend on the orientation o: reversing the edge negates (dx, dy)
+// exactly, and make_side's sign flip negates the rotated tangent back.  So the direction is
+// taken from vertex l+1 to vertex l+2 (o = 0); only a boundary edge's quadrature points need the
+// oriented start vertex and direction (p1_edge_oriented).
+struct EdgeFrame {
+  double dx, dy, rh, nx, ny;
+};
+__device__ __forceinline__ void p1_edge_dir(const double2 (&pv)[3], int l, double& dx, double& dy) {
+  dx = FSUB(pv[(l + 2) % 3].x, pv[(l + 1) % 3].x);
+  dy = FSUB(pv[(l + 2) % 3].y, pv[(l + 1) % 3].y);
+}
+__device__ __forceinline__ void p1_edge_normal(double dx, double dy, double rh, double& nx, double& ny) {
+  nx = FMUL(dy, rh);
+  ny = -FMUL(dx, rh);
+}
+__device__ __forceinline__ EdgeFrame p1_edge_frame(const double2 (&pv)[3], int l) {
+  EdgeFrame f;
+  p1_edge_dir(pv, l, f.dx, f.dy);
+  f.rh = rsqrt_nr(fma(f.dx, f.dx, FMUL(f.dy, f.dy)));
+  p1_edge_normal(f.dx, f.dy, f.rh, f.nx, f.ny);
+  return f;
+}
+// G_f^T n: the neighbour's inverse-transposed Jacobian, in its vertex order rotated to
+// (opposite, b, a), applied to this element's outward normal.
+__device__ __forceinline__ double2 p1_neighbour_normal(double2 opp, double2 pb, double2 pa, double nx, double ny) {
+  const Geo gf = element_geo_coords(opp, pb, pa);
+  return make_double2(fma(gf.G00, nx, FMUL(gf.G10, ny)), fma(gf.G01, nx, FMUL(gf.G11, ny)));
+}
+
+// The element's extent for source_points: the largest squared distance from a centre to a vertex.
+struct VertexExtent {
+  static constexpr bool kKnown = true;
+  const double2 (&pv)[3];
+  __device__ __forceinline__ double operator()(double cx, double cy) const {
+    double m = 0.0;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const double dx = pv[k].x - cx, dy = pv[k].y - cy;
+      m = fmax(m, fma(dx, dx, dy * dy));
+    }
+    return m;
+  }
+};
+
 // The block row of one element (one lane), after its gathers: neighbours, slots, block columns,
 // geometry, volume and face terms, the neighbour blocks staged in the warp's row range, and the
 // warp's RHS slice and row range sent by bulk copies.  `wait_stage` (persistent kernel): the
 // staging is reused by the next chunk, so the warp copies its row range out itself.
 // `mid()` runs between the volume terms and the edge loop (the persistent kernel issues the next
 // chunk's node gathers there).
-template <int NQV, int NQE, bool BOUND, class MID>
+// GEO (persistent kernel, bound geometry record): po[l] holds the neighbour's G_f^T n and gx the
+// reciprocals (1 / det, 1 / h_0), (1 / h_1, 1 / h_2); slots, orientations and the block count
+// come from the adjacency word.
+template <int NQV, int NQE, bool BOUND, bool GEO, class MID>
 __device__ __forceinline__ void p1_row(const Params2<3, NQV, NQE, false, true>& P, const double* tr,
                                        int mset, double* stw, double* srhs, int lane, int e_first,
                                        int ee, bool active, const int (&v)[3], int4 anb, int4 aop,
                                        int rp, int rp_next, const double2 (&pv)[3],
-                                       const double2 (&po)[3], bool wait_stage, MID&& mid) {
+                                       const double2 (&po)[3], const double2 (&gx)[2], bool wait_stage,
+                                       MID&& mid) {
   constexpr int NL = 3, N2 = 9;
   using L = Lay<NL, NQV, NQE, false, true>;
   using SM = SmemP1<NQV, NQE>;
@@ -102,7 +160,11 @@ __device__ __forceinline__ void p1_row(const Params2<3, NQV, NQE, false, true>& 
   }
   // sorted block columns -> slots (rank among the row's distinct columns)
   int slot_of[4], nb = 1;
-  {
+  if constexpr (GEO) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) slot_of[i] = (anb.w >> (12 + 2 * i)) & 3;
+    nb = (anb.w >> 23) & 7;
+  } else {
     const int cx[4] = {ee, fv[0], fv[1], fv[2]};
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -136,7 +198,7 @@ __device__ __forceinline__ void p1_row(const Params2<3, NQV, NQE, false, true>& 
   const double B00 = FSUB(pv[1].x, pv[0].x), B01 = FSUB(pv[2].x, pv[0].x);
   const double B10 = FSUB(pv[1].y, pv[0].y), B11 = FSUB(pv[2].y, pv[0].y);
   const double det = FSUB(FMUL(B00, B11), FMUL(B01, B10));
-  const double rdet = rcp_nr(det);
+  const double rdet = GEO ? gx[0].x : rcp_nr(det);
   const double G00 = B11 * rdet, G01 = -B10 * rdet;
   const double G10 = -B01 * rdet, G11 = B00 * rdet;
   const double eps = scalar_element(P.prob.diffusion, ee);
@@ -161,7 +223,8 @@ __device__ __forceinline__ void p1_row(const Params2<3, NQV, NQE, false, true>& 
           const double c = (det * P.t.x[L::VW + q]) * f;
 #pragma unroll
           for (int i = 0; i < NL; ++i) F[i] = fma(c, P.t.x[L::PHI + q * NL + i], F[i]);
-        });
+        },
+        0, 1, VertexExtent{pv});
   }
 
   // diagonal block: volume terms (registers)
@@ -191,27 +254,27 @@ __device__ __forceinline__ void p1_row(const Params2<3, NQV, NQE, false, true>& 
   // ---- edges: face terms into the diagonal, neighbour blocks staged at once --------------------
 #pragma unroll
   for (int l = 0; l < 3; ++l) {
-    const int a = v[(l + 1) % 3], b = v[(l + 2) % 3];
-    const int o = a < b ? 0 : 1;  // make_side orientation (assembly.cpp:125-126)
-    const double2 A = o == 0 ? pv[(l + 1) % 3] : pv[(l + 2) % 3];
-    const double2 Bn = o == 0 ? pv[(l + 2) % 3] : pv[(l + 1) % 3];
-    const double dx = FSUB(Bn.x, A.x), dy = FSUB(Bn.y, A.y);
-    // edge_geometry (mesh.cpp:232-257): length and its reciprocal from one rsqrt
-    const double rh = rsqrt_nr(fma(dx, dx, dy * dy));
-    const double h = fma(dx, dx, dy * dy) * rh;
-    const double tx = dx * rh, ty = dy * rh;
-    const double nx = o == 0 ? ty : -ty, ny = o == 0 ? -tx : tx;
+    // edge_geometry (mesh.cpp:232-257): length and its reciprocal from one rsqrt, outward normal
+    double dx, dy, nx, ny;
+    p1_edge_dir(pv, l, dx, dy);
+    const double r2 = fma(dx, dx, FMUL(dy, dy));
+    const double rh = GEO ? (l == 0 ? gx[0].y : (l == 1 ? gx[1].x : gx[1].y)) : rsqrt_nr(r2);
+    const double h = r2 * rh;
+    p1_edge_normal(dx, dy, rh, nx, ny);
     const double ge0 = G00 * nx + G10 * ny, ge1 = G01 * nx + G11 * ny;
     const int kind = kindv[l], lf = lfv[l], f = fv[l];
     double w0 = 0.0, w1 = 0.0, cp = 0.0;
     if (kind == DGB_EDGE_INTERIOR) {
-      Geo gf;
-      if constexpr (bound) {
+      double2 gn;  // G_f^T n of the neighbour
+      if constexpr (GEO) {
+        gn = po[l];
+      } else if constexpr (bound) {
         // the neighbour in its vertex order rotated to (opposite, b, a): the trace table's
         // gradients are rotated to match (p1_tables<.., true>)
-        gf = element_geo_coords(po[l], pv[(l + 2) % 3], pv[(l + 1) % 3]);
+        gn = p1_neighbour_normal(po[l], pv[(l + 2) % 3], pv[(l + 1) % 3], nx, ny);
       } else {
-        gf = element_geo_fast(P.nodes, vfv[l]);
+        const Geo gf = element_geo_fast(P.nodes, vfv[l]);
+        gn = make_double2(fma(gf.G00, nx, FMUL(gf.G10, ny)), fma(gf.G01, nx, FMUL(gf.G11, ny)));
       }
       double eps_e = eps;
       if (P.prob.diffusion.kind == DGB_FIELD_PER_ELEMENT) {
@@ -221,8 +284,8 @@ __device__ __forceinline__ void p1_row(const Params2<3, NQV, NQE, false, true>& 
       const double base = 0.5 * h * eps_e;
       w0 = base * ge0;
       w1 = base * ge1;
-      const double cY0 = -base * (gf.G00 * nx + gf.G10 * ny);
-      const double cY1 = -base * (gf.G01 * nx + gf.G11 * ny);
+      const double cY0 = -base * gn.x;
+      const double cY1 = -base * gn.y;
       const double cZ0 = -kappa * base * ge0;
       const double cZ1 = -kappa * base * ge1;
       const double sh = sigma_i * rh;
@@ -281,13 +344,16 @@ __device__ __forceinline__ void p1_row(const Params2<3, NQV, NQE, false, true>& 
       }
     } else {
       // boundary edge: diffusion (Dirichlet), inflow upwind, and the boundary RHS terms
+      const int o = GEO ? (anb.w >> (20 + l)) & 1 : (v[(l + 1) % 3] < v[(l + 2) % 3] ? 0 : 1);
+      const double2 A = o == 0 ? pv[(l + 1) % 3] : pv[(l + 2) % 3];
       double fls[NQE], gb[NQE];
       bool inflow = false;
 #pragma unroll
       for (int p = 0; p < NQE; ++p) {
+        // make_side orientation (assembly.cpp:125-126): the points run from the lower vertex id
         const double tq = o == 0 ? P.t.x[L::ET + p] : 1.0 - P.t.x[L::ET + p];
-        const double px = FADD(A.x, FMUL(tq, dx));
-        const double py = FADD(A.y, FMUL(tq, dy));
+        const double px = FADD(A.x, FMUL(tq, o == 0 ? dx : -dx));
+        const double py = FADD(A.y, FMUL(tq, o == 0 ? dy : -dy));
         fls[p] = FADD(FMUL(bf.p[0], nx), FMUL(bf.p[1], ny));
         if (fls[p] < -1e-12 * fmax(1.0, hypot_dd(bf.p[0], bf.p[1]))) inflow = true;
         gb[p] = scalar_point(kind == DGB_EDGE_NEUMANN ? P.prob.neumann : P.prob.dirichlet, px, py);
@@ -358,7 +424,7 @@ __device__ __forceinline__ void p1_row(const Params2<3, NQV, NQE, false, true>& 
     for (int idx = bulk + lane; idx < n_here * NL; idx += 32) dst[idx] = srhs[idx];
   }
   // ---- the warp's row range: one bulk copy, unaligned head / tail by hand ----------------------------
-  if (wait_stage) {
+  if (wait_stage && DGB_P1_BULK_OUT == 0) {
     // persistent kernel: the warp copies its range itself (16-byte coalesced stores), so the
     // staging is free again at once -- the bulk copy's read-back wait was 15% of the stall
     // samples (profiles/NOTES.md)
@@ -445,8 +511,10 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_p1_kernel(
     po[1] = hints ? ld_hint(nodes2 + max(aop.y, 0), pol_g) : __ldg(nodes2 + max(aop.y, 0));
     po[2] = hints ? ld_hint(nodes2 + max(aop.z, 0), pol_g) : __ldg(nodes2 + max(aop.z, 0));
   }
-  p1_row<NQV, NQE, BOUND>(P, tr, mset, stw, DGB_ABLATE(128) ? srhs : nullptr, lane, blockIdx.x * blockDim.x + warp * 32, ee,
-                          active, v, anb, aop, rp, rp_next, pv, po, false, [] {});
+  const double2 gx[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
+  p1_row<NQV, NQE, BOUND, false>(P, tr, mset, stw, DGB_ABLATE(128) ? srhs : nullptr, lane,
+                                 blockIdx.x * blockDim.x + warp * 32, ee, active, v, anb, aop, rp, rp_next, pv,
+                                 po, gx, false, [] {});
   if (lane == 0) bulk_wait_all();
 }
 
@@ -470,25 +538,27 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_p1_kernel(
 //
 // Each lane reads only what it copied itself, so the per-thread cp.async groups are the only
 // synchronisation on the input side.
-template <int NQV, int NQE, int WARPS>
+template <int NQV, int NQE, int WARPS, bool GEO>
 struct SmemP1Pipe {
   using SM = SmemP1<NQV, NQE>;
   static constexpr int kNb = ChunkRec::kNb, kOp = ChunkRec::kOp, kV = ChunkRec::kV,
                        kRp = ChunkRec::kRp, kRpn = ChunkRec::kRpn, kIdxInts = ChunkRec::kIdxInts;
-  static constexpr int kIdx = ChunkRec::kIdx, kNode = ChunkRec::kNode;
+  static constexpr int kIdx = ChunkRec::kIdx, kNode = GEO ? ChunkRec::kNode2 : ChunkRec::kNode;
   static constexpr int kWarp = kIdx + kNode + SM::kStage;  // RHS stored directly
   static constexpr size_t kBytes = sizeof(double) * (size_t(SM::kTr) + size_t(WARPS) * kWarp);
 };
 
-
-
+// GEO: the chunk's geometry record bound by dgb_plan_bind_mesh (geometry_kernel) replaces the
+// node gathers.  Chunks are dealt round-robin: measured (tools/p1_diag.py) the SMs finish within
+// 0.5% of one another, and handing chunks out through an atomic ticket counter cost 6% (the
+// ticket's round trip under the write stream), so the static order stays.
 template <int NQV, int NQE, int WARPS, bool GEO>
 __global__ void __launch_bounds__(WARPS * 32, 1) assemble_p1_pipe_kernel(
     const __grid_constant__ Params2<3, NQV, NQE, false, true> P) {
   constexpr int NL = 3;
   using L = Lay<NL, NQV, NQE, false, true>;
   using SM = SmemP1<NQV, NQE>;
-  using PS = SmemP1Pipe<NQV, NQE, WARPS>;
+  using PS = SmemP1Pipe<NQV, NQE, WARPS, GEO>;
   extern __shared__ double smem[];
   double* tr = smem;
   p1_tables<NQV, NQE, true>(P, tr);
@@ -497,31 +567,38 @@ __global__ void __launch_bounds__(WARPS * 32, 1) assemble_p1_pipe_kernel(
   const int mset = blockIdx.y;
   double* wbase = smem + SM::kTr + warp * PS::kWarp;
   int* idx = reinterpret_cast<int*>(wbase);                     // one chunk's records
-  double2* nod = reinterpret_cast<double2*>(wbase + PS::kIdx);  // one chunk's nodes [6][32]
+  double2* nod = reinterpret_cast<double2*>(wbase + PS::kIdx);  // one chunk's nodes / geometry
   double* stw = wbase + PS::kIdx + PS::kNode;
   double* srhs = nullptr;  // RHS stored directly (shared memory for 16 warps)
+#ifdef DGB_TUNING
+  unsigned long long t_begin = 0, c_begin = 0;
+  int n_done = 0;
+  if (P.diag) {
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_begin));
+    c_begin = clock64();
+  }
+#endif
 
   const int n_rows = P.row_end - P.row_begin;
   const int n_chunks = (n_rows + 31) >> 5;
   const int gw = blockIdx.x * WARPS + warp, n_gw = gridDim.x * WARPS;
-  const int n_local = gw < n_chunks ? (n_chunks - 1 - gw) / n_gw + 1 : 0;
   const double2* nodes2 = reinterpret_cast<const double2*>(P.nodes);
 
-  auto issue_records = [&](int j) {
-    const int e = P.row_begin + (gw + j * n_gw) * 32 + lane;
+  auto issue_records = [&](int c) {
+    const int e = P.row_begin + c * 32 + lane;
     const int r = min(e, P.row_end - 1) - P.row_begin;
     cp_async16(idx + PS::kNb + 4 * lane, P.adj_nb + r);
     if constexpr (GEO) {
-      // the chunk's vertex coordinates from the bound record: six coalesced 16-byte copies per
-      // lane, in flight together with the index records (no dependent gather)
-      const double2* g = P.geo + static_cast<size_t>(gw + j * n_gw) * (6 * 32) + lane;
+      // the chunk's geometry record: eight coalesced 16-byte copies per lane, in flight
+      // together with the index records (no dependent gather)
+      const double2* g = P.geo + static_cast<size_t>(c) * (8 * 32) + lane;
 #pragma unroll
-      for (int k = 0; k < 6; ++k) cp_async16(nod + k * 32 + lane, g + k * 32);
+      for (int k = 0; k < 8; ++k) cp_async16(nod + k * 32 + lane, g + k * 32);
     } else {
       cp_async16(idx + PS::kOp + 4 * lane, P.adj_op + r);
-    }
 #pragma unroll
-    for (int k = 0; k < 3; ++k) cp_async4(idx + PS::kV + 3 * lane + k, P.elements + 3 * (P.row_begin + r) + k);
+      for (int k = 0; k < 3; ++k) cp_async4(idx + PS::kV + 3 * lane + k, P.elements + 3 * (P.row_begin + r) + k);
+    }
     cp_async4(idx + PS::kRp + lane, P.row_ptr_src + r);
     cp_async4(idx + PS::kRpn + lane, P.row_ptr_src + r + 1);
     cp_async_commit();
@@ -543,41 +620,74 @@ __global__ void __launch_bounds__(WARPS * 32, 1) assemble_p1_pipe_kernel(
     }
     cp_async_commit();
   };
-
-  if (n_local > 0) {
-    issue_records(0);
+  int c_cur = gw, c_next = gw + n_gw;
+  if (c_cur < n_chunks) {
+    issue_records(c_cur);
     if constexpr (!GEO) {
       cp_async_wait_all();
       issue_nodes();
     }
   }
 #pragma unroll 1
-  for (int j = 0; j < n_local; ++j) {
-    cp_async_wait_all();  // chunk j's records and nodes have landed
-    // everything of chunk j into registers; the buffers take chunk j + 1 from here on
-    const int v[3] = {idx[PS::kV + 3 * lane], idx[PS::kV + 3 * lane + 1], idx[PS::kV + 3 * lane + 2]};
+  while (c_cur < n_chunks) {
+    cp_async_wait_all();  // this chunk's records and nodes have landed
+    // everything of the chunk into registers; the buffers take the next chunk from here on
+    int v[3] = {0, 0, 0};
+    if constexpr (!GEO) {
+#pragma unroll
+      for (int k = 0; k < 3; ++k) v[k] = idx[PS::kV + 3 * lane + k];
+    }
     const int4 anb = *reinterpret_cast<const int4*>(idx + PS::kNb + 4 * lane);
     const int4 aop = GEO ? make_int4(0, 0, 0, 0) : *reinterpret_cast<const int4*>(idx + PS::kOp + 4 * lane);
     const int rp = idx[PS::kRp + lane], rp_next = idx[PS::kRpn + lane];
     const double2 pv[3] = {nod[lane], nod[32 + lane], nod[64 + lane]};
     const double2 po[3] = {nod[96 + lane], nod[128 + lane], nod[160 + lane]};
-    const bool more = j + 1 < n_local;
-    if (more) issue_records(j + 1);
-    const int e_first = (gw + j * n_gw) * 32;
+    double2 gx[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
+    if constexpr (GEO) {
+      gx[0] = nod[192 + lane];
+      gx[1] = nod[224 + lane];
+    }
+    const bool more = c_next < n_chunks;
+    if (more) issue_records(c_next);
+    const int e_first = c_cur * 32;
     const int e = P.row_begin + e_first + lane;
     const bool active = e < P.row_end;
     const int ee = active ? e : P.row_end - 1;
-    p1_row<NQV, NQE, true>(P, tr, mset, stw, srhs, lane, e_first, ee, active, v, anb, aop, rp,
-                           rp_next, pv, po, true, [&] {
-                             if constexpr (!GEO) {
-                               if (more) {
-                                 cp_async_wait_all();  // chunk j + 1's records
-                                 issue_nodes();
-                               }
-                             }
-                           });
+    p1_row<NQV, NQE, true, GEO>(P, tr, mset, stw, srhs, lane, e_first, ee, active, v, anb, aop, rp,
+                                rp_next, pv, po, gx, true, [&] {
+                                  if constexpr (DGB_P1_BULK_OUT != 0) {
+                                    // the previous chunk's row range has left the staging (its bulk
+                                    // copy was issued a whole volume phase ago)
+                                    if (lane == 0) bulk_wait_read();
+                                    __syncwarp();
+                                  }
+                                  if constexpr (!GEO) {
+                                    if (more) {
+                                      cp_async_wait_all();  // the next chunk's records
+                                      issue_nodes();
+                                    }
+                                  }
+                                });
+    c_cur = c_next;
+    c_next += n_gw;
+#ifdef DGB_TUNING
+    ++n_done;
+#endif
   }
   if (lane == 0) bulk_wait_all();
+#ifdef DGB_TUNING
+  if (P.diag && lane == 0) {
+    unsigned long long t_end;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    unsigned long long* d = P.diag + 4 * (static_cast<size_t>(mset) * n_gw + gw);
+    d[0] = t_begin;
+    d[1] = t_end;
+    d[2] = clock64() - c_begin;
+    d[3] = (static_cast<unsigned long long>(n_done) << 32) | smid;
+  }
+#endif
 }
 
 }  // namespace v2

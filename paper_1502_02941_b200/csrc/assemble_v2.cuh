@@ -93,6 +93,7 @@ struct Params2 {
   const double2* geo;            // bound vertex coordinates per 32-row chunk [chunk][6][32]: own
                                  // vertices 0..2, the neighbours' opposite vertices 3..5; or null
   unsigned long long* err_edge;  // epoch << 32 | ~edge, max-reduced (lowest edge wins)
+  unsigned long long* diag;      // tuning builds: per-warp timing record, or null
   unsigned long long epoch;
   int32_t n_elements;
   int32_t row_begin, row_end;  // block rows [row_begin, row_end) of this launch (a shard)
@@ -182,6 +183,7 @@ struct ChunkRec {
   static constexpr int kNb = 0, kOp = 128, kV = 256, kRp = 352, kRpn = 384, kIdxInts = 416;
   static constexpr int kIdx = kIdxInts / 2;      // doubles
   static constexpr int kNode = 32 * 6 * 2;       // doubles
+  static constexpr int kNode2 = 32 * 8 * 2;      // doubles (extended geometry record)
 };
 
 __device__ __forceinline__ void bulk_wait_read() {

@@ -215,9 +215,22 @@ __device__ __forceinline__ double scalar_point_inline(const dgb_scalar_field& f,
 #define DGB_SRC_UNROLL 1
 #endif
 constexpr int kSrcUnroll = DGB_SRC_UNROLL;  // Gaussian source point loop (tuning: -DDGB_SRC_UNROLL)
-template <int NQV, bool UseXY, class XY, class USE>
+#ifndef DGB_SRC_FAST_UNROLL
+#define DGB_SRC_FAST_UNROLL 6
+#endif
+constexpr int kSrcFastUnroll = DGB_SRC_FAST_UNROLL;  // branch-free Gaussian point loop
+// No bound on the element's extent: the Gaussian source keeps its per-point range check.
+struct NoExtent {
+  static constexpr bool kKnown = false;
+  __device__ __forceinline__ double operator()(double, double) const { return -1.0; }
+};
+// EXTENT (optional): r2max(cx, cy) = the largest squared distance from (cx, cy) to a vertex of
+// the element, called by every lane of the warp; the volume points are convex combinations of
+// the vertices, so r^2 <= r2max at each of them.
+template <int NQV, bool UseXY, class XY, class USE, class EXTENT = NoExtent>
 __device__ __forceinline__ void source_points(const dgb_scalar_field& fs, int e, bool skip, XY xy,
-                                              USE use, int q_first = 0, int q_step = 1) {
+                                              USE use, int q_first = 0, int q_step = 1,
+                                              EXTENT r2max = EXTENT{}) {
   if (fs.kind == DGB_FIELD_PER_ELEMENT || fs.kind == DGB_FIELD_CONSTANT) {
     const double f = fs.kind == DGB_FIELD_PER_ELEMENT ? __ldg(fs.per_element + e) : fs.value;
 #pragma unroll 1
@@ -258,6 +271,22 @@ __device__ __forceinline__ void source_points(const dgb_scalar_field& fs, int e,
       const double a = fs.p[0], cx = fs.p[1], cy = fs.p[2];
       const double K0 = fma(4.0 * a, q1, q0), K1 = -4.0 * a * a * q1;
       const double K2 = -2.0 * a * q2, K3 = -2.0 * a * q3;
+      if constexpr (EXTENT::kKnown) {
+        // every point's exponent is inside exp_core's range (checked once, at the vertices, for
+        // the whole warp): the point loop is branch-free, so unrolled points overlap
+        if (__all_sync(0xffffffffu, fabs(a) * r2max(cx, cy) < 708.0)) {
+#pragma unroll kSrcFastUnroll
+          for (int q = q_first; q < NQV; q += q_step) {
+            double x, y;
+            xy(q, x, y);
+            const double dx = x - cx, dy = y - cy;
+            const double r2 = fma(dx, dx, dy * dy);
+            const double v = exp_core(-a * r2);
+            use(q, v * fma(K1, r2, fma(K2, dx, fma(K3, dy, K0))), x, y);
+          }
+          return;
+        }
+      }
 #pragma unroll kSrcUnroll
       for (int q = q_first; q < NQV; q += q_step) {
         double x, y;
@@ -419,7 +448,7 @@ __global__ void count_blocks_kernel(const uint8_t* __restrict__ edge_kind,
 
 // Element adjacency record of rows [begin, begin + n) (bound once per mesh): per local edge l
 // the neighbour element, the neighbour's vertex opposite the shared edge, and kind | lf << 2 in
-// bits 4l..4l+3 of nb.w.  Replaces the per-assembly chain element_edges -> edge_elements ->
+// bits 4l..4l+3 of nb.w (bits 12..25: block slots, edge orientations, block count).  Replaces the per-assembly chain element_edges -> edge_elements ->
 // elements[f] of dependent gathers (the "geometry / neighbour precompute" of the north star).
 __global__ void adjacency_kernel(const int32_t* __restrict__ elements,
                                  const uint8_t* __restrict__ edge_kind,
@@ -450,33 +479,73 @@ __global__ void adjacency_kernel(const int32_t* __restrict__ elements,
       nbr[l] = f;
     }
     meta |= (kind | (lf << 2)) << (4 * l);
+    // make_side orientation of local edge l (assembly.cpp:125-126): 1 when a > b
+    const int a = __ldg(elements + 3 * e + (l + 1) % 3), b = __ldg(elements + 3 * e + (l + 2) % 3);
+    meta |= (a < b ? 0 : 1) << (20 + l);
+  }
+  {
+    // slots of the row's blocks (rank among its sorted block columns) in bits 12..19: the
+    // diagonal, then local edges 0..2; the row's block count in bits 23..25
+    const int cx[4] = {e, nbr[0], nbr[1], nbr[2]};
+    int n_blocks = 1;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      int rank = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) rank += (j != i && cx[j] >= 0 && cx[j] < cx[i]) ? 1 : 0;
+      meta |= rank << (12 + 2 * i);
+      if (i > 0 && cx[i] >= 0) ++n_blocks;
+    }
+    meta |= n_blocks << 23;
   }
   nb[r] = make_int4(nbr[0], nbr[1], nbr[2], meta);
   op[r] = make_int4(opp[0], opp[1], opp[2], 0);
 }
 
-// Vertex coordinates of rows [begin, begin + n) per 32-row chunk (bound once per mesh, the P1
-// persistent kernel): geo[(chunk * 6 + k) * 32 + lane] = the element's own vertices (k = 0..2)
-// and its neighbours' vertices opposite the shared edges (k = 3..5; a boundary edge repeats
-// node 0, unused).  The block-row kernel then reads its coordinates with coalesced 16-byte
-// copies instead of six random gathers per element (the "geometry precompute" of the north
-// star); the values are copies of mesh->nodes, so results are bitwise the same.  Lanes past the
-// last row repeat it.
+// Geometry record of rows [begin, begin + n) per 32-row chunk (bound once per mesh, the P1
+// persistent kernel; the "geometry precompute" of the north star):
+//   geo[(chunk * 8 + k) * 32 + lane], k = 0..2: the element's own vertices
+//                                     k = 3..5: G_f^T n of the neighbour across local edge k - 3
+//                                               (the neighbour's inverse-transposed Jacobian in
+//                                               its (opposite, b, a) vertex order applied to
+//                                               this element's outward normal; 0 on a boundary)
+//                                     k = 6, 7: (1 / det, 1 / h_0), (1 / h_1, 1 / h_2)
+// The block-row kernel then reads its geometry with coalesced 16-byte copies: no random node
+// gathers, no reciprocals or reciprocal square roots, no neighbour Jacobians.  The values come
+// from the same device functions the kernels without a record use (p1_edge_frame,
+// p1_neighbour_normal), so results are bitwise the same.  Lanes past the last row repeat it.
 __global__ void geometry_kernel(const double* __restrict__ nodes, const int32_t* __restrict__ elements,
-                                const int4* __restrict__ op, int32_t begin, int32_t n,
-                                double2* __restrict__ geo) {
+                                const int4* __restrict__ nb, const int4* __restrict__ op,
+                                int32_t begin, int32_t n, double2* __restrict__ geo) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= ((n + 31) & ~31)) return;
   const int r = min(t, n - 1);
   const int e = begin + r;
   const double2* nodes2 = reinterpret_cast<const double2*>(nodes);
   const int4 o = __ldg(op + r);
-  double2* g = geo + static_cast<size_t>(t >> 5) * (6 * 32) + (t & 31);
+  const int meta = __ldg(nb + r).w;
+  double2* g = geo + static_cast<size_t>(t >> 5) * (8 * 32) + (t & 31);
+  double2 pv[3];
 #pragma unroll
-  for (int k = 0; k < 3; ++k) g[k * 32] = __ldg(nodes2 + __ldg(elements + 3 * e + k));
-  g[3 * 32] = __ldg(nodes2 + max(o.x, 0));
-  g[4 * 32] = __ldg(nodes2 + max(o.y, 0));
-  g[5 * 32] = __ldg(nodes2 + max(o.z, 0));
+  for (int k = 0; k < 3; ++k) pv[k] = __ldg(nodes2 + __ldg(elements + 3 * e + k));
+  const int opp[3] = {o.x, o.y, o.z};
+  double rh[3];
+#pragma unroll
+  for (int l = 0; l < 3; ++l) {
+    const v2::EdgeFrame fr = v2::p1_edge_frame(pv, l);
+    rh[l] = fr.rh;
+    double2 gn = make_double2(0.0, 0.0);
+    if (((meta >> (4 * l)) & 3) == DGB_EDGE_INTERIOR) {
+      gn = v2::p1_neighbour_normal(__ldg(nodes2 + opp[l]), pv[(l + 2) % 3], pv[(l + 1) % 3], fr.nx, fr.ny);
+    }
+    g[(3 + l) * 32] = gn;
+  }
+#pragma unroll
+  for (int k = 0; k < 3; ++k) g[k * 32] = pv[k];
+  const double det = FSUB(FMUL(FSUB(pv[1].x, pv[0].x), FSUB(pv[2].y, pv[0].y)),
+                          FMUL(FSUB(pv[2].x, pv[0].x), FSUB(pv[1].y, pv[0].y)));
+  g[6 * 32] = make_double2(rcp_nr(det), rh[0]);
+  g[7 * 32] = make_double2(rh[1], rh[2]);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -1079,6 +1148,7 @@ struct dgb_plan {
   // DMMA B fragments of the diagonal terms, one table per kappa (W depends on kappa)
   std::vector<std::pair<double, double*>> bfrag_cache;
   int ablate = 0;  // profiling diagnostics (dgb_plan_set_option 1000)
+  unsigned long long* d_diag = nullptr;  // tuning builds: per-warp timing records (not owned)
   // nonlinear reaction Jacobian: Phi_q,(i,j) = phi_qj phi_qi as DMMA B fragments [ks][nt][lane]
   double* d_nlfrag = nullptr;
   int nl_ks = 0;
@@ -1177,6 +1247,7 @@ void launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_prob
     if (plan->d_geo && plan->geo_cache > 0 && plan->bound_nodes == mesh->nodes) P.geo = plan->d_geo;
   }
   P.err_edge = plan->d_err;
+  P.diag = plan->d_diag;
   P.epoch = plan->epoch & 0xFFFFFFFFull;
   P.n_elements = mesh->n_elements;
   P.row_begin = out_row_begin;
@@ -1514,11 +1585,11 @@ void launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_prob
         cuda_check(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev), "sm count");
         const_cast<dgb_plan*>(plan)->sm_count = n;
       }
-      auto launch = [&](auto tag) {
+      auto launch = [&](auto tag, auto geo_tag) {
         constexpr int W = decltype(tag)::value;
-        using PS = dgb::v2::SmemP1Pipe<NQV, NQE, W>;
-        auto pk = P.geo ? dgb::v2::assemble_p1_pipe_kernel<NQV, NQE, W, true>
-                        : dgb::v2::assemble_p1_pipe_kernel<NQV, NQE, W, false>;
+        constexpr bool GEO = decltype(geo_tag)::value;
+        using PS = dgb::v2::SmemP1Pipe<NQV, NQE, W, GEO>;
+        auto pk = dgb::v2::assemble_p1_pipe_kernel<NQV, NQE, W, GEO>;
         dgb::ensure_dynamic_smem(reinterpret_cast<const void*>(pk), PS::kBytes, "cudaFuncSetAttribute(p1 pipe)");
         const int n_chunks = (out_row_end - out_row_begin + 31) / 32;
         cfg.gridDim = dim3(std::max(1, std::min(plan->sm_count, (n_chunks + W - 1) / W)), nb);
@@ -1529,7 +1600,11 @@ void launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_prob
       // 12 warps per CTA (one CTA per SM) at 166 registers.  Registers are allocated per SM
       // sub-partition, so 13-15 warps get 128 like 16; 16 warps spilled and measured slower
       // (1.103 vs 1.073 ms) and was removed.
-      launch(std::integral_constant<int, 12>{});
+      if (P.geo) {
+        launch(std::integral_constant<int, 12>{}, std::true_type{});
+      } else {
+        launch(std::integral_constant<int, 12>{}, std::false_type{});
+      }
       return;
     }
   }
@@ -1755,7 +1830,7 @@ int dgb_plan_bind_mesh(dgb_plan* plan, const dgb_mesh_arrays* mesh, int32_t row_
     } else {
       cuda_check(cudaMemsetAsync(plan->d_pattern, 0, sizeof(int32_t), s), "cudaMemsetAsync");
     }
-    // P1 persistent kernel: the rows' vertex coordinates in chunk order (96 B per element)
+    // P1 persistent kernel: the rows' geometry record in chunk order (128 B per element)
     plan->bound_nodes = nullptr;
     const bool want_geo = plan->nl == 3 && plan->p1_pipe > 0 && plan->geo_cache > 0 && rows > 0;
     if (want_geo) {
@@ -1764,11 +1839,12 @@ int dgb_plan_bind_mesh(dgb_plan* plan, const dgb_mesh_arrays* mesh, int32_t row_
         cudaFree(plan->d_geo);
         plan->d_geo = nullptr;
         plan->geo_cap = 0;
-        cuda_check(cudaMalloc(&plan->d_geo, padded * 6 * sizeof(double2)), "cudaMalloc(geometry)");
+        cuda_check(cudaMalloc(&plan->d_geo, padded * 8 * sizeof(double2)), "cudaMalloc(geometry)");
         plan->geo_cap = padded;
       }
       dgb::geometry_kernel<<<static_cast<unsigned>((padded + 255) / 256), 256, 0, s>>>(
-          mesh->nodes, mesh->elements, plan->d_adj + rows, row_begin, row_end - row_begin, plan->d_geo);
+          mesh->nodes, mesh->elements, plan->d_adj, plan->d_adj + rows, row_begin, row_end - row_begin,
+          plan->d_geo);
       cuda_check(cudaGetLastError(), "geometry_kernel");
       plan->bound_nodes = mesh->nodes;
     } else if (plan->d_geo) {
@@ -2141,6 +2217,16 @@ int dgb_plan_set_kernel_events(dgb_plan* plan, void* start, void* stop) {
   plan->ev_stop = static_cast<cudaEvent_t>(stop);
   return DGB_OK;
 }
+
+#ifdef DGB_TUNING
+// Tuning builds only: per-warp timing records of the persistent P1 kernel (4 words per warp:
+// globaltimer at entry and exit, SM cycles in between, chunks << 32 | smid); not in the header.
+extern "C" int dgb_tuning_set_diag(dgb_plan* plan, void* device_words) {
+  if (!plan) return DGB_STATUS_INVALID_ARGUMENT;
+  plan->d_diag = static_cast<unsigned long long*>(device_words);
+  return DGB_OK;
+}
+#endif
 
 int dgb_plan_set_option(dgb_plan* plan, int32_t option, int32_t value) {
   if (!plan) return DGB_STATUS_INVALID_ARGUMENT;
