@@ -16,6 +16,14 @@
 #ifndef DGB_P1_BULK_OUT
 #define DGB_P1_BULK_OUT 1
 #endif
+// The volume RHS term (the source at the volume points) may run after the copy-out has been
+// issued instead of before the diagonal block (p1_row's kSrcLate).  Measured same-box on the
+// specialised kernels: late is 8% faster with the sine-product source (config-1 batch 0.151 ->
+// 0.140 ms) and 3% slower with the Gaussian (config 4 0.664 -> 0.686 ms), so it is chosen per
+// source family; -DDGB_P1_SRC_LATE=0/1 forces it for A/B runs.
+#ifndef DGB_P1_SRC_LATE
+#define DGB_P1_SRC_LATE -1
+#endif
 
 namespace dgb {
 namespace v2 {
@@ -112,10 +120,11 @@ struct VertexExtent {
 // staging is reused by the next chunk, so the warp copies its row range out itself.
 // `mid()` runs between the volume terms and the edge loop (the persistent kernel issues the next
 // chunk's node gathers there).
+// SRC: the source family the kernel is specialised for (source_points' ONLY).
 // GEO (persistent kernel, bound geometry record): po[l] holds the neighbour's G_f^T n and gx the
 // reciprocals (1 / det, 1 / h_0), (1 / h_1, 1 / h_2); slots, orientations and the block count
 // come from the adjacency word.
-template <int NQV, int NQE, bool BOUND, bool GEO, class MID>
+template <int NQV, int NQE, bool BOUND, bool GEO, int SRC, class MID>
 __device__ __forceinline__ void p1_row(const Params2<3, NQV, NQE, false, true>& P, const double* tr,
                                        int mset, double* stw, double* srhs, int lane, int e_first,
                                        int ee, bool active, const int (&v)[3], int4 anb, int4 aop,
@@ -207,12 +216,15 @@ __device__ __forceinline__ void p1_row(const Params2<3, NQV, NQE, false, true>& 
     return;
   }
 
-  // RHS volume term
+  // RHS volume term.  kSrcLate: evaluated after the row range's copy-out has been issued
+  // (the source needs no staging, so the copy engine drains the staging meanwhile); the boundary
+  // terms of the edge loop then come first in F's sums (a boundary element's F differs in the
+  // last bit from the early order).
   double F[NL];
 #pragma unroll
   for (int i = 0; i < NL; ++i) F[i] = 0.0;
-  {
-    source_points<NQV, false>(
+  auto volume_rhs = [&] {
+    source_points<NQV, false, SRC>(
         P.prob.source, ee, DGB_ABLATE(2),
         [&](int q, double& px, double& py) {
           // volume points only evaluate coefficients (no term selection): fused
@@ -225,7 +237,9 @@ __device__ __forceinline__ void p1_row(const Params2<3, NQV, NQE, false, true>& 
           for (int i = 0; i < NL; ++i) F[i] = fma(c, P.t.x[L::PHI + q * NL + i], F[i]);
         },
         0, 1, VertexExtent{pv});
-  }
+  };
+  constexpr bool kSrcLate = DGB_P1_SRC_LATE < 0 ? SRC == SRC_SIN_SIN : DGB_P1_SRC_LATE != 0;
+  if constexpr (!kSrcLate) volume_rhs();
 
   // diagonal block: volume terms (registers)
   double acc[N2];
@@ -346,8 +360,11 @@ __device__ __forceinline__ void p1_row(const Params2<3, NQV, NQE, false, true>& 
       // boundary edge: diffusion (Dirichlet), inflow upwind, and the boundary RHS terms
       const int o = GEO ? (anb.w >> (20 + l)) & 1 : (v[(l + 1) % 3] < v[(l + 2) % 3] ? 0 : 1);
       const double2 A = o == 0 ? pv[(l + 1) % 3] : pv[(l + 2) % 3];
+      const dgb_scalar_field& bfld = kind == DGB_EDGE_NEUMANN ? P.prob.neumann : P.prob.dirichlet;
+      const bool bfast = boundary_fast_ok(bfld, pv[(l + 1) % 3], pv[(l + 2) % 3]);
       double fls[NQE], gb[NQE];
       bool inflow = false;
+      const double inflow_tol = -1e-12 * fmax(1.0, hypot_dd(bf.p[0], bf.p[1]));
 #pragma unroll
       for (int p = 0; p < NQE; ++p) {
         // make_side orientation (assembly.cpp:125-126): the points run from the lower vertex id
@@ -355,8 +372,8 @@ __device__ __forceinline__ void p1_row(const Params2<3, NQV, NQE, false, true>& 
         const double px = FADD(A.x, FMUL(tq, o == 0 ? dx : -dx));
         const double py = FADD(A.y, FMUL(tq, o == 0 ? dy : -dy));
         fls[p] = FADD(FMUL(bf.p[0], nx), FMUL(bf.p[1], ny));
-        if (fls[p] < -1e-12 * fmax(1.0, hypot_dd(bf.p[0], bf.p[1]))) inflow = true;
-        gb[p] = scalar_point(kind == DGB_EDGE_NEUMANN ? P.prob.neumann : P.prob.dirichlet, px, py);
+        if (fls[p] < inflow_tol) inflow = true;
+        gb[p] = scalar_point_fast(bfld, px, py, bfast);
       }
       double cG[NQE], cH[NQE];
       if (kind == DGB_EDGE_NEUMANN) {
@@ -407,27 +424,9 @@ __device__ __forceinline__ void p1_row(const Params2<3, NQV, NQE, false, true>& 
     for (int k = 0; k < N2; ++k) myrow[slot_of[0] * N2 + k] = acc[k];
   }
 
-  // ---- RHS: the warp's contiguous slice in one bulk copy (srhs == nullptr: direct stores) ----------
-  if (srhs == nullptr) {
-    double* dst = o_rhs + static_cast<long long>(e_first + lane) * NL;
-#pragma unroll
-    for (int i = 0; i < NL; ++i) if (active) dst[i] = F[i];
-  } else {
-#pragma unroll
-    for (int i = 0; i < NL; ++i) srhs[lane * NL + i] = F[i];
-    fence_smem_to_async();  // every writer: its shared-memory stores -> the async (TMA) proxy
-    __syncwarp();
-    const int n_here = min(32, P.row_end - P.row_begin - e_first);
-    double* dst = o_rhs + static_cast<long long>(e_first) * NL;
-    const int bulk = (n_here * NL) & ~1;
-    if (lane == 0 && bulk > 0) bulk_store(dst, srhs, bulk * sizeof(double), P.evict_first);
-    for (int idx = bulk + lane; idx < n_here * NL; idx += 32) dst[idx] = srhs[idx];
-  }
   // ---- the warp's row range: one bulk copy, unaligned head / tail by hand ----------------------------
   if (wait_stage && DGB_P1_BULK_OUT == 0) {
-    // persistent kernel: the warp copies its range itself (16-byte coalesced stores), so the
-    // staging is free again at once -- the bulk copy's read-back wait was 15% of the stall
-    // samples (profiles/NOTES.md)
+    // the warp copies its range itself (16-byte coalesced stores)
     __syncwarp();
     const int n = (rp_last - rp_first) * N2;
     double* dst = o_val + static_cast<long long>(rp_first) * N2;
@@ -444,11 +443,11 @@ __device__ __forceinline__ void p1_row(const Params2<3, NQV, NQE, false, true>& 
     if (lane == 1 && head && n > 0) dst[0] = srow[0];
     if (lane == 2 && n > 0 && ((n - head) & 1)) dst[n - 1] = srow[n - 1];
     __syncwarp();
-    return;
-  }
-  fence_smem_to_async();  // every writer: its staged blocks -> the async (TMA) proxy
-  __syncwarp();
-  {
+  } else {
+    // (persistent kernel: the staging is reused by the next chunk, which waits for this copy's
+    // read of it after its own volume terms -- the `mid` hook)
+    fence_smem_to_async();  // every writer: its staged blocks -> the async (TMA) proxy
+    __syncwarp();
     const int n = (rp_last - rp_first) * N2;
     double* dst = o_val + static_cast<long long>(rp_first) * N2;
     const int head = rp_first & 1;
@@ -457,6 +456,24 @@ __device__ __forceinline__ void p1_row(const Params2<3, NQV, NQE, false, true>& 
     // (a warp past the last row has no range: n <= 0, nothing to write)
     if (lane == 1 && head && n > 0) dst[0] = srow[0];
     if (lane == 2 && n > 0 && head + body < n) dst[n - 1] = srow[n - 1];
+  }
+  if constexpr (kSrcLate) volume_rhs();
+
+  // ---- RHS: direct stores (srhs == nullptr), or the warp's contiguous slice in one bulk copy --------
+  if (srhs == nullptr) {
+    double* dst = o_rhs + static_cast<long long>(e_first + lane) * NL;
+#pragma unroll
+    for (int i = 0; i < NL; ++i) if (active) dst[i] = F[i];
+  } else {
+#pragma unroll
+    for (int i = 0; i < NL; ++i) srhs[lane * NL + i] = F[i];
+    fence_smem_to_async();  // every writer: its shared-memory stores -> the async (TMA) proxy
+    __syncwarp();
+    const int n_here = min(32, P.row_end - P.row_begin - e_first);
+    double* dst = o_rhs + static_cast<long long>(e_first) * NL;
+    const int bulk = (n_here * NL) & ~1;
+    if (lane == 0 && bulk > 0) bulk_store(dst, srhs, bulk * sizeof(double), P.evict_first);
+    for (int idx = bulk + lane; idx < n_here * NL; idx += 32) dst[idx] = srhs[idx];
   }
 }
 
@@ -512,7 +529,7 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_p1_kernel(
     po[2] = hints ? ld_hint(nodes2 + max(aop.z, 0), pol_g) : __ldg(nodes2 + max(aop.z, 0));
   }
   const double2 gx[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
-  p1_row<NQV, NQE, BOUND, false>(P, tr, mset, stw, DGB_ABLATE(128) ? srhs : nullptr, lane,
+  p1_row<NQV, NQE, BOUND, false, SRC_ANY>(P, tr, mset, stw, DGB_ABLATE(128) ? srhs : nullptr, lane,
                                  blockIdx.x * blockDim.x + warp * 32, ee, active, v, anb, aop, rp, rp_next, pv,
                                  po, gx, false, [] {});
   if (lane == 0) bulk_wait_all();
@@ -552,7 +569,7 @@ struct SmemP1Pipe {
 // node gathers.  Chunks are dealt round-robin: measured (tools/p1_diag.py) the SMs finish within
 // 0.5% of one another, and handing chunks out through an atomic ticket counter cost 6% (the
 // ticket's round trip under the write stream), so the static order stays.
-template <int NQV, int NQE, int WARPS, bool GEO>
+template <int NQV, int NQE, int WARPS, bool GEO, int SRC>
 __global__ void __launch_bounds__(WARPS * 32, 1) assemble_p1_pipe_kernel(
     const __grid_constant__ Params2<3, NQV, NQE, false, true> P) {
   constexpr int NL = 3;
@@ -653,7 +670,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) assemble_p1_pipe_kernel(
     const int e = P.row_begin + e_first + lane;
     const bool active = e < P.row_end;
     const int ee = active ? e : P.row_end - 1;
-    p1_row<NQV, NQE, true, GEO>(P, tr, mset, stw, srhs, lane, e_first, ee, active, v, anb, aop, rp,
+    p1_row<NQV, NQE, true, GEO, SRC>(P, tr, mset, stw, srhs, lane, e_first, ee, active, v, anb, aop, rp,
                                 rp_next, pv, po, gx, true, [&] {
                                   if constexpr (DGB_P1_BULK_OUT != 0) {
                                     // the previous chunk's row range has left the staging (its bulk

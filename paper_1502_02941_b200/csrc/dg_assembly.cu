@@ -193,6 +193,35 @@ __device__ __forceinline__ double scalar_point(const dgb_scalar_field& f, double
                          f.q[3], x, y);
 }
 
+// Boundary data g(x, y) on an edge with end points a, b, through the branch-free cores
+// (device_math.cuh) when the field is the VALUE of a sine-product or Gaussian family and the
+// edge lies inside the cores' ranges; otherwise scalar_point.  A boundary edge is evaluated by
+// one or two lanes of a warp while the others wait, so its instruction count is paid by all 32.
+__device__ __forceinline__ bool boundary_fast_ok(const dgb_scalar_field& f, double2 a, double2 b) {
+  if (f.kind != DGB_FIELD_FUNCTION || f.mode != DGB_MODE_VALUE) return false;
+  if (f.fn == DGB_FN_SIN_SIN) {
+    return fmax(fmax(fabs(a.x), fabs(a.y)), fmax(fabs(b.x), fabs(b.y))) < 1e8;
+  }
+  if (f.fn == DGB_FN_GAUSSIAN) {
+    const double ax = a.x - f.p[1], ay = a.y - f.p[2], bx = b.x - f.p[1], by = b.y - f.p[2];
+    return fabs(f.p[0]) * fmax(fma(ax, ax, ay * ay), fma(bx, bx, by * by)) < 708.0;
+  }
+  return false;
+}
+__device__ __forceinline__ double scalar_point_fast(const dgb_scalar_field& f, double x, double y, bool fast) {
+  if (fast) {
+    if (f.fn == DGB_FN_SIN_SIN) {
+      // the penalty multiplies g by sigma eps / h, so where F is small (g ~ 0 on the unit
+      // square's boundary) parity at 1e-12 needs the reference's sin(pi * x) of the ROUNDED
+      // product, not sin of the exact pi x
+      return f.p[0] * (sin_pi_product(x) * sin_pi_product(y));
+    }
+    const double dx = x - f.p[1], dy = y - f.p[2];
+    return exp_core(-f.p[0] * fma(dx, dx, dy * dy));
+  }
+  return scalar_point(f, x, y);
+}
+
 __device__ __forceinline__ double scalar_point_inline(const dgb_scalar_field& f, double x, double y) {
   if (f.kind == DGB_FIELD_CONSTANT) return f.value;
   double u, ux, uy, lap;
@@ -227,11 +256,26 @@ struct NoExtent {
 // EXTENT (optional): r2max(cx, cy) = the largest squared distance from (cx, cy) to a vertex of
 // the element, called by every lane of the warp; the volume points are convex combinations of
 // the vertices, so r^2 <= r2max at each of them.
-template <int NQV, bool UseXY, class XY, class USE, class EXTENT = NoExtent>
+// ONLY (a kernel specialised by the host for the source it will see, source_only()): the other
+// families' code is left out, which matters to a kernel whose hot loop is larger than the
+// instruction cache (the P1 persistent kernel gained 3% from it).
+enum SourceOnly { SRC_ANY = -1, SRC_CONST = 0, SRC_SIN_SIN = 1, SRC_GAUSSIAN = 2 };
+inline int source_only(const dgb_scalar_field& fs) {
+  if (fs.kind == DGB_FIELD_PER_ELEMENT || fs.kind == DGB_FIELD_CONSTANT) return SRC_CONST;
+  if (fs.kind == DGB_FIELD_FUNCTION && fs.mode == DGB_MODE_SOURCE) {
+    if (fs.fn == DGB_FN_SIN_SIN) return SRC_SIN_SIN;
+    if (fs.fn == DGB_FN_GAUSSIAN) return SRC_GAUSSIAN;
+  }
+  return SRC_ANY;
+}
+template <int NQV, bool UseXY, int ONLY = SRC_ANY, class XY, class USE, class EXTENT = NoExtent>
 __device__ __forceinline__ void source_points(const dgb_scalar_field& fs, int e, bool skip, XY xy,
                                               USE use, int q_first = 0, int q_step = 1,
                                               EXTENT r2max = EXTENT{}) {
-  if (fs.kind == DGB_FIELD_PER_ELEMENT || fs.kind == DGB_FIELD_CONSTANT) {
+  constexpr bool kAny = ONLY == SRC_ANY;
+  if constexpr (!kAny) skip = false;
+  if constexpr (kAny || ONLY == SRC_CONST) {
+  if (!kAny || fs.kind == DGB_FIELD_PER_ELEMENT || fs.kind == DGB_FIELD_CONSTANT) {
     const double f = fs.kind == DGB_FIELD_PER_ELEMENT ? __ldg(fs.per_element + e) : fs.value;
 #pragma unroll 1
     for (int q = q_first; q < NQV; q += q_step) {
@@ -241,7 +285,9 @@ __device__ __forceinline__ void source_points(const dgb_scalar_field& fs, int e,
     }
     return;
   }
-  if (!skip && fs.mode == DGB_MODE_SOURCE && fs.fn == DGB_FN_SIN_SIN) {
+  }
+  if constexpr (kAny || ONLY == SRC_SIN_SIN) {
+  if (!kAny || (!skip && fs.mode == DGB_MODE_SOURCE && fs.fn == DGB_FN_SIN_SIN)) {
     // u = p0 sin(pi x) sin(pi y): the source q0 u - q1 lap(u) + q2 u_x + q3 u_y regrouped as
     // p0 ((q0 + 2 pi^2 q1) sx sy + pi q2 cx sy + pi q3 sx cy), with sincospi: a cheaper
     // reduction than sincos of the rounded product pi * x (the reference's sin(pi * x) differs
@@ -249,6 +295,21 @@ __device__ __forceinline__ void source_points(const dgb_scalar_field& fs, int e,
     constexpr double pi = 3.14159265358979323846;
     const double A = fs.p[0] * fma(2.0 * pi * pi, fs.q[1], fs.q[0]);
     const double Bx = fs.p[0] * (pi * fs.q[2]), By = fs.p[0] * (pi * fs.q[3]);
+    if constexpr (EXTENT::kKnown) {
+      // every point's coordinates are inside sincospi_core's range (checked once, at the
+      // vertices, for the whole warp): branch-free point loop, unrolled points overlap
+      if (__all_sync(0xffffffffu, r2max(0.0, 0.0) < 1e16)) {
+#pragma unroll kSrcFastUnroll
+        for (int q = q_first; q < NQV; q += q_step) {
+          double x, y, sx, cx, sy, cy;
+          xy(q, x, y);
+          sincospi_core(x, sx, cx);
+          sincospi_core(y, sy, cy);
+          use(q, fma(A * sx, sy, fma(Bx * cx, sy, (By * sx) * cy)), x, y);
+        }
+        return;
+      }
+    }
 #pragma unroll 1
     for (int q = q_first; q < NQV; q += q_step) {
       double x, y, sx, cx, sy, cy;
@@ -259,9 +320,11 @@ __device__ __forceinline__ void source_points(const dgb_scalar_field& fs, int e,
     }
     return;
   }
-  if (!skip && fs.mode == DGB_MODE_SOURCE && (fs.fn == DGB_FN_GAUSSIAN || fs.fn == DGB_FN_TANH_LAYER)) {
+  }
+  if constexpr (kAny || ONLY == SRC_GAUSSIAN) {
+  if (!kAny || (!skip && fs.mode == DGB_MODE_SOURCE && (fs.fn == DGB_FN_GAUSSIAN || fs.fn == DGB_FN_TANH_LAYER))) {
     const double q0 = fs.q[0], q1 = fs.q[1], q2 = fs.q[2], q3 = fs.q[3];
-    if (fs.fn == DGB_FN_GAUSSIAN) {
+    if (!kAny || fs.fn == DGB_FN_GAUSSIAN) {
       // u = exp(-a r^2), r = (x - cx, y - cy): the source
       //   q0 u - q1 lap(u) + q2 u_x + q3 u_y = u (K0 + K1 r^2 + K2 dx + K3 dy),
       //   K0 = q0 + 4 a q1, K1 = -4 a^2 q1, K2 = -2 a q2, K3 = -2 a q3,
@@ -296,7 +359,7 @@ __device__ __forceinline__ void source_points(const dgb_scalar_field& fs, int e,
         const double v = exp_fast(-a * r2);
         use(q, v * fma(K1, r2, fma(K2, dx, fma(K3, dy, K0))), x, y);
       }
-    } else {
+    } else if constexpr (kAny) {
       const double gx = fs.p[0] / fs.p[3], gy = fs.p[1] / fs.p[3];
 #pragma unroll 1
       for (int q = q_first; q < NQV; q += q_step) {
@@ -308,11 +371,14 @@ __device__ __forceinline__ void source_points(const dgb_scalar_field& fs, int e,
     }
     return;
   }
+  }
+  if constexpr (kAny) {
 #pragma unroll 1
-  for (int q = q_first; q < NQV; q += q_step) {
-    double x, y;
-    xy(q, x, y);
-    use(q, skip ? x : scalar_point_inline(fs, x, y), x, y);
+    for (int q = q_first; q < NQV; q += q_step) {
+      double x, y;
+      xy(q, x, y);
+      use(q, skip ? x : scalar_point_inline(fs, x, y), x, y);
+    }
   }
 }
 
@@ -1585,11 +1651,12 @@ void launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_prob
         cuda_check(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev), "sm count");
         const_cast<dgb_plan*>(plan)->sm_count = n;
       }
-      auto launch = [&](auto tag, auto geo_tag) {
+      auto launch = [&](auto tag, auto geo_tag, auto src_tag) {
         constexpr int W = decltype(tag)::value;
         constexpr bool GEO = decltype(geo_tag)::value;
+        constexpr int SRC = decltype(src_tag)::value;
         using PS = dgb::v2::SmemP1Pipe<NQV, NQE, W, GEO>;
-        auto pk = dgb::v2::assemble_p1_pipe_kernel<NQV, NQE, W, GEO>;
+        auto pk = dgb::v2::assemble_p1_pipe_kernel<NQV, NQE, W, GEO, SRC>;
         dgb::ensure_dynamic_smem(reinterpret_cast<const void*>(pk), PS::kBytes, "cudaFuncSetAttribute(p1 pipe)");
         const int n_chunks = (out_row_end - out_row_begin + 31) / 32;
         cfg.gridDim = dim3(std::max(1, std::min(plan->sm_count, (n_chunks + W - 1) / W)), nb);
@@ -1600,10 +1667,18 @@ void launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_prob
       // 12 warps per CTA (one CTA per SM) at 166 registers.  Registers are allocated per SM
       // sub-partition, so 13-15 warps get 128 like 16; 16 warps spilled and measured slower
       // (1.103 vs 1.073 ms) and was removed.
+      // (the kernel with the geometry record is specialised by source family: only that family's
+      // point loop is compiled in)
+      using W12 = std::integral_constant<int, 12>;
       if (P.geo) {
-        launch(std::integral_constant<int, 12>{}, std::true_type{});
+        switch (dgb::source_only(problem->source)) {
+          case dgb::SRC_CONST: launch(W12{}, std::true_type{}, std::integral_constant<int, dgb::SRC_CONST>{}); break;
+          case dgb::SRC_SIN_SIN: launch(W12{}, std::true_type{}, std::integral_constant<int, dgb::SRC_SIN_SIN>{}); break;
+          case dgb::SRC_GAUSSIAN: launch(W12{}, std::true_type{}, std::integral_constant<int, dgb::SRC_GAUSSIAN>{}); break;
+          default: launch(W12{}, std::true_type{}, std::integral_constant<int, dgb::SRC_ANY>{}); break;
+        }
       } else {
-        launch(std::integral_constant<int, 12>{}, std::false_type{});
+        launch(W12{}, std::false_type{}, std::integral_constant<int, dgb::SRC_ANY>{});
       }
       return;
     }
