@@ -340,12 +340,13 @@ enum dgb_plan_option {
   DGB_OPTION_L2_CARVEOUT_MB = 7, /* cap (MiB) on the persisting-L2 carve-out that L2 policy bits
                                     0 / 2 set up at bind time; 0 = the node array (tuning) */
   DGB_OPTION_GEOMETRY_CACHE = 8, /* P1 persistent kernel (default 1): dgb_plan_bind_mesh also
-                                    copies the bound rows' vertex coordinates (own vertices and
-                                    the neighbours' opposite vertices, 96 B per element, in
-                                    32-row chunks) so that an assembly reads them with coalesced
-                                    16-byte copies instead of six random gathers per element;
-                                    0 = gather from mesh->nodes at every assembly.  With 1,
-                                    rebind after changing mesh->nodes */
+                                    builds the bound rows' geometry record (own vertices, per
+                                    edge the neighbour's G^T n and 1/h, 1/det; 128 B per
+                                    element, in 32-row chunks) so that an assembly reads its
+                                    geometry with coalesced 16-byte copies: no node gathers,
+                                    reciprocals or neighbour Jacobians per assembly (same
+                                    values, bitwise); 0 = gather from mesh->nodes at every
+                                    assembly.  With 1, rebind after changing mesh->nodes */
   DGB_OPTION_PROFILE_ABLATE = 1000 /* DIAGNOSTICS ONLY -- RESULTS ARE WRONG while nonzero: skip
                                       kernel parts to attribute time (bits: 1 block stores,
                                       2 source evaluation, 4 neighbour blocks, 8 diagonal
@@ -355,11 +356,11 @@ int dgb_plan_set_option(dgb_plan* plan, int32_t option, int32_t value);
 
 /* Binds block rows [row_begin, row_end) of `mesh` (DEVICE arrays) to the plan, computing once
  * (on `stream`) what depends only on the mesh: the BSR row_ptr (count + scan) and an element
- * adjacency record (neighbour per local edge, its vertex opposite the shared edge, edge kinds;
- * 32 B per element).  Later dgb_assemble / dgb_assemble_rows calls on the same mesh arrays and
+ * adjacency record (neighbour per local edge, its vertex opposite the shared edge, edge kinds,
+ * orientations and block slots; 32 B per element).  Later dgb_assemble / dgb_assemble_rows calls on the same mesh arrays and
  * rows run as one kernel that reads the record with coalesced loads instead of the dependent
  * element_edges -> edge_elements -> elements gathers, and copy the bound row_ptr into their
- * output.  For P1 the bind also copies the rows' vertex coordinates (DGB_OPTION_GEOMETRY_CACHE).
+ * output.  For P1 the bind also builds the rows' geometry record (DGB_OPTION_GEOMETRY_CACHE).
  * Rebind (or unbind) if elements / element_edges / edge_kind / edge_elements change, or, for
  * P1, if the node coordinates change (a plan bound to another `nodes` pointer gathers from
  * mesh->nodes as before). */

@@ -419,3 +419,50 @@ def test_p1_persistent_kernel_equals_one_shot(oracle, rows):
         rp, col, val, rhs = oracle.assemble(mesh.arrays(), ref.tables(), spec.c, params)
         assert np.array_equal(base[0], rp) and np.array_equal(base[1], col)
         assert np.abs(got["pipe12"][2] - val).max() <= 1e-12 * np.abs(val).max()
+
+
+P1_SOURCES = {
+    "constant": lambda: problems.constant(1.5),
+    "sine": lambda: problems.source_of(capi.FN_SIN_SIN, (1.0,), alpha=1.0, eps=0.05, bx=0.8, by=-0.3),
+    "gaussian": lambda: problems.source_of(capi.FN_GAUSSIAN, (50.0, 0.5, 0.5), alpha=1.0, eps=0.05,
+                                           bx=0.8, by=-0.3),
+    "tanh": lambda: problems.source_of(capi.FN_TANH_LAYER, (1.0, -1.0, -0.25, 0.1), alpha=1.0, eps=0.05,
+                                       bx=0.8, by=-0.3),
+}
+P1_DIRICHLET = {
+    "constant": lambda: problems.constant(0.25),
+    "sine": lambda: problems.function(capi.FN_SIN_SIN, (1.0,)),
+    "gaussian": lambda: problems.function(capi.FN_GAUSSIAN, (50.0, 0.5, 0.5)),
+    "tanh": lambda: problems.function(capi.FN_TANH_LAYER, (1.0, -1.0, -0.25, 0.1)),
+}
+
+
+@pytest.mark.parametrize("family", sorted(P1_SOURCES))
+def test_p1_bound_kernel_every_source_family(oracle, family):
+    """The persistent P1 kernel is compiled once per source family (constant / per-element, sine
+    product, Gaussian, any other) and reads its geometry from the record bound per chunk; boundary
+    data go through the branch-free cores.  Every instantiation, with the geometry record, with
+    the node gathers (DGB_OPTION_GEOMETRY_CACHE 0) and unbound, against the oracle with the
+    per-row comparator -- jittered permuted mesh, Neumann sides, per-element eps and alpha."""
+    import torch
+    cfg = problems.CONFIGS[1]
+    mesh = dgfem.unit_square_mesh(37, 0.2, 21, True, 22, 2)
+    ref = dgfem.ReferenceElement(cfg.degree, cfg.quad_order)
+    spec = problems.make_problem("p1-" + family, 0.05, problems.vec_constant(0.8, -0.3), 1.0,
+                                 P1_SOURCES[family](), P1_DIRICHLET[family](), neumann_sides=2)
+    r = problems.uniform01(4242, 2 * mesh.n_elements)
+    spec.set_per_element("diffusion", 10.0 ** (-3.0 + 3.0 * r[:mesh.n_elements]))
+    spec.set_per_element("linear_reaction", 2.0 * r[mesh.n_elements:])
+    params = dgfem.set_parameters(capi.SIPG, cfg.degree, capi.INFLOW_DROP)
+    want = oracle.assemble(mesh.arrays(), ref.tables(), spec.c, params)
+    got = {}
+    for key, geo, bind in (("record", 1, True), ("gathers", 0, True), ("unbound", 1, False)):
+        a = shard.ShardAssembler(mesh, ref, spec, 0, 0, mesh.n_elements, bind=False)
+        a.plan.set_option(capi.OPTION_GEOMETRY_CACHE, geo)
+        if bind:
+            a.plan.bind_mesh(a.dmesh, 0, mesh.n_elements)
+        got[key] = to_np(a.assemble(params))
+        torch.cuda.synchronize()
+        compare_system(got[key], want)
+    # the record holds the kernel's own values: interior rows agree bitwise with the gathers
+    np.testing.assert_array_equal(got["record"][2], got["gathers"][2])

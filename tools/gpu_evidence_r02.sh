@@ -8,7 +8,7 @@ python __graft_entry__.py smoke > $O/e2_smoke.log 2>&1; echo "smoke rc=$?" >> $O
 python bench.py > $O/e2_bench.json 2> $O/e2_bench.err
 python bench.py --impl reference > $O/e2_reference.json 2> $O/e2_reference.err
 python bench.py --op spmv > $O/e2_spmv.json 2> $O/e2_spmv.err
-python bench.py --op c1-throughput > $O/e2_c1.json 2> $O/e2_c1.err
+python bench.py --op c1-throughput > $O/e2_c1tp.json 2> $O/e2_c1tp.err
 python bench.py --op nonlinear --config 4 > $O/e2_nl4.json 2> $O/e2_nl4.err
 python bench.py --op solve --config 1 > $O/e2_solve1.json 2> $O/e2_solve1.err
 python bench.py --op mesh > $O/e2_mesh_a.json 2> $O/e2_mesh_a.err
