@@ -344,9 +344,9 @@ enum dgb_plan_option {
                                     edge the neighbour's G^T n and 1/h, 1/det; 128 B per
                                     element, in 32-row chunks) so that an assembly reads its
                                     geometry with coalesced 16-byte copies: no node gathers,
-                                    reciprocals or neighbour Jacobians per assembly (same
-                                    values, bitwise); 0 = gather from mesh->nodes at every
-                                    assembly.  With 1, rebind after changing mesh->nodes */
+                                    reciprocals or neighbour Jacobians per assembly (the same
+                                    expressions; results agree to the last bits); 0 = gather
+                                    from mesh->nodes at every assembly.  With 1, rebind after changing mesh->nodes */
   DGB_OPTION_PROFILE_ABLATE = 1000 /* DIAGNOSTICS ONLY -- RESULTS ARE WRONG while nonzero: skip
                                       kernel parts to attribute time (bits: 1 block stores,
                                       2 source evaluation, 4 neighbour blocks, 8 diagonal

@@ -16,6 +16,16 @@
 #ifndef DGB_P1_BULK_OUT
 #define DGB_P1_BULK_OUT 1
 #endif
+// Where the persistent kernel waits for the previous chunk's bulk copy to have read the staging:
+// before the edge loop, or (p1_late_stage) only before the chunk's first staging store, edge 0's
+// neighbour block being computed into registers first.  Measured same-box on the specialised
+// kernels: the late wait is 6% faster with the sine-product source (config-1 batch 0.138 ->
+// 0.129 ms) and 4% slower with the Gaussian (config 4 0.660 -> 0.689 ms; keeping the blocks in
+// registers across the branch alone costs 1.4% there), so it is chosen per source family;
+// -DDGB_P1_WAIT_IN_EDGE0=0/1 forces it for A/B runs.
+#ifndef DGB_P1_WAIT_IN_EDGE0
+#define DGB_P1_WAIT_IN_EDGE0 -1
+#endif
 // The volume RHS term (the source at the volume points) may run after the copy-out has been
 // issued instead of before the diagonal block (p1_row's kSrcLate).  Measured same-box on the
 // specialised kernels: late is 8% faster with the sine-product source (config-1 batch 0.151 ->
@@ -27,6 +37,10 @@
 
 namespace dgb {
 namespace v2 {
+
+constexpr bool p1_late_stage(int src) {
+  return DGB_P1_WAIT_IN_EDGE0 < 0 ? src == SRC_SIN_SIN : DGB_P1_WAIT_IN_EDGE0 != 0;
+}
 
 template <int NQV, int NQE>
 struct SmemP1 {
@@ -124,13 +138,13 @@ struct VertexExtent {
 // GEO (persistent kernel, bound geometry record): po[l] holds the neighbour's G_f^T n and gx the
 // reciprocals (1 / det, 1 / h_0), (1 / h_1, 1 / h_2); slots, orientations and the block count
 // come from the adjacency word.
-template <int NQV, int NQE, bool BOUND, bool GEO, int SRC, class MID>
+template <int NQV, int NQE, bool BOUND, bool GEO, int SRC, class MID, class STG>
 __device__ __forceinline__ void p1_row(const Params2<3, NQV, NQE, false, true>& P, const double* tr,
                                        int mset, double* stw, double* srhs, int lane, int e_first,
                                        int ee, bool active, const int (&v)[3], int4 anb, int4 aop,
                                        int rp, int rp_next, const double2 (&pv)[3],
                                        const double2 (&po)[3], const double2 (&gx)[2], bool wait_stage,
-                                       MID&& mid) {
+                                       MID&& mid, STG&& before_stage) {
   constexpr int NL = 3, N2 = 9;
   using L = Lay<NL, NQV, NQE, false, true>;
   using SM = SmemP1<NQV, NQE>;
@@ -278,6 +292,8 @@ __device__ __forceinline__ void p1_row(const Params2<3, NQV, NQE, false, true>& 
     const double ge0 = G00 * nx + G10 * ny, ge1 = G01 * nx + G11 * ny;
     const int kind = kindv[l], lf = lfv[l], f = fv[l];
     double w0 = 0.0, w1 = 0.0, cp = 0.0;
+    double rr[N2];  // (p1_late_stage) the neighbour block of an interior edge, staged after the branch
+    bool have_block = false;
     if (kind == DGB_EDGE_INTERIOR) {
       double2 gn;  // G_f^T n of the neighbour
       if constexpr (GEO) {
@@ -338,6 +354,7 @@ __device__ __forceinline__ void p1_row(const Params2<3, NQV, NQE, false, true>& 
           b1[p][j] = fma(cV, fr, fma(uY0, g0, uY1 * g1));
         }
       }
+      have_block = true;
       double* blk = myrow + slot_of[1 + l] * N2;
 #pragma unroll
       for (int i = 0; i < NL; ++i) {
@@ -353,7 +370,10 @@ __device__ __forceinline__ void p1_row(const Params2<3, NQV, NQE, false, true>& 
           for (int j = 0; j < NL; ++j) r[j] = fma(ph, b1[p][j], fma(a2, pm[p][j], r[j]));
         }
 #pragma unroll
-        for (int j = 0; j < NL; ++j) if (active) blk[i * NL + j] = r[j];
+        for (int j = 0; j < NL; ++j) {
+          if constexpr (p1_late_stage(SRC)) rr[i * NL + j] = r[j];
+          else if (active) blk[i * NL + j] = r[j];
+        }
       }
       }
     } else {
@@ -410,6 +430,16 @@ __device__ __forceinline__ void p1_row(const Params2<3, NQV, NQE, false, true>& 
                      fma(h0, P.t.x[L::EDPHI + ((l * NQE + p) * 2) * NL + i],
                          fma(h1, P.t.x[L::EDPHI + ((l * NQE + p) * 2 + 1) * NL + i], F[i])));
         }
+      }
+    }
+    // (convergent again) the first staging store of the chunk: the persistent kernel waits here
+    // for the previous chunk's bulk copy to have read the staging
+    if constexpr (p1_late_stage(SRC)) {
+      if (l == 0) before_stage();
+      if (have_block && active) {
+        double* blk = myrow + slot_of[1 + l] * N2;
+#pragma unroll
+        for (int k = 0; k < N2; ++k) blk[k] = rr[k];
       }
     }
     // face terms of the diagonal block (the general kernel's order: W then P, per edge)
@@ -531,7 +561,7 @@ __global__ void __launch_bounds__(THREADS, MINB) assemble_p1_kernel(
   const double2 gx[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
   p1_row<NQV, NQE, BOUND, false, SRC_ANY>(P, tr, mset, stw, DGB_ABLATE(128) ? srhs : nullptr, lane,
                                  blockIdx.x * blockDim.x + warp * 32, ee, active, v, anb, aop, rp, rp_next, pv,
-                                 po, gx, false, [] {});
+                                 po, gx, false, [] {}, [] {});
   if (lane == 0) bulk_wait_all();
 }
 
@@ -672,7 +702,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) assemble_p1_pipe_kernel(
     const int ee = active ? e : P.row_end - 1;
     p1_row<NQV, NQE, true, GEO, SRC>(P, tr, mset, stw, srhs, lane, e_first, ee, active, v, anb, aop, rp,
                                 rp_next, pv, po, gx, true, [&] {
-                                  if constexpr (DGB_P1_BULK_OUT != 0) {
+                                  if constexpr (DGB_P1_BULK_OUT != 0 && !p1_late_stage(SRC)) {
                                     // the previous chunk's row range has left the staging (its bulk
                                     // copy was issued a whole volume phase ago)
                                     if (lane == 0) bulk_wait_read();
@@ -683,6 +713,11 @@ __global__ void __launch_bounds__(WARPS * 32, 1) assemble_p1_pipe_kernel(
                                       cp_async_wait_all();  // the next chunk's records
                                       issue_nodes();
                                     }
+                                  }
+                                }, [&] {
+                                  if constexpr (DGB_P1_BULK_OUT != 0 && p1_late_stage(SRC)) {
+                                    if (lane == 0) bulk_wait_read();
+                                    __syncwarp();
                                   }
                                 });
     c_cur = c_next;

@@ -579,7 +579,8 @@ __global__ void adjacency_kernel(const int32_t* __restrict__ elements,
 // The block-row kernel then reads its geometry with coalesced 16-byte copies: no random node
 // gathers, no reciprocals or reciprocal square roots, no neighbour Jacobians.  The values come
 // from the same device functions the kernels without a record use (p1_edge_frame,
-// p1_neighbour_normal), so results are bitwise the same.  Lanes past the last row repeat it.
+// p1_neighbour_normal); results agree to the last bits (each kernel instantiation has its own
+// FMA contraction).  Lanes past the last row repeat it.
 __global__ void geometry_kernel(const double* __restrict__ nodes, const int32_t* __restrict__ elements,
                                 const int4* __restrict__ nb, const int4* __restrict__ op,
                                 int32_t begin, int32_t n, double2* __restrict__ geo) {
