@@ -511,7 +511,8 @@ def run_e2e(args, mesh, ref, spec, params, device):
     b = Bsr()
     b.n_block_rows, b.block_dim, b.nnzb = E, nl, nnzb
     b.row_ptr, b.col, b.val = rp.data_ptr(), col.data_ptr(), val.data_ptr()
-    h2d = sum(t.numel() * t.element_size() for t in pinned.values()) + sum(
+    # (dgb_assemble_all_host uploads every mesh array except `edges`, which no device code reads)
+    h2d = sum(t.numel() * t.element_size() for k, t in pinned.items() if k != "edges") + sum(
         t.numel() * t.element_size() for t in keep)
     d2h = rp.numel() * 4 + col.numel() * 4 + val.numel() * 8 + rhs.numel() * 8
 
@@ -650,6 +651,10 @@ def run_nonlinear(args, world, rank, local):
     dm = dgfem.DeviceMesh(mesh, local)
     coef = torch.from_numpy(coef_np).cuda(local)
     stream = torch.cuda.current_stream(local)
+    if cfg.degree == 1:
+        # P1: the plan bound to the mesh (as for the assembly): the kernel reads the vertices from
+        # the bound geometry record instead of gathering nodes
+        plan.bind_mesh(dm)
     h, hj = plan.assemble_nonlinear(dm, coef, capi.REACTION_SQUARE, stream=stream)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=f"cuda:{local}")
 

@@ -2382,7 +2382,7 @@ int dgb_assemble_all_host(const dgb_mesh_arrays* mesh, const dgb_reference_table
     dgb_mesh_arrays dm = *mesh;
     dm.nodes = static_cast<const double*>(up(mesh->nodes, sizeof(double) * 2 * nn));
     dm.elements = static_cast<const int32_t*>(up(mesh->elements, sizeof(int32_t) * 3 * E));
-    dm.edges = static_cast<const int32_t*>(up(mesh->edges, sizeof(int32_t) * 2 * ne));
+    dm.edges = nullptr;  // (the sorted vertex pairs: no device code reads them, so they stay on the host)
     dm.edge_kind = static_cast<const uint8_t*>(up(mesh->edge_kind, ne));
     dm.edge_elements = static_cast<const int32_t*>(up(mesh->edge_elements, sizeof(int32_t) * 2 * ne));
     dm.element_edges = static_cast<const int32_t*>(up(mesh->element_edges, sizeof(int32_t) * 3 * E));
@@ -2458,6 +2458,10 @@ int dgb_assemble_nonlinear(dgb_plan* plan, const dgb_mesh_arrays* mesh, const do
     dgb::nlr::NlParams P;
     P.nodes = mesh->nodes;
     P.elements = mesh->elements;
+    // a plan bound to all rows of this mesh (P1: dgb_plan_bind_mesh builds the geometry record)
+    P.geo = (plan->d_geo && plan->geo_cache > 0 && plan->bound_nodes == mesh->nodes &&
+             plan->bound_elements == mesh->elements && plan->bound_begin == 0 && plan->bound_end == E)
+                ? plan->d_geo : nullptr;
     P.coef = coef;
     P.phi = plan->d_tens + plan->L.PHI;
     P.w = plan->d_tens + plan->L.VW;

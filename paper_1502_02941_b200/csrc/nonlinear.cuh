@@ -37,6 +37,7 @@ __device__ __forceinline__ void reaction(int kind, double u, double& r, double& 
 struct NlParams {
   const double* nodes;
   const int32_t* elements;
+  const double2* geo;   // the plan's bound geometry record [chunk][8][32] (dg_assembly.cu), or null
   const double* coef;
   const double* phi;    // [nq][nl]
   const double* w;      // [nq]
@@ -72,12 +73,20 @@ __global__ void __launch_bounds__(128) nonlinear_kernel(const __grid_constant__ 
   if (e0 >= P.n_elements) return;  // whole warp past the end (warp-uniform)
 
   // element_geometry's det, unfused (mesh.cpp:212-230)
-  int v[3];
-#pragma unroll
-  for (int k = 0; k < 3; ++k) v[k] = __ldg(P.elements + 3 * ee + k);
   double2 pv[3];
+  if (P.geo) {
+    // the vertices from the record bound with the mesh (copies of the nodes, coalesced): no
+    // connectivity read, no random node gathers
+    const double2* g = P.geo + static_cast<size_t>(e0 >> 5) * (8 * 32) + lane;
 #pragma unroll
-  for (int k = 0; k < 3; ++k) pv[k] = __ldg(reinterpret_cast<const double2*>(P.nodes) + v[k]);
+    for (int k = 0; k < 3; ++k) pv[k] = __ldg(g + k * 32);
+  } else {
+    int v[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) v[k] = __ldg(P.elements + 3 * ee + k);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) pv[k] = __ldg(reinterpret_cast<const double2*>(P.nodes) + v[k]);
+  }
   const double B00 = __dsub_rn(pv[1].x, pv[0].x), B01 = __dsub_rn(pv[2].x, pv[0].x);
   const double B10 = __dsub_rn(pv[1].y, pv[0].y), B11 = __dsub_rn(pv[2].y, pv[0].y);
   const double det = __dsub_rn(__dmul_rn(B00, B11), __dmul_rn(B01, B10));

@@ -111,3 +111,25 @@ def test_jacobian_matches_finite_differences():
         assert np.all(np.abs(col - fd[rows]) <= 1e-6 * np.maximum(1.0, np.abs(fd[rows])))
         others = np.delete(fd, np.arange(e * nl, (e + 1) * nl))
         assert np.abs(others).max() <= 1e-6
+
+
+def test_bound_plan_reads_the_geometry_record():
+    """P1 plan bound to the mesh (dgb_plan_bind_mesh builds the geometry record): the nonlinear
+    kernel takes the vertices from the record instead of gathering nodes -- copies of the same
+    coordinates, so H and HJ are bitwise what the unbound plan gives (ragged last chunk, jittered
+    permuted mesh); a plan bound to a row shard keeps gathering."""
+    import torch
+    mesh = dgfem.unit_square_mesh(29, 0.2, 5, True, 6, 0)
+    ref = dgfem.ReferenceElement(1)
+    n = mesh.n_elements * ref.n_local
+    coef = torch.from_numpy(2.0 * problems.uniform01(99, n) - 1.0).cuda()
+    dm = dgfem.DeviceMesh(mesh)
+    plan = dgfem.Plan(ref.view)
+    h0, hj0 = plan.assemble_nonlinear(dm, coef, capi.REACTION_CUBIC)
+    torch.cuda.synchronize()
+    h0, v0 = h0.clone(), hj0.val.clone()
+    for rows in ((0, mesh.n_elements), (0, mesh.n_elements // 2)):
+        plan.bind_mesh(dm, *rows)
+        h1, hj1 = plan.assemble_nonlinear(dm, coef, capi.REACTION_CUBIC)
+        torch.cuda.synchronize()
+        assert torch.equal(h0, h1) and torch.equal(v0, hj1.val)
