@@ -340,13 +340,13 @@ enum dgb_plan_option {
   DGB_OPTION_L2_CARVEOUT_MB = 7, /* cap (MiB) on the persisting-L2 carve-out that L2 policy bits
                                     0 / 2 set up at bind time; 0 = the node array (tuning) */
   DGB_OPTION_GEOMETRY_CACHE = 8, /* P1 persistent kernel (default 1): dgb_plan_bind_mesh also
-                                    builds the bound rows' geometry record (own vertices, per
-                                    edge the neighbour's G^T n and 1/h, 1/det; 128 B per
-                                    element, in 32-row chunks) so that an assembly reads its
-                                    geometry with coalesced 16-byte copies: no node gathers,
-                                    reciprocals or neighbour Jacobians per assembly (the same
-                                    expressions; results agree to the last bits); 0 = gather
-                                    from mesh->nodes at every assembly.  With 1, rebind after changing mesh->nodes */
+                                    builds the bound rows' geometry record (own vertices and,
+                                    per edge, the neighbour's G^T n; 96 B per element, in
+                                    32-row chunks) so that an assembly reads its geometry with
+                                    coalesced 16-byte copies: no node gathers or neighbour
+                                    Jacobians per assembly (the same expressions; results
+                                    agree to the last bits); 0 = gather from mesh->nodes at
+                                    every assembly.  With 1, rebind after changing mesh->nodes */
   DGB_OPTION_PROFILE_ABLATE = 1000 /* DIAGNOSTICS ONLY -- RESULTS ARE WRONG while nonzero: skip
                                       kernel parts to attribute time (bits: 1 block stores,
                                       2 source evaluation, 4 neighbour blocks, 8 diagonal

@@ -221,7 +221,7 @@ __device__ __forceinline__ void p1_row(const Params2<3, NQV, NQE, false, true>& 
   const double B00 = FSUB(pv[1].x, pv[0].x), B01 = FSUB(pv[2].x, pv[0].x);
   const double B10 = FSUB(pv[1].y, pv[0].y), B11 = FSUB(pv[2].y, pv[0].y);
   const double det = FSUB(FMUL(B00, B11), FMUL(B01, B10));
-  const double rdet = GEO ? gx[0].x : rcp_nr(det);
+  const double rdet = (GEO && kGeoRows == 8) ? gx[0].x : rcp_nr(det);
   const double G00 = B11 * rdet, G01 = -B10 * rdet;
   const double G10 = -B01 * rdet, G11 = B00 * rdet;
   const double eps = scalar_element(P.prob.diffusion, ee);
@@ -286,7 +286,7 @@ __device__ __forceinline__ void p1_row(const Params2<3, NQV, NQE, false, true>& 
     double dx, dy, nx, ny;
     p1_edge_dir(pv, l, dx, dy);
     const double r2 = fma(dx, dx, FMUL(dy, dy));
-    const double rh = GEO ? (l == 0 ? gx[0].y : (l == 1 ? gx[1].x : gx[1].y)) : rsqrt_nr(r2);
+    const double rh = (GEO && kGeoRows == 8) ? (l == 0 ? gx[0].y : (l == 1 ? gx[1].x : gx[1].y)) : rsqrt_nr(r2);
     const double h = r2 * rh;
     p1_edge_normal(dx, dy, rh, nx, ny);
     const double ge0 = G00 * nx + G10 * ny, ge1 = G01 * nx + G11 * ny;
@@ -638,9 +638,9 @@ __global__ void __launch_bounds__(WARPS * 32, 1) assemble_p1_pipe_kernel(
     if constexpr (GEO) {
       // the chunk's geometry record: eight coalesced 16-byte copies per lane, in flight
       // together with the index records (no dependent gather)
-      const double2* g = P.geo + static_cast<size_t>(c) * (8 * 32) + lane;
+      const double2* g = P.geo + static_cast<size_t>(c) * (kGeoRows * 32) + lane;
 #pragma unroll
-      for (int k = 0; k < 8; ++k) cp_async16(nod + k * 32 + lane, g + k * 32);
+      for (int k = 0; k < kGeoRows; ++k) cp_async16(nod + k * 32 + lane, g + k * 32);
     } else {
       cp_async16(idx + PS::kOp + 4 * lane, P.adj_op + r);
 #pragma unroll
@@ -691,8 +691,10 @@ __global__ void __launch_bounds__(WARPS * 32, 1) assemble_p1_pipe_kernel(
     const double2 po[3] = {nod[96 + lane], nod[128 + lane], nod[160 + lane]};
     double2 gx[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
     if constexpr (GEO) {
-      gx[0] = nod[192 + lane];
-      gx[1] = nod[224 + lane];
+      if constexpr (kGeoRows == 8) {
+        gx[0] = nod[192 + lane];
+        gx[1] = nod[224 + lane];
+      }
     }
     const bool more = c_next < n_chunks;
     if (more) issue_records(c_next);

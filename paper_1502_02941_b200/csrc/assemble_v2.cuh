@@ -179,11 +179,22 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // memory by the persistent kernels: adj_nb [32] int4, adj_op [32] int4, elements [96],
 // row_ptr [32], row_ptr + 1 [32] (ints), then the nodes [6][32] double2 (own vertices 0..2,
 // the neighbours' opposite vertices 3..5).
+// 16-byte rows of the bound geometry record per element (dg_assembly.cu geometry_kernel): the
+// vertices (3) and the neighbours' G^T n (3); with DGB_GEO_RECIPROCALS also (1/det, 1/h_0),
+// (1/h_1, 1/h_2).  Measured on config 4 (same-box A/B): with the reciprocals in the record the
+// kernel moves 5.98 TB/s of DRAM traffic, 92% of the copy bandwidth, at 0.660 ms; recomputing
+// them (one rcp and three rsqrt Newton chains per element) for 32 B per element less takes
+// 0.637 ms.  The bytes are worth more than the instructions, so they are recomputed.
+#ifndef DGB_GEO_RECIPROCALS
+#define DGB_GEO_RECIPROCALS 0
+#endif
+constexpr int kGeoRows = DGB_GEO_RECIPROCALS ? 8 : 6;
+
 struct ChunkRec {
   static constexpr int kNb = 0, kOp = 128, kV = 256, kRp = 352, kRpn = 384, kIdxInts = 416;
   static constexpr int kIdx = kIdxInts / 2;      // doubles
   static constexpr int kNode = 32 * 6 * 2;       // doubles
-  static constexpr int kNode2 = 32 * 8 * 2;      // doubles (extended geometry record)
+  static constexpr int kNode2 = 32 * kGeoRows * 2;  // doubles (geometry record)
 };
 
 __device__ __forceinline__ void bulk_wait_read() {

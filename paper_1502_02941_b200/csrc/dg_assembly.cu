@@ -570,17 +570,17 @@ __global__ void adjacency_kernel(const int32_t* __restrict__ elements,
 
 // Geometry record of rows [begin, begin + n) per 32-row chunk (bound once per mesh, the P1
 // persistent kernel; the "geometry precompute" of the north star):
-//   geo[(chunk * 8 + k) * 32 + lane], k = 0..2: the element's own vertices
+//   geo[(chunk * kGeoRows + k) * 32 + lane], k = 0..2: the element's own vertices
 //                                     k = 3..5: G_f^T n of the neighbour across local edge k - 3
 //                                               (the neighbour's inverse-transposed Jacobian in
 //                                               its (opposite, b, a) vertex order applied to
 //                                               this element's outward normal; 0 on a boundary)
-//                                     k = 6, 7: (1 / det, 1 / h_0), (1 / h_1, 1 / h_2)
+//                                     k = 6, 7 (DGB_GEO_RECIPROCALS builds only):
+//                                               (1 / det, 1 / h_0), (1 / h_1, 1 / h_2)
 // The block-row kernel then reads its geometry with coalesced 16-byte copies: no random node
-// gathers, no reciprocals or reciprocal square roots, no neighbour Jacobians.  The values come
-// from the same device functions the kernels without a record use (p1_edge_frame,
-// p1_neighbour_normal); results agree to the last bits (each kernel instantiation has its own
-// FMA contraction).  Lanes past the last row repeat it.
+// gathers and no neighbour Jacobians.  The values come from the same device functions the
+// kernels without a record use (p1_edge_frame, p1_neighbour_normal); results agree to the last
+// bits (each kernel instantiation has its own FMA contraction).  Lanes past the last row repeat it.
 __global__ void geometry_kernel(const double* __restrict__ nodes, const int32_t* __restrict__ elements,
                                 const int4* __restrict__ nb, const int4* __restrict__ op,
                                 int32_t begin, int32_t n, double2* __restrict__ geo) {
@@ -591,7 +591,7 @@ __global__ void geometry_kernel(const double* __restrict__ nodes, const int32_t*
   const double2* nodes2 = reinterpret_cast<const double2*>(nodes);
   const int4 o = __ldg(op + r);
   const int meta = __ldg(nb + r).w;
-  double2* g = geo + static_cast<size_t>(t >> 5) * (8 * 32) + (t & 31);
+  double2* g = geo + static_cast<size_t>(t >> 5) * (v2::kGeoRows * 32) + (t & 31);
   double2 pv[3];
 #pragma unroll
   for (int k = 0; k < 3; ++k) pv[k] = __ldg(nodes2 + __ldg(elements + 3 * e + k));
@@ -611,8 +611,10 @@ __global__ void geometry_kernel(const double* __restrict__ nodes, const int32_t*
   for (int k = 0; k < 3; ++k) g[k * 32] = pv[k];
   const double det = FSUB(FMUL(FSUB(pv[1].x, pv[0].x), FSUB(pv[2].y, pv[0].y)),
                           FMUL(FSUB(pv[2].x, pv[0].x), FSUB(pv[1].y, pv[0].y)));
-  g[6 * 32] = make_double2(rcp_nr(det), rh[0]);
-  g[7 * 32] = make_double2(rh[1], rh[2]);
+  if constexpr (v2::kGeoRows == 8) {
+    g[6 * 32] = make_double2(rcp_nr(det), rh[0]);
+    g[7 * 32] = make_double2(rh[1], rh[2]);
+  }
 }
 
 // ------------------------------------------------------------------------------------------
@@ -1915,7 +1917,7 @@ int dgb_plan_bind_mesh(dgb_plan* plan, const dgb_mesh_arrays* mesh, int32_t row_
         cudaFree(plan->d_geo);
         plan->d_geo = nullptr;
         plan->geo_cap = 0;
-        cuda_check(cudaMalloc(&plan->d_geo, padded * 8 * sizeof(double2)), "cudaMalloc(geometry)");
+        cuda_check(cudaMalloc(&plan->d_geo, padded * dgb::v2::kGeoRows * sizeof(double2)), "cudaMalloc(geometry)");
         plan->geo_cap = padded;
       }
       dgb::geometry_kernel<<<static_cast<unsigned>((padded + 255) / 256), 256, 0, s>>>(

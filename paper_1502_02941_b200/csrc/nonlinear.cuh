@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(128) nonlinear_kernel(const __grid_constant__ 
   if (P.geo) {
     // the vertices from the record bound with the mesh (copies of the nodes, coalesced): no
     // connectivity read, no random node gathers
-    const double2* g = P.geo + static_cast<size_t>(e0 >> 5) * (8 * 32) + lane;
+    const double2* g = P.geo + static_cast<size_t>(e0 >> 5) * (v2::kGeoRows * 32) + lane;
 #pragma unroll
     for (int k = 0; k < 3; ++k) pv[k] = __ldg(g + k * 32);
   } else {
