@@ -135,9 +135,9 @@ struct VertexExtent {
 // `mid()` runs between the volume terms and the edge loop (the persistent kernel issues the next
 // chunk's node gathers there).
 // SRC: the source family the kernel is specialised for (source_points' ONLY).
-// GEO (persistent kernel, bound geometry record): po[l] holds the neighbour's G_f^T n and gx the
-// reciprocals (1 / det, 1 / h_0), (1 / h_1, 1 / h_2); slots, orientations and the block count
-// come from the adjacency word.
+// GEO (persistent kernel, bound geometry record): po[l] holds the neighbour's G_f^T n (and, in a
+// DGB_GEO_RECIPROCALS build, gx the reciprocals (1 / det, 1 / h_0), (1 / h_1, 1 / h_2)); slots,
+// orientations and the block count come from the adjacency word.
 template <int NQV, int NQE, bool BOUND, bool GEO, int SRC, class MID, class STG>
 __device__ __forceinline__ void p1_row(const Params2<3, NQV, NQE, false, true>& P, const double* tr,
                                        int mset, double* stw, double* srhs, int lane, int e_first,
@@ -636,7 +636,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) assemble_p1_pipe_kernel(
     const int r = min(e, P.row_end - 1) - P.row_begin;
     cp_async16(idx + PS::kNb + 4 * lane, P.adj_nb + r);
     if constexpr (GEO) {
-      // the chunk's geometry record: eight coalesced 16-byte copies per lane, in flight
+      // the chunk's geometry record: kGeoRows coalesced 16-byte copies per lane, in flight
       // together with the index records (no dependent gather)
       const double2* g = P.geo + static_cast<size_t>(c) * (kGeoRows * 32) + lane;
 #pragma unroll
