@@ -628,7 +628,9 @@ __global__ void __launch_bounds__(WARPS * 32, 1) assemble_p1_pipe_kernel(
 
   const int n_rows = P.row_end - P.row_begin;
   const int n_chunks = (n_rows + 31) >> 5;
-  const int gw = blockIdx.x * WARPS + warp, n_gw = gridDim.x * WARPS;
+  // chunks go warp-major across the CTAs (warp w of CTA b starts at chunk b + w gridDim.x): a
+  // small mesh then spreads over the SMs, one busy warp each, instead of filling a few CTAs
+  const int gw = warp * static_cast<int>(gridDim.x) + static_cast<int>(blockIdx.x), n_gw = gridDim.x * WARPS;
   const double2* nodes2 = reinterpret_cast<const double2*>(P.nodes);
 
   auto issue_records = [&](int c) {

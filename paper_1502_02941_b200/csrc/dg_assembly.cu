@@ -1662,7 +1662,7 @@ void launch_v2(const dgb_plan* plan, const dgb_mesh_arrays* mesh, const dgb_prob
         auto pk = dgb::v2::assemble_p1_pipe_kernel<NQV, NQE, W, GEO, SRC>;
         dgb::ensure_dynamic_smem(reinterpret_cast<const void*>(pk), PS::kBytes, "cudaFuncSetAttribute(p1 pipe)");
         const int n_chunks = (out_row_end - out_row_begin + 31) / 32;
-        cfg.gridDim = dim3(std::max(1, std::min(plan->sm_count, (n_chunks + W - 1) / W)), nb);
+        cfg.gridDim = dim3(std::max(1, std::min(plan->sm_count, n_chunks)), nb);
         cfg.blockDim = dim3(32 * W);
         cfg.dynamicSmemBytes = PS::kBytes;
         cuda_check(cudaLaunchKernelEx(&cfg, pk, P), "cudaLaunchKernelEx(p1 pipe)");
