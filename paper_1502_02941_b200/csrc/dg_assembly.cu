@@ -273,7 +273,6 @@ __device__ __forceinline__ void source_points(const dgb_scalar_field& fs, int e,
                                               USE use, int q_first = 0, int q_step = 1,
                                               EXTENT r2max = EXTENT{}) {
   constexpr bool kAny = ONLY == SRC_ANY;
-  if constexpr (!kAny) skip = false;
   if constexpr (kAny || ONLY == SRC_CONST) {
   if (!kAny || fs.kind == DGB_FIELD_PER_ELEMENT || fs.kind == DGB_FIELD_CONSTANT) {
     const double f = fs.kind == DGB_FIELD_PER_ELEMENT ? __ldg(fs.per_element + e) : fs.value;
